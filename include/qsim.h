@@ -1,0 +1,193 @@
+/*
+ * qsim.h — C-ABI of the B200-native hot path of the partitioned simulator of
+ * arXiv:1802.06952 ("64-qubit quantum circuit simulation", Chen et al. 2018).
+ *
+ * Method (§2.1, Supp. A Eqs. 1-8): every CZ that
+ * crosses the horizontal cut of a rows x cols grid circuit is rewritten as
+ * CZ = P0 (x) I + P1 (x) Z (Eq. 1), splitting the circuit into 2^c
+ * branches ("copies") whose upper and lower half-circuits are independent.
+ * Sampled amplitudes are reconstructed as
+ *     a(x_u, x_l) = sum_b U_b[x_u] * L_b[x_l]
+ * then p = |a|^2 and outcomes are drawn (north-star extension).
+ *
+ * Conventions (bit-exact contract):
+ *  - qubit k = row*cols + col; the full bitstring has qubit 0 as its MSB.
+ *  - upper half = rows [0, cut_row): h_u = cut_row*cols qubits, x_u = top h_u bits;
+ *    lower half = the rest: h_l = n - h_u, x_l = bottom h_l bits; x = (x_u << h_l) | x_l.
+ *  - layer 0 (H on every qubit) is implicit; gate layers are 1..depth.
+ *  - cuts are ordered by (layer, upper qubit); branch b takes bit (b >> (c-1-g)) & 1
+ *    for cut g (first cut = MSB); bit 0 -> P0 on the upper endpoint / I on the lower,
+ *    bit 1 -> P1 / Z (Supp. Eq. 7).
+ *  - gates: SX = X^1/2, SY = Y^1/2 (principal roots), T = diag(1, (1+i)/sqrt2),
+ *    CZ = diag(1,1,1,-1).
+ *
+ * Threading / ownership: one host thread per ctx.  Every input array is a
+ * caller-owned HOST array, read during the call only.  Every output array is a
+ * caller-allocated HOST buffer.  The ctx owns all device memory, events and the
+ * NCCL communicator; qsim_destroy frees them.  One process drives one GPU; for
+ * several GPUs run one process per GPU and join them with qsim_comm_init.
+ *
+ * Errors: every call returns a qsim_status; qsim_last_error() gives a message
+ * that stays valid until the next call on the same ctx.  No C++ exception
+ * crosses the ABI.  Status codes 2/3/4 mirror the exit codes of SPEC S:477.
+ */
+#ifndef QSIM_H
+#define QSIM_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct qsim_ctx qsim_ctx;
+
+typedef enum {
+  QSIM_OK = 0,
+  QSIM_EINVAL = 2,   /* invalid argument / circuit / block                       */
+  QSIM_ENOMEM = 3,   /* device (or host) memory does not fit the plan            */
+  QSIM_ENUMERIC = 4, /* numeric sanity failure (e.g. zero block mass)            */
+  QSIM_ECUDA = 5,    /* CUDA runtime error (includes "no CUDA device")           */
+  QSIM_ENCCL = 6,    /* NCCL error                                               */
+  QSIM_ESTATE = 7    /* call out of order (no circuit, no blocks, not evolved)   */
+} qsim_status;
+
+typedef enum { QSIM_C64 = 0, QSIM_C128 = 1 } qsim_precision;
+
+typedef enum { QSIM_SX = 1, QSIM_SY = 2, QSIM_T = 3, QSIM_CZ = 4 } qsim_kind;
+
+#define QSIM_NO_QUBIT 0xFFFFFFFFu
+
+/* One gate: layer in 1..depth; q1 = QSIM_NO_QUBIT unless kind == QSIM_CZ. */
+typedef struct { uint32_t layer, kind, q0, q1; } qsim_gate;
+
+/* One cut CZ (E_int,t member, Supp. A P:305). */
+typedef struct { uint32_t layer, q_upper, q_lower; } qsim_cut;
+
+/* Counters of the ctx (cumulative since creation or the last qsim_stats_reset). */
+typedef struct {
+  uint64_t kernel_launches;  /* every kernel this library launched                       */
+  uint64_t sweeps;           /* gate-sweep kernel launches (one state pass each)          */
+  uint64_t sweep_states;     /* state passes done by those launches (>= sweeps if batched) */
+  double sweep_bytes;        /* algorithmic bytes of the sweeps: (reads + writes) * amp size */
+  double sweep_ms;           /* summed CUDA-event time of sweep launches (QSIM_OPT_TIME_SWEEPS) */
+  uint64_t timed_sweeps;     /* sweep launches included in sweep_ms                      */
+  double gemm_flops;         /* 8*M*N*K of the reconstruction GEMMs                      */
+  double gemm_ms;            /* CUDA-event time of GEMM launches (QSIM_OPT_TIME_SWEEPS)  */
+  uint64_t branches_evolved; /* branch pairs whose slices were gathered                  */
+} qsim_stats_t;
+
+typedef enum {
+  QSIM_OPT_TIME_SWEEPS = 1, /* 1: bracket each sweep/GEMM launch with CUDA events (default 0) */
+  QSIM_OPT_MODE = 2,        /* 0: auto, 1: flat in-shared-memory per-branch kernel (h <= 12),
+                               2: prefix-shared branch tree of tile sweeps (h >= 13)          */
+  QSIM_OPT_MEM_BUDGET = 3     /* cap in bytes on device memory for half-state buffers (0 = free memory) */
+} qsim_option;
+
+/* Create a context bound to CUDA device `device` (no device call is made until the
+ * first evolve/sample call, so load/partition work on a machine without a GPU).
+ * Errors: EINVAL (bad precision / device < 0), ENOMEM (host). */
+qsim_status qsim_create(qsim_ctx **out, qsim_precision prec, int device);
+void qsim_destroy(qsim_ctx *ctx);
+const char *qsim_last_error(const qsim_ctx *ctx);
+const char *qsim_version(void);
+
+/* Set a qsim_option.  EINVAL on an unknown key or value. */
+qsim_status qsim_set_option(qsim_ctx *ctx, int key, int64_t value);
+
+/* Launch all work on this cudaStream_t (e.g. torch.cuda.current_stream().cuda_stream);
+ * NULL = the ctx's own non-blocking stream (default). */
+qsim_status qsim_set_stream(qsim_ctx *ctx, void *cuda_stream);
+
+/* qsim_load_circuit — the circuit and its bipartition (P:285-311 Supp. A).
+ *  rows, cols: grid (n = rows*cols <= 64);  depth: number of gate layers;
+ *  gates[n_gates]: host array, any order; each qubit at most once per layer;
+ *    CZ only between grid neighbours; single-qubit gates: SX, SY, T.
+ *  cut_row: upper half = rows [0, cut_row); 0 = rows/2.  Both halves must have
+ *    1 <= h <= 32 qubits.
+ *  cut_layers[n_cut_layers]: optional cross-check of the layers holding cut CZs
+ *    (e.g. {7, 8, 15, 16}); NULL = derive.  A mismatch is EINVAL.
+ * Replaces any previous circuit (and drops blocks / accumulated amplitudes). */
+qsim_status qsim_load_circuit(qsim_ctx *ctx, uint32_t rows, uint32_t cols, uint32_t depth,
+                              const qsim_gate *gates, size_t n_gates, uint32_t cut_row,
+                              const uint32_t *cut_layers, size_t n_cut_layers);
+
+/* qsim_partition — branch enumeration (§2.1 P:38 "2^c copies").
+ *  *n_cuts = c, *n_branches = 2^c; cuts (nullable, capacity >= c) receives the cut
+ *  list in branch-bit order.  ESTATE without a circuit; EINVAL if c > 40. */
+qsim_status qsim_partition(qsim_ctx *ctx, uint32_t *n_cuts, uint64_t *n_branches, qsim_cut *cuts);
+
+/* qsim_set_blocks — the sampled index blocks S_u (upper, values < 2^h_u) and S_l
+ * (lower, values < 2^h_l), host uint64 arrays, unique (any order; output follows it).
+ * Zeroes the amplitude accumulator.  EINVAL on out-of-range / duplicate / empty. */
+qsim_status qsim_set_blocks(qsim_ctx *ctx, const uint64_t *upper_block, size_t n_upper,
+                            const uint64_t *lower_block, size_t n_lower);
+
+/* qsim_evolve_range — evolve branches [branch_begin, branch_end) (both halves, prefix-
+ * shared), gather their slices U[b, :] = U_b[S_u], L[b, :] = L_b[S_l] and accumulate
+ * A += U^T L into the device block ("results are finally added to the resultant
+ * vector").  ESTATE without blocks; EINVAL on a bad range; ENOMEM. */
+qsim_status qsim_evolve_range(qsim_ctx *ctx, uint64_t branch_begin, uint64_t branch_end);
+
+/* qsim_evolve_halves — qsim_set_blocks + qsim_evolve_range over this rank's share of
+ * [0, 2^c) (all branches when not joined to a communicator; SURVEY §8(e) sharding). */
+qsim_status qsim_evolve_halves(qsim_ctx *ctx, const uint64_t *upper_block, size_t n_upper,
+                               const uint64_t *lower_block, size_t n_lower);
+
+/* qsim_reset_block — zero the device amplitude accumulator (blocks kept). */
+qsim_status qsim_reset_block(qsim_ctx *ctx);
+
+/* qsim_amplitudes — the reconstructed block a(S_u[i], S_l[j]).
+ *  The blocks passed must equal the ones set (ESTATE otherwise; NULL = the set ones).
+ *  amps: host, n_upper*n_lower complex (float2 for QSIM_C64, double2 for QSIM_C128),
+ *  row-major [i][j].  With a communicator, partial blocks are summed over ranks (NCCL)
+ *  and only rank 0 writes amps (others may pass NULL).  amps == NULL: reduce only. */
+qsim_status qsim_amplitudes(qsim_ctx *ctx, const uint64_t *upper_block, size_t n_upper,
+                            const uint64_t *lower_block, size_t n_lower, void *amps);
+
+/* qsim_sample — p = |a|^2 of the (reduced) block, then n_draws outcomes drawn with
+ * Philox4x32-10 (key = seed) and the two-level inverse CDF of SURVEY §8(c):
+ *  bitstrings: host uint64[n_draws], x = (S_u[i] << h_l) | S_l[j]; NULL = keep on device.
+ *  block_mass: host double (nullable) = W = sum of p over the block.
+ *  ENUMERIC if W == 0.  With a communicator only rank 0 draws and writes outputs. */
+qsim_status qsim_sample(qsim_ctx *ctx, uint64_t seed, size_t n_draws, uint64_t *bitstrings,
+                        double *block_mass);
+
+/* qsim_sample_probs — the same sampler on caller-given probabilities (host double
+ * p[n_upper*n_lower], row-major), for sampler parity tests.  h_lower = shift of the
+ * upper index.  Outputs as qsim_sample.  No circuit needed. */
+qsim_status qsim_sample_probs(qsim_ctx *ctx, const double *p, const uint64_t *upper_block,
+                              size_t n_upper, const uint64_t *lower_block, size_t n_lower,
+                              uint32_t h_lower, uint64_t seed, size_t n_draws,
+                              uint64_t *bitstrings, double *block_mass);
+
+/* qsim_branch_sum — the reconstruction contraction alone (a6): A[i,j] = sum_b U[b,i] L[b,j]
+ * for host slices U[n_branches, n_upper], L[n_branches, n_lower] (complex of the ctx
+ * precision); A: host complex double [n_upper, n_lower].  No circuit needed. */
+qsim_status qsim_branch_sum(qsim_ctx *ctx, const void *U, const void *L, size_t n_branches,
+                            size_t n_upper, size_t n_lower, void *A);
+
+/* qsim_branch_state — one half-state of one branch after the last layer (the leaf of
+ * the branch tree, before gathering), evolved by the same kernels as qsim_evolve_range.
+ *  half: 0 = upper, 1 = lower; out: host, 2^h complex of the ctx precision.
+ *  For spot checks at full size.  ESTATE without circuit. */
+qsim_status qsim_branch_state(qsim_ctx *ctx, int half, uint64_t branch, void *out);
+
+/* Multi-GPU (one process per GPU).  qsim_nccl_unique_id writes 128 bytes
+ * (ncclUniqueId) on rank 0; every rank passes the same bytes to qsim_comm_init. */
+qsim_status qsim_nccl_unique_id(void *out128);
+qsim_status qsim_comm_init(qsim_ctx *ctx, int rank, int world, const void *unique_id128);
+/* This rank's share [*begin, *end) of the 2^c branches (contiguous, prefix aligned). */
+qsim_status qsim_rank_range(qsim_ctx *ctx, uint64_t *begin, uint64_t *end);
+
+/* Counters (see qsim_stats_t).  Synchronises the ctx stream when sweeps are timed. */
+qsim_status qsim_stats(qsim_ctx *ctx, qsim_stats_t *out);
+qsim_status qsim_stats_reset(qsim_ctx *ctx);
+/* Block until all work queued by this ctx has finished. */
+qsim_status qsim_synchronize(qsim_ctx *ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* QSIM_H */

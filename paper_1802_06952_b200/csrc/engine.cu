@@ -1,0 +1,803 @@
+// Engine: device memory plan, prefix-shared branch-tree executor, reconstruction,
+// sampling and the NCCL reduction of partial blocks.
+#include "engine.h"
+
+#include <algorithm>
+#include <cstring>
+#include <functional>
+#include <sstream>
+
+namespace qsim {
+
+// ---------------------------------------------------------------- helpers
+void DevBuf::reserve(size_t n) {
+  if (n <= bytes && ptr) return;
+  release();
+  if (n == 0) return;
+  cudaError_t e = cudaMalloc(&ptr, n);
+  if (e != cudaSuccess) {
+    ptr = nullptr;
+    bytes = 0;
+    (void)cudaGetLastError();
+    std::ostringstream m;
+    m << "cudaMalloc of " << n << " bytes failed: " << cudaGetErrorString(e);
+    throw Error(QSIM_ENOMEM, m.str());
+  }
+  bytes = n;
+}
+
+void DevBuf::release() {
+  if (ptr) cudaFree(ptr);
+  ptr = nullptr;
+  bytes = 0;
+}
+
+void Engine::check(cudaError_t e, const char *what) {
+  if (e != cudaSuccess) {
+    std::ostringstream m;
+    m << what << ": " << cudaGetErrorString(e);
+    throw Error(e == cudaErrorMemoryAllocation ? QSIM_ENOMEM : QSIM_ECUDA, m.str());
+  }
+}
+
+static DiagDev to_dev(const Diag &d, int vs, bool force_active = false) {
+  DiagDev o;
+  o.t1 = d.t1;
+  o.t2 = d.t2;
+  o.zm = d.zm;
+  o.hm = d.hm;
+  o.vm = d.vm;
+  o.pm = d.pm;
+  o.pv = d.pv & d.pm;
+  o.vs = vs >= 32 ? 31 : vs;
+  if (vs >= 32) o.vm = 0;
+  o.ph0 = d.ph0 & 7;
+  o.active = (force_active || !d.identity()) ? 1 : 0;
+  o.scale = d.scale();
+  if (d.allzero) {  // (i & 1) == 2 never holds
+    o.pm = 1;
+    o.pv = 2;
+    o.active = 1;
+  }
+  return o;
+}
+
+// ---------------------------------------------------------------- construction
+Engine::Engine(qsim_precision prec, int device) : prec_(prec), device_(device) {
+  if (prec != QSIM_C64 && prec != QSIM_C128) throw Error(QSIM_EINVAL, "precision must be QSIM_C64 or QSIM_C128");
+  if (device < 0) throw Error(QSIM_EINVAL, "device must be >= 0");
+  c128_ = prec == QSIM_C128;
+  amp_ = c128_ ? 16 : 8;
+}
+
+Engine::~Engine() {
+  if (inited_) {
+    cudaSetDevice(device_);
+    cudaStreamSynchronize(stream_);
+    for (auto &pr : ev_sweep_) {
+      cudaEventDestroy(pr.first);
+      cudaEventDestroy(pr.second);
+    }
+    for (auto &pr : ev_gemm_) {
+      cudaEventDestroy(pr.first);
+      cudaEventDestroy(pr.second);
+    }
+    for (auto e : ev_pool_) cudaEventDestroy(e);
+    for (auto *b : states_) delete b;
+    states_.clear();
+    if (comm_) ncclCommDestroy(comm_);
+    if (own_stream_) cudaStreamDestroy(own_stream_);
+  }
+}
+
+void Engine::ensure_device() {
+  if (inited_) {
+    check(cudaSetDevice(device_), "cudaSetDevice");
+    return;
+  }
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess || n == 0) {
+    (void)cudaGetLastError();
+    throw Error(QSIM_ECUDA, std::string("no CUDA device available: ") +
+                                (e != cudaSuccess ? cudaGetErrorString(e) : "0 devices"));
+  }
+  if (device_ >= n) throw Error(QSIM_EINVAL, "device index out of range");
+  check(cudaSetDevice(device_), "cudaSetDevice");
+  cudaDeviceProp prop;
+  check(cudaGetDeviceProperties(&prop, device_), "cudaGetDeviceProperties");
+  if (prop.major != 10) {
+    std::ostringstream m;
+    m << "this build targets sm_100a (B200); device " << device_ << " is sm_" << prop.major << prop.minor;
+    throw Error(QSIM_ECUDA, m.str());
+  }
+  num_sms_ = prop.multiProcessorCount;
+  check(cudaStreamCreateWithFlags(&own_stream_, cudaStreamNonBlocking), "cudaStreamCreate");
+  if (!stream_) stream_ = own_stream_;
+  check(tile_sweep_setup(&occ1_, &occ2_, c128_), "tile sweep setup");
+  occ1_ = std::max(occ1_, 1);
+  occ2_ = std::max(occ2_, 1);
+  inited_ = true;
+}
+
+void Engine::set_option(int key, int64_t value) {
+  switch (key) {
+    case QSIM_OPT_TIME_SWEEPS:
+      time_sweeps_ = value != 0;
+      return;
+    case QSIM_OPT_MODE:
+      if (value < 0 || value > 2) throw Error(QSIM_EINVAL, "QSIM_OPT_MODE must be 0, 1 or 2");
+      mode_ = (int)value;
+      if (have_circuit_) {
+        for (int h = 0; h < 2; ++h) {
+          half_[h].uploaded = false;
+          compile_plans(half_[h]);
+        }
+      }
+      return;
+    case QSIM_OPT_MEM_BUDGET:
+      if (value < 0) throw Error(QSIM_EINVAL, "memory budget must be >= 0");
+      mem_budget_ = value;
+      return;
+    default:
+      throw Error(QSIM_EINVAL, "unknown option key");
+  }
+}
+
+void Engine::set_stream(void *s) {
+  stream_ = s ? reinterpret_cast<cudaStream_t>(s) : own_stream_;
+}
+
+// ---------------------------------------------------------------- circuit
+void Engine::load_circuit(uint32_t rows, uint32_t cols, uint32_t depth, const qsim_gate *gates,
+                          size_t n_gates, uint32_t cut_row, const uint32_t *cut_layers,
+                          size_t n_cut_layers) {
+  Circuit c;
+  std::string err = build_circuit(rows, cols, depth, gates, n_gates, cut_row, cut_layers, n_cut_layers, c);
+  if (!err.empty()) throw Error(QSIM_EINVAL, err);
+  circ_ = std::move(c);
+  for (int h = 0; h < 2; ++h) {
+    half_[h].prog = compile_half(circ_, h == 0);
+    half_[h].uploaded = false;
+    compile_plans(half_[h]);
+  }
+  have_circuit_ = true;
+  have_blocks_ = false;
+  reduced_ = false;
+}
+
+void Engine::partition(uint32_t *n_cuts, uint64_t *n_branches, qsim_cut *cuts) const {
+  if (!have_circuit_) throw Error(QSIM_ESTATE, "no circuit loaded");
+  const size_t c = circ_.cuts.size();
+  if (c > 63) throw Error(QSIM_EINVAL, "more than 63 cut CZs: 2^c branches do not fit in uint64");
+  if (n_cuts) *n_cuts = (uint32_t)c;
+  if (n_branches) *n_branches = 1ull << c;
+  if (cuts)
+    for (size_t g = 0; g < c; ++g) cuts[g] = circ_.cuts[g];
+}
+
+// Tile plan of every sweep (host only; precision-dependent tile geometry).
+void Engine::compile_plans(HalfExec &he) {
+  const HalfProgram &hp = he.prog;
+  const int L = tile_low_bits(c128_), T = L + kHiBits;
+  const bool can_tree = hp.h >= T, can_small = hp.h <= small_max_h(c128_);
+  if (mode_ == 1)
+    he.tree = false;
+  else if (mode_ == 2)
+    he.tree = true;
+  else
+    he.tree = !can_small;
+  he.plans.clear();
+  if ((he.tree && !can_tree) || (!he.tree && !can_small)) return;  // reported at evolve time
+  if (!he.tree) return;
+  he.plans.resize(hp.levels.size());
+  for (size_t l = 0; l < hp.levels.size(); ++l) {
+    const Level &lev = hp.levels[l];
+    he.plans[l].resize(lev.sweeps.size());
+    for (size_t s = 0; s < lev.sweeps.size(); ++s) {
+      const Sweep &sw = lev.sweeps[s];
+      std::vector<Gate1> low, high;
+      for (auto &g : sw.gates) (g.bit < L ? low : high).push_back(g);
+      const int nchunks = std::max<int>(1, (int)((high.size() + kHiBits - 1) / kHiBits));
+      std::vector<std::vector<Gate1>> chunks(nchunks);
+      for (size_t i = 0; i < high.size(); ++i) chunks[i * nchunks / high.size()].push_back(high[i]);
+      for (int ci = 0; ci < nchunks; ++ci) {
+        TilePlan tp;
+        std::memset(&tp.p, 0, sizeof(tp.p));
+        const auto &H = chunks[ci];
+        std::vector<int> hb;
+        for (auto &g : H) hb.push_back(g.bit);
+        for (int b = L; (int)hb.size() < kHiBits && b < hp.h; ++b)
+          if (std::find(hb.begin(), hb.end(), b) == hb.end()) hb.push_back(b);
+        std::sort(hb.begin(), hb.end());
+        auto idx_of = [&](int bit) { return (int)(std::find(hb.begin(), hb.end(), bit) - hb.begin()); };
+        auto kind_of = [&](int bit) {
+          for (auto &g : H)
+            if (g.bit == bit) return (int)g.kind;
+          return 0;
+        };
+        for (int j = 0; j < kHiBits; ++j) tp.p.hb[j] = (uint8_t)hb[j];
+        tp.npass = H.size() <= 4 ? 1 : 2;
+        std::vector<int> tgt_idx;
+        for (auto &g : H) tgt_idx.push_back(idx_of(g.bit));
+        for (int q = 0; q < tp.npass; ++q) {
+          std::vector<int> regs;
+          const size_t from = q * 4, to = std::min(H.size(), (size_t)(q * 4 + 4));
+          for (size_t i = from; i < to; ++i) regs.push_back(tgt_idx[i]);
+          const size_t ntgt = regs.size();
+          for (int j = 0; j < kHiBits && regs.size() < 4; ++j) {
+            const bool is_tgt = std::find(tgt_idx.begin(), tgt_idx.end(), j) != tgt_idx.end();
+            if (!is_tgt && std::find(regs.begin(), regs.end(), j) == regs.end()) regs.push_back(j);
+          }
+          for (int j = 0; j < kHiBits && regs.size() < 4; ++j)
+            if (std::find(regs.begin(), regs.end(), j) == regs.end()) regs.push_back(j);
+          std::vector<int> warps;
+          for (int j = 0; j < kHiBits; ++j)
+            if (std::find(regs.begin(), regs.end(), j) == regs.end()) warps.push_back(j);
+          for (int s4 = 0; s4 < 4; ++s4) {
+            tp.p.gsel[q][s4] = (uint8_t)regs[s4];
+            tp.p.gkind[q][s4] = (uint8_t)((size_t)s4 < ntgt ? kind_of(hb[regs[s4]]) : 0);
+          }
+          for (int s3 = 0; s3 < 3; ++s3) tp.p.wsel[q][s3] = (uint8_t)warps[s3];
+        }
+        if (ci == 0)
+          for (auto &g : low) tp.p.lowkind[g.bit] = g.kind;
+        // outer runs
+        int nr = 0;
+        for (int b = L; b < hp.h;) {
+          if (std::find(hb.begin(), hb.end(), b) != hb.end()) {
+            ++b;
+            continue;
+          }
+          int e = b;
+          while (e < hp.h && std::find(hb.begin(), hb.end(), e) == hb.end()) ++e;
+          tp.p.run_start[nr] = (uint8_t)b;
+          tp.p.run_len[nr] = (uint8_t)(e - b);
+          ++nr;
+          b = e;
+        }
+        tp.p.nruns = nr;
+        tp.p.log2_ntiles = hp.h - T;
+        tp.use_pre = ci == 0;
+        tp.gen = sw.gen && ci == 0;
+        tp.pre = sw.pre;
+        tp.p.post = to_dev(ci == nchunks - 1 ? sw.post : Diag(), hp.vs);
+        he.plans[l][s].push_back(tp);
+      }
+    }
+  }
+}
+
+void Engine::upload_small(HalfExec &he) {
+  if (he.uploaded) return;
+  const HalfProgram &hp = he.prog;
+  std::vector<SmallLevelDev> levs(hp.levels.size());
+  std::vector<SmallSweepDev> sws;
+  for (size_t l = 0; l < hp.levels.size(); ++l) {
+    const Level &lev = hp.levels[l];
+    SmallLevelDev d;
+    std::memset(&d, 0, sizeof(d));
+    d.k = lev.k;
+    d.first_sweep = (int)sws.size();
+    d.nsweeps = (int)lev.sweeps.size();
+    for (int j = 0; j < lev.k; ++j) d.cut_bits[j] = (uint8_t)lev.cut_bits[j];
+    levs[l] = d;
+    for (auto &sw : lev.sweeps) {
+      SmallSweepDev s;
+      std::memset(&s, 0, sizeof(s));
+      s.pre = to_dev(sw.pre, hp.vs, sw.gen);
+      s.post = to_dev(sw.post, hp.vs);
+      s.gen = sw.gen ? 1 : 0;
+      s.ngates = (int)sw.gates.size();
+      for (size_t g = 0; g < sw.gates.size(); ++g) {
+        s.bit[g] = sw.gates[g].bit;
+        s.kind[g] = sw.gates[g].kind;
+      }
+      sws.push_back(s);
+    }
+  }
+  he.d_levels.reserve(levs.size() * sizeof(SmallLevelDev));
+  he.d_sweeps.reserve(std::max<size_t>(1, sws.size()) * sizeof(SmallSweepDev));
+  check(cudaMemcpyAsync(he.d_levels.ptr, levs.data(), levs.size() * sizeof(SmallLevelDev),
+                        cudaMemcpyHostToDevice, stream_),
+        "upload small program");
+  if (!sws.empty())
+    check(cudaMemcpyAsync(he.d_sweeps.ptr, sws.data(), sws.size() * sizeof(SmallSweepDev),
+                          cudaMemcpyHostToDevice, stream_),
+          "upload small program");
+  check(cudaStreamSynchronize(stream_), "upload small program");
+  he.uploaded = true;
+}
+
+// ---------------------------------------------------------------- blocks
+static void validate_block(const uint64_t *v, size_t n, uint32_t h, const char *name) {
+  if (n == 0 || !v) throw Error(QSIM_EINVAL, std::string(name) + " block is empty");
+  std::vector<uint64_t> s(v, v + n);
+  const uint64_t lim = h >= 64 ? ~0ull : (1ull << h);
+  for (uint64_t x : s)
+    if (x >= lim) {
+      std::ostringstream m;
+      m << name << " block index " << x << " >= 2^" << h;
+      throw Error(QSIM_EINVAL, m.str());
+    }
+  std::sort(s.begin(), s.end());
+  if (std::adjacent_find(s.begin(), s.end()) != s.end())
+    throw Error(QSIM_EINVAL, std::string(name) + " block has duplicate indices");
+}
+
+void Engine::set_blocks(const uint64_t *up, size_t nu, const uint64_t *lo, size_t nl) {
+  if (!have_circuit_) throw Error(QSIM_ESTATE, "no circuit loaded");
+  validate_block(up, nu, circ_.h_u, "upper");
+  validate_block(lo, nl, circ_.h_l, "lower");
+  ensure_device();
+  Su_.assign(up, up + nu);
+  Sl_.assign(lo, lo + nl);
+  d_Su_.reserve(nu * 8);
+  d_Sl_.reserve(nl * 8);
+  check(cudaMemcpyAsync(d_Su_.ptr, up, nu * 8, cudaMemcpyHostToDevice, stream_), "upload S_u");
+  check(cudaMemcpyAsync(d_Sl_.ptr, lo, nl * 8, cudaMemcpyHostToDevice, stream_), "upload S_l");
+  A_acc_.reserve(nu * nl * 16);
+  check(cudaMemsetAsync(A_acc_.ptr, 0, nu * nl * 16, stream_), "zero block");
+  check(cudaStreamSynchronize(stream_), "set_blocks");
+  have_blocks_ = true;
+  reduced_ = false;
+}
+
+void Engine::check_blocks(const uint64_t *up, size_t nu, const uint64_t *lo, size_t nl) const {
+  if (!have_blocks_) throw Error(QSIM_ESTATE, "no blocks set / evolved");
+  if (up && (nu != Su_.size() || !std::equal(Su_.begin(), Su_.end(), up)))
+    throw Error(QSIM_ESTATE, "upper block differs from the evolved one");
+  if (lo && (nl != Sl_.size() || !std::equal(Sl_.begin(), Sl_.end(), lo)))
+    throw Error(QSIM_ESTATE, "lower block differs from the evolved one");
+}
+
+void Engine::reset_block() {
+  if (!have_blocks_) throw Error(QSIM_ESTATE, "no blocks set");
+  ensure_device();
+  check(cudaMemsetAsync(A_acc_.ptr, 0, Su_.size() * Sl_.size() * 16, stream_), "zero block");
+  reduced_ = false;
+}
+
+// ---------------------------------------------------------------- events
+cudaEvent_t Engine::get_event() {
+  if (!ev_pool_.empty()) {
+    cudaEvent_t e = ev_pool_.back();
+    ev_pool_.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  check(cudaEventCreate(&e), "cudaEventCreate");
+  return e;
+}
+
+void Engine::resolve_events() {
+  auto drain = [&](std::vector<std::pair<cudaEvent_t, cudaEvent_t>> &v, double &ms, uint64_t *cnt) {
+    if (v.empty()) return;
+    check(cudaEventSynchronize(v.back().second), "cudaEventSynchronize");
+    for (auto &pr : v) {
+      float t = 0.f;
+      check(cudaEventElapsedTime(&t, pr.first, pr.second), "cudaEventElapsedTime");
+      ms += t;
+      if (cnt) ++*cnt;
+      ev_pool_.push_back(pr.first);
+      ev_pool_.push_back(pr.second);
+    }
+    v.clear();
+  };
+  drain(ev_sweep_, st_.sweep_ms, &st_.timed_sweeps);
+  drain(ev_gemm_, st_.gemm_ms, nullptr);
+}
+
+// ---------------------------------------------------------------- executor
+void Engine::launch_plan(const TilePlan &tp, const Diag &fork, bool first, const void *src, void *dst,
+                         int h) {
+  TileSweepParams p = tp.p;
+  int pre_mode = 0;
+  Diag pre;
+  if (tp.use_pre) {
+    pre = Diag::merge(fork, tp.pre);
+    if (tp.gen)
+      pre_mode = 2;
+    else if (!pre.identity())
+      pre_mode = 1;
+  }
+  const int vs = half_[0].prog.vs;
+  p.pre = to_dev(pre, vs, pre_mode != 0);
+  p.njobs = 1;
+  p.src[0] = tp.gen ? nullptr : src;
+  p.dst[0] = dst;
+  p.job_pv[0] = p.pre.pv;
+  p.job_zm[0] = p.pre.zm;
+  const uint64_t tiles = (1ull << p.log2_ntiles) * (uint64_t)p.njobs;
+  const int occ = tp.npass == 1 ? occ1_ : occ2_;
+  const int grid = (int)std::min<uint64_t>(tiles, (uint64_t)num_sms_ * occ);
+  const bool timed = time_sweeps_;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (timed) {
+    e0 = get_event();
+    e1 = get_event();
+    check(cudaEventRecord(e0, stream_), "cudaEventRecord");
+  }
+  check(launch_tile_sweep(p, c128_, pre_mode, tp.npass, grid, stream_), "tile sweep launch");
+  if (timed) {
+    check(cudaEventRecord(e1, stream_), "cudaEventRecord");
+    ev_sweep_.emplace_back(e0, e1);
+    if (ev_sweep_.size() > 8192) resolve_events();
+  }
+  (void)first;
+  st_.kernel_launches++;
+  st_.sweeps++;
+  st_.sweep_states += (uint64_t)p.njobs;
+  st_.sweep_bytes += (tp.gen ? 1.0 : 2.0) * std::ldexp(1.0, h) * (double)amp_ * p.njobs;
+}
+
+// Runs the sweeps of `level` for fork child `child`; returns where the state ended.
+void Engine::run_level(int half, int level, uint64_t child, const void *src, void *dst) {
+  HalfExec &he = half_[half];
+  const Level &lev = he.prog.levels[level];
+  const Diag fork = he.prog.fork_diag(level, child);
+  for (size_t s = 0; s < lev.sweeps.size(); ++s) {
+    const auto &chunks = he.plans[level][s];
+    for (size_t ci = 0; ci < chunks.size(); ++ci) {
+      const bool first = s == 0 && ci == 0;
+      launch_plan(chunks[ci], first ? fork : Diag(), first, first ? src : dst, dst, he.prog.h);
+    }
+  }
+}
+
+void Engine::gather_leaf(int half, uint64_t child_last, const void *psi, const uint64_t *dS, int64_t nS,
+                         void *out_row) {
+  HalfExec &he = half_[half];
+  const int F = (int)he.prog.levels.size() - 1;
+  Diag pend;
+  if (F >= 1 && he.prog.levels[F].sweeps.empty()) pend = he.prog.fork_diag(F, child_last);
+  check(launch_gather(psi, dS, nS, out_row, to_dev(pend, he.prog.vs), c128_, stream_), "gather launch");
+  st_.kernel_launches++;
+}
+
+int Engine::materialized_from(int half, size_t free_bytes, int *nbuf) {
+  const HalfProgram &hp = half_[half].prog;
+  const int F = (int)hp.levels.size() - 1;
+  size_t budget = free_bytes;
+  if (mem_budget_ > 0) budget = std::min(budget, (size_t)mem_budget_);
+  int m0 = 0;
+  while ((size_t)(F + 1 - m0) * state_bytes_ > budget && m0 < F) ++m0;
+  if ((size_t)(F + 1 - m0) * state_bytes_ > budget) {
+    std::ostringstream m;
+    m << "a " << hp.h << "-qubit half state needs " << state_bytes_ << " bytes; only " << budget
+      << " bytes available for state buffers";
+    throw Error(QSIM_ENOMEM, m.str());
+  }
+  *nbuf = F + 1 - m0;
+  return m0;
+}
+
+void Engine::ensure_states(int half, int nbuf) {
+  (void)half;
+  while ((int)states_.size() < nbuf) states_.push_back(new DevBuf());
+  for (int i = 0; i < nbuf; ++i) states_[i]->reserve(state_bytes_);
+}
+
+void Engine::evolve_half(int half, uint64_t b0, uint64_t b1, void *slice, const uint64_t *dS, int64_t nS) {
+  HalfExec &he = half_[half];
+  const HalfProgram &hp = he.prog;
+  const int c = (int)circ_.cuts.size();
+  if (!he.tree) {
+    if (hp.h > small_max_h(c128_))
+      throw Error(QSIM_EINVAL, "flat (small-state) mode needs h <= 12");
+    upload_small(he);
+    SmallParams sp;
+    sp.levels = he.d_levels.as<SmallLevelDev>();
+    sp.sweeps = he.d_sweeps.as<SmallSweepDev>();
+    sp.nlevels = (int)hp.levels.size();
+    sp.h = hp.h;
+    sp.upper = hp.upper ? 1 : 0;
+    sp.c = c;
+    sp.S = dS;
+    sp.nS = nS;
+    const uint64_t maxb = 1u << 30;
+    for (uint64_t b = b0; b < b1; b += maxb) {
+      const uint64_t nb = std::min(maxb, b1 - b);
+      sp.b0 = b;
+      sp.out = (char *)slice + (b - b0) * (uint64_t)nS * amp_;
+      check(launch_small(sp, c128_, nb, stream_), "small kernel launch");
+      st_.kernel_launches++;
+      st_.sweeps++;
+      st_.sweep_states += nb;
+    }
+    return;
+  }
+  const int T = tile_low_bits(c128_) + kHiBits;
+  if (hp.h < T) throw Error(QSIM_EINVAL, "tree mode needs h >= tile bits");
+  state_bytes_ = ((size_t)1 << hp.h) * amp_;
+  size_t free_b = 0, total_b = 0;
+  check(cudaMemGetInfo(&free_b, &total_b), "cudaMemGetInfo");
+  size_t have = 0;
+  for (auto *b : states_) have += b->bytes;
+  const size_t margin = (size_t)512 << 20;
+  const size_t avail = free_b + have > margin ? free_b + have - margin : 0;
+  int nbuf = 0;
+  const int m0 = materialized_from(half, avail, &nbuf);
+  ensure_states(half, nbuf);
+  const int F = (int)hp.levels.size() - 1;
+  std::vector<int> sbits(F + 1, 0);  // cut bits consumed up to and including level l
+  for (int l = 1; l <= F; ++l) sbits[l] = sbits[l - 1] + hp.levels[l].k;
+  auto buf = [&](int l) { return states_[std::max(l, m0) - m0]->ptr; };
+
+  // recompute levels 0..lt along the path of prefix `cp` in place in buf(m0)
+  auto recompute_path = [&](int lt, uint64_t cp) {
+    void *b = buf(m0);
+    run_level(half, 0, 0, nullptr, b);
+    for (int l = 1; l <= lt; ++l) {
+      const uint64_t ch = (cp >> (sbits[lt] - sbits[l])) & ((1ull << hp.levels[l].k) - 1ull);
+      run_level(half, l, ch, b, b);
+    }
+  };
+
+  std::function<void(int, uint64_t, const void *)> node = [&](int l, uint64_t prefix, const void *state) {
+    if (l == F) {
+      const uint64_t b = prefix;
+      const uint64_t ch = F >= 1 ? (b & ((1ull << hp.levels[F].k) - 1ull)) : 0;
+      gather_leaf(half, ch, state, dS, nS, (char *)slice + (b - b0) * (uint64_t)nS * amp_);
+      return;
+    }
+    const int k = hp.levels[l + 1].k;
+    const int shift = c - sbits[l + 1];
+    for (uint64_t ch = 0; ch < (1ull << k); ++ch) {
+      const uint64_t cp = (prefix << k) | ch;
+      const uint64_t lo = cp << shift, hi = (cp + 1) << shift;
+      if (hi <= b0 || lo >= b1) continue;
+      if (l + 1 < m0) {
+        node(l + 1, cp, nullptr);
+      } else if (l + 1 == m0) {
+        recompute_path(m0, cp);
+        node(m0, cp, buf(m0));
+      } else {
+        void *dst = buf(l + 1);
+        run_level(half, l + 1, ch, state, dst);
+        node(l + 1, cp, hp.levels[l + 1].sweeps.empty() ? state : dst);
+      }
+    }
+  };
+  if (m0 == 0) {
+    run_level(half, 0, 0, nullptr, buf(0));
+    node(0, 0, buf(0));
+  } else {
+    node(0, 0, nullptr);
+  }
+}
+
+void Engine::gemm(const void *U, const void *L, int64_t K, int64_t M, int64_t N, double *A) {
+  const bool timed = time_sweeps_;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (timed) {
+    e0 = get_event();
+    e1 = get_event();
+    check(cudaEventRecord(e0, stream_), "cudaEventRecord");
+  }
+  check(launch_branch_gemm(U, L, K, M, N, A, c128_, stream_), "branch gemm launch");
+  if (timed) {
+    check(cudaEventRecord(e1, stream_), "cudaEventRecord");
+    ev_gemm_.emplace_back(e0, e1);
+  }
+  st_.kernel_launches++;
+  st_.gemm_flops += 8.0 * (double)M * (double)N * (double)K;
+}
+
+void Engine::evolve_range(uint64_t b0, uint64_t b1) {
+  if (!have_circuit_) throw Error(QSIM_ESTATE, "no circuit loaded");
+  if (!have_blocks_) throw Error(QSIM_ESTATE, "no blocks set (qsim_set_blocks)");
+  const int c = (int)circ_.cuts.size();
+  if (c > 62) throw Error(QSIM_EINVAL, "too many cuts");
+  const uint64_t B = 1ull << c;
+  if (b0 >= b1 || b1 > B) throw Error(QSIM_EINVAL, "bad branch range");
+  ensure_device();
+  for (int h = 0; h < 2; ++h) {
+    const HalfExec &he = half_[h];
+    const int T = tile_low_bits(c128_) + kHiBits;
+    if (he.tree && he.prog.h < T) throw Error(QSIM_EINVAL, "tree mode needs h >= 13 (c64) / 12 (c128)");
+    if (!he.tree && he.prog.h > small_max_h(c128_)) throw Error(QSIM_EINVAL, "flat mode needs h <= 12");
+  }
+  const int64_t nu = (int64_t)Su_.size(), nl = (int64_t)Sl_.size();
+  // slices for a chunk of branches (bounded at 1 GiB per half)
+  const uint64_t per_branch = (uint64_t)std::max(nu, nl) * amp_;
+  uint64_t chunk = std::max<uint64_t>(1, ((uint64_t)1 << 30) / per_branch);
+  // align the chunk to a power of two so that chunks are whole subtrees
+  uint64_t p2 = 1;
+  while (p2 * 2 <= chunk) p2 *= 2;
+  chunk = std::min<uint64_t>(p2, b1 - b0);
+  U_.reserve(chunk * nu * amp_);
+  L_.reserve(chunk * nl * amp_);
+  for (uint64_t s = b0; s < b1;) {
+    uint64_t e = std::min(b1, (s / p2 + 1) * p2);
+    e = std::min(e, s + chunk);
+    evolve_half(0, s, e, U_.ptr, d_Su_.as<uint64_t>(), nu);
+    evolve_half(1, s, e, L_.ptr, d_Sl_.as<uint64_t>(), nl);
+    gemm(U_.ptr, L_.ptr, (int64_t)(e - s), nu, nl, A_acc_.as<double>());
+    st_.branches_evolved += e - s;
+    s = e;
+  }
+  check(cudaGetLastError(), "evolve");
+  reduced_ = false;
+}
+
+// ---------------------------------------------------------------- reduction / outputs
+double *Engine::reduced_block() {
+  const size_t n = Su_.size() * Sl_.size();
+  if (world_ == 1) return A_acc_.as<double>();
+  if (!reduced_) {
+    if (rank_ == 0) A_tot_.reserve(n * 16);
+    ncclResult_t r = ncclReduce(A_acc_.ptr, rank_ == 0 ? A_tot_.ptr : nullptr, 2 * n, ncclDouble, ncclSum,
+                                0, comm_, stream_);
+    if (r != ncclSuccess) throw Error(QSIM_ENCCL, std::string("ncclReduce: ") + ncclGetErrorString(r));
+    reduced_ = true;
+  }
+  return rank_ == 0 ? A_tot_.as<double>() : nullptr;
+}
+
+void Engine::amplitudes(void *amps) {
+  if (!have_blocks_) throw Error(QSIM_ESTATE, "no blocks evolved");
+  ensure_device();
+  double *A = reduced_block();
+  const size_t n = Su_.size() * Sl_.size();
+  if (A && amps) {
+    if (c128_) {
+      check(cudaMemcpyAsync(amps, A, n * 16, cudaMemcpyDeviceToHost, stream_), "D2H amplitudes");
+    } else {
+      tmp_.reserve(n * 8);
+      check(launch_cast_c128_to_c64(A, (int64_t)(2 * n), tmp_.as<float>(), stream_), "cast");
+      st_.kernel_launches++;
+      check(cudaMemcpyAsync(amps, tmp_.ptr, n * 8, cudaMemcpyDeviceToHost, stream_), "D2H amplitudes");
+    }
+  }
+  check(cudaStreamSynchronize(stream_), "amplitudes");
+}
+
+void Engine::run_sampler(const double *p, int64_t M, int64_t N, const uint64_t *dSu, const uint64_t *dSl,
+                         uint32_t hl, uint64_t seed, size_t n, uint64_t *out, double *mass) {
+  C_.reserve((size_t)M * N * 8);
+  r_.reserve((size_t)M * 8);
+  R_.reserve((size_t)M * 8);
+  W_.reserve(8);
+  check(launch_row_scan(p, M, N, C_.as<double>(), r_.as<double>(), stream_), "row scan");
+  check(launch_row_prefix(r_.as<double>(), M, R_.as<double>(), W_.as<double>(), stream_), "row prefix");
+  st_.kernel_launches += 2;
+  if (out || mass) {
+    double W = 0;
+    check(cudaMemcpyAsync(&W, W_.ptr, 8, cudaMemcpyDeviceToHost, stream_), "D2H block mass");
+    check(cudaStreamSynchronize(stream_), "sample");
+    if (!(W > 0.0)) throw Error(QSIM_ENUMERIC, "block has zero total probability mass");
+    if (mass) *mass = W;
+  }
+  if (n > 0) {
+    draws_.reserve(n * 8);
+    check(launch_draws(p, C_.as<double>(), r_.as<double>(), R_.as<double>(), W_.as<double>(), M, N, dSu,
+                       dSl, hl, seed, (int64_t)n, draws_.as<uint64_t>(), stream_),
+          "draws");
+    st_.kernel_launches++;
+    if (out) {
+      check(cudaMemcpyAsync(out, draws_.ptr, n * 8, cudaMemcpyDeviceToHost, stream_), "D2H draws");
+      check(cudaStreamSynchronize(stream_), "sample");
+    }
+  }
+}
+
+void Engine::sample(uint64_t seed, size_t n, uint64_t *out, double *mass) {
+  if (!have_blocks_) throw Error(QSIM_ESTATE, "no blocks evolved");
+  ensure_device();
+  double *A = reduced_block();
+  if (!A) {
+    check(cudaStreamSynchronize(stream_), "sample");
+    return;
+  }
+  const int64_t M = (int64_t)Su_.size(), N = (int64_t)Sl_.size();
+  p_.reserve((size_t)M * N * 8);
+  check(launch_abs2(A, M * N, p_.as<double>(), stream_), "abs2");
+  st_.kernel_launches++;
+  run_sampler(p_.as<double>(), M, N, d_Su_.as<uint64_t>(), d_Sl_.as<uint64_t>(), circ_.h_l, seed, n, out,
+              mass);
+}
+
+void Engine::sample_probs(const double *p, const uint64_t *up, size_t nu, const uint64_t *lo, size_t nl,
+                          uint32_t hl, uint64_t seed, size_t n, uint64_t *out, double *mass) {
+  if (!p || !up || !lo || nu == 0 || nl == 0) throw Error(QSIM_EINVAL, "empty probability block");
+  if (hl > 63) throw Error(QSIM_EINVAL, "h_lower must be < 64");
+  for (size_t i = 0; i < nu * nl; ++i)
+    if (!(p[i] >= 0.0)) throw Error(QSIM_EINVAL, "probabilities must be >= 0");
+  ensure_device();
+  p_.reserve(nu * nl * 8);
+  tmp_.reserve((nu + nl) * 8);
+  check(cudaMemcpyAsync(p_.ptr, p, nu * nl * 8, cudaMemcpyHostToDevice, stream_), "upload p");
+  uint64_t *dsu = tmp_.as<uint64_t>(), *dsl = dsu + nu;
+  check(cudaMemcpyAsync(dsu, up, nu * 8, cudaMemcpyHostToDevice, stream_), "upload S_u");
+  check(cudaMemcpyAsync(dsl, lo, nl * 8, cudaMemcpyHostToDevice, stream_), "upload S_l");
+  double W = 0;
+  run_sampler(p_.as<double>(), (int64_t)nu, (int64_t)nl, dsu, dsl, hl, seed, n, out, mass ? mass : &W);
+}
+
+void Engine::branch_sum(const void *U, const void *L, size_t nb, size_t nu, size_t nl, void *A) {
+  if (!U || !L || !A || nb == 0 || nu == 0 || nl == 0) throw Error(QSIM_EINVAL, "empty slices");
+  ensure_device();
+  U_.reserve(nb * nu * amp_);
+  L_.reserve(nb * nl * amp_);
+  A_tot_.reserve(nu * nl * 16);
+  check(cudaMemcpyAsync(U_.ptr, U, nb * nu * amp_, cudaMemcpyHostToDevice, stream_), "upload U");
+  check(cudaMemcpyAsync(L_.ptr, L, nb * nl * amp_, cudaMemcpyHostToDevice, stream_), "upload L");
+  check(cudaMemsetAsync(A_tot_.ptr, 0, nu * nl * 16, stream_), "zero A");
+  gemm(U_.ptr, L_.ptr, (int64_t)nb, (int64_t)nu, (int64_t)nl, A_tot_.as<double>());
+  check(cudaMemcpyAsync(A, A_tot_.ptr, nu * nl * 16, cudaMemcpyDeviceToHost, stream_), "D2H A");
+  check(cudaStreamSynchronize(stream_), "branch_sum");
+  reduced_ = false;
+}
+
+void Engine::branch_state(int half, uint64_t b, void *out) {
+  if (!have_circuit_) throw Error(QSIM_ESTATE, "no circuit loaded");
+  if (half != 0 && half != 1) throw Error(QSIM_EINVAL, "half must be 0 (upper) or 1 (lower)");
+  const int c = (int)circ_.cuts.size();
+  if (c > 62 || b >= (1ull << c)) throw Error(QSIM_EINVAL, "branch out of range");
+  if (!out) throw Error(QSIM_EINVAL, "out is NULL");
+  ensure_device();
+  HalfExec &he = half_[half];
+  const int h = he.prog.h;
+  const size_t n = (size_t)1 << h;
+  // gather every index of the leaf: the same executor, S = 0 .. 2^h - 1
+  tmp_.reserve(n * 8);
+  std::vector<uint64_t> all(n);
+  for (size_t i = 0; i < n; ++i) all[i] = i;
+  check(cudaMemcpyAsync(tmp_.ptr, all.data(), n * 8, cudaMemcpyHostToDevice, stream_), "upload S");
+  DevBuf slice;
+  slice.reserve(n * amp_);
+  evolve_half(half, b, b + 1, slice.ptr, tmp_.as<uint64_t>(), (int64_t)n);
+  check(cudaMemcpyAsync(out, slice.ptr, n * amp_, cudaMemcpyDeviceToHost, stream_), "D2H state");
+  check(cudaStreamSynchronize(stream_), "branch_state");
+}
+
+// ---------------------------------------------------------------- multi-GPU
+void Engine::comm_init(int rank, int world, const void *id) {
+  if (world < 1 || rank < 0 || rank >= world || !id) throw Error(QSIM_EINVAL, "bad rank / world / id");
+  ensure_device();
+  if (comm_) {
+    ncclCommDestroy(comm_);
+    comm_ = nullptr;
+  }
+  if (world > 1) {
+    ncclUniqueId uid;
+    std::memcpy(&uid, id, sizeof(uid));
+    ncclResult_t r = ncclCommInitRank(&comm_, world, uid, rank);
+    if (r != ncclSuccess) throw Error(QSIM_ENCCL, std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
+  }
+  rank_ = rank;
+  world_ = world;
+  reduced_ = false;
+}
+
+void Engine::rank_range(uint64_t *b0, uint64_t *b1) const {
+  if (!have_circuit_) throw Error(QSIM_ESTATE, "no circuit loaded");
+  const int c = (int)circ_.cuts.size();
+  if (c > 62) throw Error(QSIM_EINVAL, "too many cuts");
+  const unsigned __int128 B = (unsigned __int128)1 << c;
+  *b0 = (uint64_t)(B * (unsigned)rank_ / (unsigned)world_);
+  *b1 = (uint64_t)(B * (unsigned)(rank_ + 1) / (unsigned)world_);
+}
+
+// ---------------------------------------------------------------- stats
+void Engine::stats(qsim_stats_t *out) {
+  if (inited_) {
+    check(cudaSetDevice(device_), "cudaSetDevice");
+    resolve_events();
+  }
+  *out = st_;
+}
+
+void Engine::stats_reset() {
+  if (inited_) resolve_events();
+  st_ = qsim_stats_t{};
+}
+
+void Engine::synchronize() {
+  if (!inited_) return;
+  check(cudaSetDevice(device_), "cudaSetDevice");
+  check(cudaStreamSynchronize(stream_), "cudaStreamSynchronize");
+}
+
+}  // namespace qsim

@@ -1,0 +1,149 @@
+// Per-context engine: device memory plan, branch-tree executor, reconstruction,
+// sampling, NCCL reduction of partial amplitude blocks.
+#pragma once
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include "../../include/qsim.h"
+#include "kernels.h"
+#include "program.h"
+
+namespace qsim {
+
+struct Error : std::runtime_error {
+  qsim_status code;
+  Error(qsim_status c, const std::string &m) : std::runtime_error(m), code(c) {}
+};
+
+struct DevBuf {
+  void *ptr = nullptr;
+  size_t bytes = 0;
+  void reserve(size_t n);  // grows (re-allocates without preserving contents)
+  void release();
+  template <typename T>
+  T *as() const { return reinterpret_cast<T *>(ptr); }
+  ~DevBuf() { release(); }
+  DevBuf() = default;
+  DevBuf(const DevBuf &) = delete;
+  DevBuf &operator=(const DevBuf &) = delete;
+};
+
+// One planned launch of the tile sweep (a Sweep may split into several when it has
+// more than 7 high target bits).
+struct TilePlan {
+  TileSweepParams p;  // src/dst/job fields filled at launch
+  int npass = 1;
+  bool use_pre = false;  // first chunk of a sweep: the sweep's pre diagonal applies
+  bool gen = false;
+  Diag pre;              // the sweep's pre diagonal (fork diagonal merged at launch)
+};
+
+struct HalfExec {
+  HalfProgram prog;
+  bool tree = false;                                // tile sweeps (true) or the small kernel
+  std::vector<std::vector<std::vector<TilePlan>>> plans;  // [level][sweep][chunk]
+  // small kernel program on the device
+  DevBuf d_levels, d_sweeps;
+  bool uploaded = false;
+};
+
+class Engine {
+ public:
+  Engine(qsim_precision prec, int device);
+  ~Engine();
+
+  std::string last_error;
+
+  void set_option(int key, int64_t value);
+  void set_stream(void *s);
+  void load_circuit(uint32_t rows, uint32_t cols, uint32_t depth, const qsim_gate *gates,
+                    size_t n_gates, uint32_t cut_row, const uint32_t *cut_layers, size_t n_cut_layers);
+  void partition(uint32_t *n_cuts, uint64_t *n_branches, qsim_cut *cuts) const;
+  void set_blocks(const uint64_t *up, size_t nu, const uint64_t *lo, size_t nl);
+  void check_blocks(const uint64_t *up, size_t nu, const uint64_t *lo, size_t nl) const;
+  void evolve_range(uint64_t b0, uint64_t b1);
+  void reset_block();
+  void amplitudes(void *amps);
+  void sample(uint64_t seed, size_t n, uint64_t *out, double *mass);
+  void sample_probs(const double *p, const uint64_t *up, size_t nu, const uint64_t *lo, size_t nl,
+                    uint32_t hl, uint64_t seed, size_t n, uint64_t *out, double *mass);
+  void branch_sum(const void *U, const void *L, size_t nb, size_t nu, size_t nl, void *A);
+  void branch_state(int half, uint64_t b, void *out);
+  void comm_init(int rank, int world, const void *id);
+  void rank_range(uint64_t *b0, uint64_t *b1) const;
+  void stats(qsim_stats_t *out);
+  void stats_reset();
+  void synchronize();
+
+  bool have_circuit() const { return have_circuit_; }
+
+ private:
+  qsim_precision prec_;
+  bool c128_;
+  size_t amp_;  // bytes per amplitude
+  int device_;
+  bool inited_ = false;
+  cudaStream_t stream_ = nullptr;
+  cudaStream_t own_stream_ = nullptr;
+  int num_sms_ = 148;
+  int occ1_ = 2, occ2_ = 2;
+  int mode_ = 0;
+  int64_t mem_budget_ = 0;
+  bool time_sweeps_ = false;
+
+  bool have_circuit_ = false;
+  Circuit circ_;
+  HalfExec half_[2];
+
+  bool have_blocks_ = false;
+  std::vector<uint64_t> Su_, Sl_;
+  DevBuf d_Su_, d_Sl_;
+  DevBuf A_acc_;  // double2 [nu, nl]
+  DevBuf A_tot_;  // reduced block (rank 0 with a communicator)
+  bool reduced_ = false;
+  DevBuf U_, L_;  // slices
+  std::vector<DevBuf *> states_;
+  size_t state_bytes_ = 0;
+  // sampler
+  DevBuf p_, C_, r_, R_, W_, draws_, tmp_;
+
+  // comm
+  ncclComm_t comm_ = nullptr;
+  int rank_ = 0, world_ = 1;
+
+  // stats
+  qsim_stats_t st_{};
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_sweep_, ev_gemm_;
+  std::vector<cudaEvent_t> ev_pool_;
+
+  void ensure_device();
+  void check(cudaError_t e, const char *what);
+  void compile_plans(HalfExec &he);
+  void upload_small(HalfExec &he);
+  void ensure_states(int half, int nbuf);
+  int materialized_from(int half, size_t free_bytes, int *nbuf);
+
+  // executor
+  void evolve_half(int half, uint64_t b0, uint64_t b1, void *slice, const uint64_t *dS, int64_t nS);
+  void run_level(int half, int level, uint64_t child, const void *src, void *dst);
+  void launch_plan(const TilePlan &tp, const Diag &fork, bool first_chunk_of_level, const void *src,
+                   void *dst, int h);
+  void gather_leaf(int half, uint64_t child_last, const void *psi, const uint64_t *dS, int64_t nS,
+                   void *out_row);
+  void gemm(const void *U, const void *L, int64_t K, int64_t M, int64_t N, double *A);
+  double *reduced_block();
+  void run_sampler(const double *p, int64_t M, int64_t N, const uint64_t *dSu, const uint64_t *dSl,
+                   uint32_t hl, uint64_t seed, size_t n, uint64_t *out, double *mass);
+
+  cudaEvent_t get_event();
+  void resolve_events();
+};
+
+}  // namespace qsim

@@ -1,0 +1,109 @@
+// Device parameter blocks and host launch wrappers of the sm_100a kernels.
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+
+#include <cuda_runtime.h>
+
+namespace qsim {
+
+// Device form of a fused diagonal (program.h Diag):
+//   D(i) = scale * w^{(ph0 + popc(i&t1) + 2popc(i&t2) + 4(popc(i&zm) + popc(i&i>>1&hm)
+//          + popc(i&i>>vs&vm))) & 7} * [(i & pm) == pv]
+struct DiagDev {
+  uint32_t t1, t2, zm, hm, vm, pm, pv;
+  int32_t vs;
+  int32_t ph0;
+  int32_t active;  // 0: identity, skip
+  double scale;
+};
+
+// ---------------------------------------------------------------- tile sweep
+// One launch = one memory pass over `njobs` half states of 2^h amplitudes.
+// Tile = 2^T amplitudes: the L low bits (contiguous 512-byte rows) + 7 "hi" bits
+// (the layer's high target bits, padded with the lowest free bits); the other bits
+// are the outer bits enumerated by the tile index.  256 threads hold the tile in
+// registers (16 register slots per thread x 16-byte vectors); targets on register
+// bits are butterflies in registers, on lane bits warp shuffles, and a second pass
+// through shared memory re-maps 4 other hi bits to registers when > 4 hi targets.
+constexpr int kMaxJobs = 16;
+constexpr int kHiBits = 7;
+
+struct TileSweepParams {
+  const void *src[kMaxJobs];
+  void *dst[kMaxJobs];
+  uint32_t job_pv[kMaxJobs];  // per-job projector value of the pre diagonal
+  uint32_t job_zm[kMaxJobs];  // per-job Z mask of the pre diagonal
+  int32_t njobs;
+  int32_t log2_ntiles;  // tiles per job = 2^(h - T)
+  int32_t nruns;
+  uint8_t run_start[32], run_len[32];  // outer bit runs, ascending
+  uint8_t hb[kHiBits];                 // hi tile bit positions, ascending
+  uint8_t gsel[2][4];                  // pass p: hb indices held in registers
+  uint8_t wsel[2][3];                  // pass p: hb indices mapped to the 3 warp bits
+  uint8_t gkind[2][4];                 // gate kind (0 none, 1 SX', 2 SY') per register bit
+  uint8_t lowkind[6];                  // gate kind per low bit (lane / vector bits), pass 0
+  DiagDev pre, post;
+};
+
+// pre_mode: 0 none, 1 apply pre diagonal to loaded values, 2 generate (no load)
+// c128: amplitudes are double2, else float2.
+cudaError_t launch_tile_sweep(const TileSweepParams &p, bool c128, int pre_mode, int npass,
+                              int grid, cudaStream_t s);
+int tile_low_bits(bool c128);  // L: 6 (c64) or 5 (c128); tile T = L + 7
+cudaError_t tile_sweep_setup(int *blocks_per_sm_1pass, int *blocks_per_sm_2pass, bool c128);
+
+// ---------------------------------------------------------------- small states (h <= 12)
+// Whole half state in shared memory; one CTA per branch; every level and sweep of the
+// half program in one launch; the leaf is gathered straight into the slice row.
+struct SmallSweepDev {
+  DiagDev pre, post;
+  int32_t ngates;
+  int32_t gen;
+  uint8_t bit[32];
+  uint8_t kind[32];
+};
+struct SmallLevelDev {
+  int32_t k;
+  int32_t first_sweep;
+  int32_t nsweeps;
+  uint8_t cut_bits[32];
+};
+struct SmallParams {
+  const SmallLevelDev *levels;
+  const SmallSweepDev *sweeps;
+  int32_t nlevels;
+  int32_t h;
+  int32_t upper;
+  int32_t c;                 // total cuts
+  uint64_t b0;               // first branch of this launch (blockIdx.x = b - b0)
+  const uint64_t *S;         // sampled indices of this half
+  int64_t nS;
+  void *out;                 // slice [nb, nS] complex
+};
+cudaError_t launch_small(const SmallParams &p, bool c128, uint64_t nb, cudaStream_t s);
+int small_max_h(bool c128);
+
+// ---------------------------------------------------------------- gather / reconstruction
+// out[j] = psi[S[j]] * pend(S[j])
+cudaError_t launch_gather(const void *psi, const uint64_t *S, int64_t n, void *out,
+                          const DiagDev &pend, bool c128, cudaStream_t s);
+// A[m, n] += sum_k U[k, m] * L[k, n]   (complex; U, L of the ctx precision, A double2)
+cudaError_t launch_branch_gemm(const void *U, const void *L, int64_t K, int64_t M, int64_t N,
+                               double *A, bool c128, cudaStream_t s);
+// p[i] = fma(re, re, im*im)
+cudaError_t launch_abs2(const double *A, int64_t n, double *p, cudaStream_t s);
+// C[i, :] = sequential inclusive prefix of p[i, :]; r[i] = C[i, N-1]
+cudaError_t launch_row_scan(const double *p, int64_t M, int64_t N, double *C, double *r,
+                            cudaStream_t s);
+// R = sequential inclusive prefix of r; W = R[M-1] (written to *W)
+cudaError_t launch_row_prefix(const double *r, int64_t M, double *R, double *W, cudaStream_t s);
+// draws k in [0, n): Philox4x32-10 uniforms, inverse CDF, x = (Su[i] << hl) | Sl[j]
+cudaError_t launch_draws(const double *p, const double *C, const double *r, const double *R,
+                         const double *W, int64_t M, int64_t N, const uint64_t *Su,
+                         const uint64_t *Sl, uint32_t hl, uint64_t seed, int64_t n,
+                         uint64_t *out, cudaStream_t s);
+cudaError_t launch_cast_c128_to_c64(const double *A, int64_t n, float *out, cudaStream_t s);
+
+}  // namespace qsim

@@ -1,0 +1,276 @@
+// Front end: validation, cut list, branch-tree levels and fused sweeps (see program.h).
+#include "program.h"
+
+#include <algorithm>
+#include <cmath>
+#include <map>
+#include <set>
+#include <sstream>
+
+namespace qsim {
+
+int Diag::count(int bit) const {
+  return (int)((t1 >> bit) & 1u) + 2 * (int)((t2 >> bit) & 1u) + 4 * (int)((zm >> bit) & 1u);
+}
+
+void Diag::set_count(int bit, int c) {
+  c &= 7;
+  const uint32_t m = 1u << bit;
+  t1 = (t1 & ~m) | ((c & 1) ? m : 0u);
+  t2 = (t2 & ~m) | ((c & 2) ? m : 0u);
+  zm = (zm & ~m) | ((c & 4) ? m : 0u);
+}
+
+void Diag::add_proj(int bit, int value) {
+  const uint32_t m = 1u << bit;
+  const uint32_t v = value ? m : 0u;
+  if ((pm & m) && ((pv & m) != v)) allzero = true;  // P0 P1 = 0
+  pm |= m;
+  pv = (pv & ~m) | v;
+}
+
+Diag Diag::merge(const Diag &a, const Diag &b) {
+  Diag d = a;
+  for (int bit = 0; bit < 32; ++bit) {
+    const int cb = b.count(bit);
+    if (cb) d.set_count(bit, d.count(bit) + cb);
+  }
+  d.hm ^= b.hm;  // CZ^2 = I
+  d.vm ^= b.vm;
+  const uint32_t overlap = a.pm & b.pm;
+  if ((a.pv & overlap) != (b.pv & overlap)) d.allzero = true;
+  d.pm = a.pm | b.pm;
+  d.pv = (a.pv & a.pm) | (b.pv & b.pm);
+  d.ph0 = (a.ph0 + b.ph0) & 7;
+  d.nhalf = a.nhalf + b.nhalf;
+  d.allzero = d.allzero || a.allzero || b.allzero;
+  return d;
+}
+
+double Diag::scale() const {
+  double s = std::ldexp(1.0, -(nhalf / 2));
+  if (nhalf & 1) s *= 0.70710678118654752440;
+  return s;
+}
+
+Diag HalfProgram::fork_diag(int level, uint64_t child) const {
+  Diag d;
+  if (level <= 0) return d;
+  const Level &L = levels[level];
+  for (int j = 0; j < L.k; ++j) {
+    const int bit = (int)((child >> (L.k - 1 - j)) & 1u);
+    if (upper)
+      d.add_proj(L.cut_bits[j], bit);
+    else if (bit)
+      d.add_Z(L.cut_bits[j]);
+  }
+  return d;
+}
+
+size_t HalfProgram::total_sweeps() const {
+  size_t s = 0;
+  for (auto &l : levels) s += l.sweeps.size();
+  return s;
+}
+
+static bool neighbours(uint32_t a, uint32_t b, uint32_t cols) {
+  const uint32_t ra = a / cols, ca = a % cols, rb = b / cols, cb = b % cols;
+  if (ra == rb) return (ca + 1 == cb) || (cb + 1 == ca);
+  if (ca == cb) return (ra + 1 == rb) || (rb + 1 == ra);
+  return false;
+}
+
+std::string build_circuit(uint32_t rows, uint32_t cols, uint32_t depth, const qsim_gate *gates,
+                          size_t n_gates, uint32_t cut_row, const uint32_t *cut_layers,
+                          size_t n_cut_layers, Circuit &out) {
+  std::ostringstream err;
+  if (rows < 2 || cols < 1) return "grid must have rows >= 2 and cols >= 1";
+  if ((uint64_t)rows * cols > 64) return "at most 64 qubits";
+  if (depth > 100000) return "depth too large";
+  if (cut_row == 0) cut_row = rows / 2;
+  if (cut_row < 1 || cut_row >= rows) return "cut_row must be in [1, rows)";
+  Circuit c;
+  c.rows = rows;
+  c.cols = cols;
+  c.depth = depth;
+  c.cut_row = cut_row;
+  c.n = rows * cols;
+  c.h_u = cut_row * cols;
+  c.h_l = c.n - c.h_u;
+  if (c.h_u > 32 || c.h_l > 32) {
+    err << "each half must have at most 32 qubits (h_u=" << c.h_u << ", h_l=" << c.h_l << ")";
+    return err.str();
+  }
+  if (n_gates && !gates) return "gates is NULL";
+  std::map<uint32_t, std::set<uint32_t>> used;  // layer -> qubits
+  c.gates.assign(gates, gates + n_gates);
+  for (size_t i = 0; i < n_gates; ++i) {
+    const qsim_gate &g = gates[i];
+    if (g.layer < 1 || g.layer > depth) {
+      err << "gate " << i << ": layer " << g.layer << " outside 1.." << depth;
+      return err.str();
+    }
+    if (g.kind < QSIM_SX || g.kind > QSIM_CZ) {
+      err << "gate " << i << ": unknown kind " << g.kind;
+      return err.str();
+    }
+    if (g.q0 >= c.n) {
+      err << "gate " << i << ": qubit " << g.q0 << " >= n = " << c.n;
+      return err.str();
+    }
+    auto &u = used[g.layer];
+    if (g.kind == QSIM_CZ) {
+      if (g.q1 >= c.n || g.q1 == g.q0) {
+        err << "gate " << i << ": bad CZ partner " << g.q1;
+        return err.str();
+      }
+      if (!neighbours(g.q0, g.q1, cols)) {
+        err << "gate " << i << ": CZ(" << g.q0 << "," << g.q1 << ") is not a grid edge";
+        return err.str();
+      }
+      if (u.count(g.q0) || u.count(g.q1)) {
+        err << "gate " << i << ": qubit used twice in layer " << g.layer << " (P:285)";
+        return err.str();
+      }
+      u.insert(g.q0);
+      u.insert(g.q1);
+      const bool a_up = g.q0 < c.h_u, b_up = g.q1 < c.h_u;
+      if (a_up != b_up) {
+        qsim_cut cut;
+        cut.layer = g.layer;
+        cut.q_upper = a_up ? g.q0 : g.q1;
+        cut.q_lower = a_up ? g.q1 : g.q0;
+        c.cuts.push_back(cut);
+      }
+    } else {
+      if (g.q1 != QSIM_NO_QUBIT) {
+        err << "gate " << i << ": single-qubit gate with q1 != QSIM_NO_QUBIT";
+        return err.str();
+      }
+      if (u.count(g.q0)) {
+        err << "gate " << i << ": qubit used twice in layer " << g.layer << " (P:285)";
+        return err.str();
+      }
+      u.insert(g.q0);
+    }
+  }
+  std::sort(c.cuts.begin(), c.cuts.end(), [](const qsim_cut &a, const qsim_cut &b) {
+    return a.layer != b.layer ? a.layer < b.layer : a.q_upper < b.q_upper;
+  });
+  for (auto &cut : c.cuts) {
+    if (c.fork_layers.empty() || c.fork_layers.back() != (int)cut.layer) {
+      c.fork_layers.push_back((int)cut.layer);
+      c.fork_k.push_back(0);
+    }
+    c.fork_k.back()++;
+  }
+  if (cut_layers) {
+    std::set<uint32_t> given(cut_layers, cut_layers + n_cut_layers);
+    std::set<uint32_t> derived;
+    for (int l : c.fork_layers) derived.insert((uint32_t)l);
+    if (given != derived) {
+      err << "cut_layers disagree with the cut CZs of the circuit (derived:";
+      for (auto l : derived) err << " " << l;
+      err << ")";
+      return err.str();
+    }
+  }
+  out = std::move(c);
+  return "";
+}
+
+namespace {
+struct LayerSpec {
+  std::vector<Gate1> gates;
+  Diag diag;
+};
+}  // namespace
+
+HalfProgram compile_half(const Circuit &c, bool upper) {
+  HalfProgram hp;
+  hp.upper = upper;
+  hp.h = (int)(upper ? c.h_u : c.h_l);
+  hp.vs = (int)c.cols;
+  const uint32_t lo = upper ? 0 : c.h_u, hi = upper ? c.h_u : c.n;
+  auto bit_of = [&](uint32_t q) { return hp.h - 1 - (int)(q - lo); };
+
+  std::vector<LayerSpec> layers(c.depth + 1);
+  for (const qsim_gate &g : c.gates) {
+    LayerSpec &L = layers[g.layer];
+    if (g.kind == QSIM_CZ) {
+      const bool in0 = g.q0 >= lo && g.q0 < hi, in1 = g.q1 >= lo && g.q1 < hi;
+      if (!(in0 && in1)) continue;  // cut CZ (handled as a fork) or the other half
+      const int b0 = bit_of(g.q0), b1 = bit_of(g.q1);
+      const int low = std::min(b0, b1), d = std::abs(b0 - b1);
+      if (d == 1 && (g.q0 / c.cols) == (g.q1 / c.cols))
+        L.diag.add_cz_h(low);
+      else
+        L.diag.add_cz_v(low);  // d == cols (validated grid edge)
+    } else {
+      if (!(g.q0 >= lo && g.q0 < hi)) continue;
+      const int b = bit_of(g.q0);
+      if (g.kind == QSIM_T) {
+        L.diag.add_T(b);
+      } else {
+        L.gates.push_back(Gate1{(uint8_t)b, (uint8_t)(g.kind == QSIM_SX ? 1 : 2)});
+      }
+    }
+  }
+  for (auto &L : layers) {
+    std::sort(L.gates.begin(), L.gates.end(),
+              [](const Gate1 &a, const Gate1 &b) { return a.bit < b.bit; });
+    // each factored gate carries the global factor w / sqrt2
+    L.diag.ph0 = (L.diag.ph0 + (int)L.gates.size()) & 7;
+    L.diag.nhalf += (int)L.gates.size();
+  }
+
+  const int F = (int)c.fork_layers.size();
+  hp.levels.resize(F + 1);
+  int g0 = 0;
+  for (int l = 0; l <= F; ++l) {
+    Level &lev = hp.levels[l];
+    if (l > 0) {
+      lev.fork_layer = c.fork_layers[l - 1];
+      lev.k = c.fork_k[l - 1];
+      lev.g0 = g0;
+      for (int j = 0; j < lev.k; ++j) {
+        const qsim_cut &cut = c.cuts[g0 + j];
+        lev.cut_bits.push_back(bit_of(upper ? cut.q_upper : cut.q_lower));
+      }
+      g0 += lev.k;
+    }
+    const int first = (l == 0) ? 1 : c.fork_layers[l - 1] + 1;
+    const int last = (l < F) ? c.fork_layers[l] : (int)c.depth;
+    Diag pending;
+    if (l == 0) pending.nhalf = hp.h;  // H^{(x)h}|0> = 2^{-h/2} everywhere (layer 0)
+    for (int t = first; t <= last; ++t) {
+      const LayerSpec &L = layers[t];
+      if (!L.gates.empty()) {
+        Sweep s;
+        s.gates = L.gates;
+        s.pre = pending;
+        s.post = L.diag;
+        s.gen = (l == 0 && lev.sweeps.empty());
+        s.first_layer = s.last_layer = t;
+        pending = Diag();
+        lev.sweeps.push_back(s);
+      } else if (!lev.sweeps.empty()) {
+        lev.sweeps.back().post = Diag::merge(lev.sweeps.back().post, L.diag);
+        lev.sweeps.back().last_layer = t;
+      } else {
+        pending = Diag::merge(pending, L.diag);
+      }
+    }
+    if (lev.sweeps.empty() && (l == 0 || first <= last)) {
+      Sweep s;
+      s.pre = pending;
+      s.gen = (l == 0);
+      s.first_layer = first;
+      s.last_layer = last;
+      lev.sweeps.push_back(s);
+    }
+  }
+  return hp;
+}
+
+}  // namespace qsim

@@ -1,0 +1,97 @@
+// Front end of the partitioned simulator (host C++, no CUDA).
+//
+// Turns a validated grid circuit into two "half programs" (upper / lower), one per
+// half of the bipartition of PAPER.md Supp. A, organised as the levels of
+// the branch tree: level 0 = layers 1..f_1 (shared by every branch), level l >= 1 =
+// the children created by the k_l cut CZs of fork layer f_l, covering layers
+// f_l+1 .. f_{l+1}.  Each level is a list of Sweeps; one Sweep is one memory pass
+// over a 2^h half state that applies
+//     post-diagonal  o  (X^1/2 / Y^1/2 gates on distinct bits)  o  pre-diagonal
+// where every run of diagonal gates (CZ, T, projectors P0/P1, Z) is fused into a
+// single phase pass "as the paper does" (§2.4, Eqs. 3-6).
+#pragma once
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/qsim.h"
+
+namespace qsim {
+
+// D(i) = 2^(-nhalf/2) * w^ph(i) * [(i & pm) == pv],  w = e^{i pi/4},
+// ph(i) = ph0 + popc(i&t1) + 2 popc(i&t2) + 4 (popc(i&zm) + popc(i & i>>1 & hm)
+//         + popc(i & i>>vs & vm))   (mod 8).
+// t1/t2/zm carry the per-bit T count mod 8 (T = w on |1>; Z = w^4), hm / vm
+// the horizontal / vertical CZ pairs (bit b with b+1 / b+vs; CZ = w^4 on |11>),
+// pm/pv the projector constraint (P0 / P1, Eq. 1), nhalf the 1/sqrt2 factors.
+struct Diag {
+  uint32_t t1 = 0, t2 = 0, zm = 0, hm = 0, vm = 0, pm = 0, pv = 0;
+  int ph0 = 0;
+  int nhalf = 0;
+  bool allzero = false;
+
+  bool identity() const {
+    return !allzero && !t1 && !t2 && !zm && !hm && !vm && !pm && ph0 == 0 && nhalf == 0;
+  }
+  int count(int bit) const;          // T count (mod 8) at bit
+  void set_count(int bit, int c);
+  void add_T(int bit) { set_count(bit, count(bit) + 1); }
+  void add_Z(int bit) { set_count(bit, count(bit) + 4); }
+  void add_cz_h(int lowbit) { hm ^= 1u << lowbit; }
+  void add_cz_v(int lowbit) { vm ^= 1u << lowbit; }
+  void add_proj(int bit, int value);  // P0 (value 0) or P1 (value 1)
+  // the product of two diagonals (they commute)
+  static Diag merge(const Diag &a, const Diag &b);
+  double scale() const;  // 2^(-nhalf/2)
+};
+
+// One non-diagonal gate of a sweep after factoring out its global phase:
+// SX = (w/sqrt2) [[1,-i],[-i,1]] (kind 1), SY = (w/sqrt2) [[1,-1],[1,1]] (kind 2).
+struct Gate1 {
+  uint8_t bit;
+  uint8_t kind;
+};
+
+struct Sweep {
+  std::vector<Gate1> gates;  // distinct bits
+  Diag pre, post;
+  bool gen = false;  // input not read: value = pre(i) (the H layer and leading diagonals)
+  int first_layer = 0, last_layer = 0;
+};
+
+struct Level {
+  int fork_layer = 0;          // 0 for the root
+  int k = 0;                   // cuts at this fork (children = 2^k)
+  int g0 = 0;                  // index of the first of them in the cut list
+  std::vector<int> cut_bits;   // half-local bit of each cut endpoint in this half
+  std::vector<Sweep> sweeps;
+};
+
+struct HalfProgram {
+  bool upper = true;
+  int h = 0;
+  int vs = 0;  // vertical pair distance (= cols)
+  std::vector<Level> levels;
+  // Diagonal of fork child c at level l (P_{bits} on the upper endpoints, Z^{bits} on the lower)
+  Diag fork_diag(int level, uint64_t child) const;
+  size_t total_sweeps() const;
+};
+
+struct Circuit {
+  uint32_t rows = 0, cols = 0, depth = 0, cut_row = 0;
+  uint32_t n = 0, h_u = 0, h_l = 0;
+  std::vector<qsim_gate> gates;
+  std::vector<qsim_cut> cuts;       // ordered by (layer, q_upper)
+  std::vector<int> fork_layers;     // distinct cut layers, ascending
+  std::vector<int> fork_k;          // cuts per fork layer
+};
+
+// Validates and derives the cut list.  Returns "" or an error message (EINVAL).
+std::string build_circuit(uint32_t rows, uint32_t cols, uint32_t depth, const qsim_gate *gates,
+                          size_t n_gates, uint32_t cut_row, const uint32_t *cut_layers,
+                          size_t n_cut_layers, Circuit &out);
+
+HalfProgram compile_half(const Circuit &c, bool upper);
+
+}  // namespace qsim

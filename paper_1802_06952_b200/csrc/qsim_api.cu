@@ -1,0 +1,174 @@
+// C-ABI of include/qsim.h: argument checks, exception -> status translation.
+#include <cstring>
+#include <new>
+#include <string>
+
+#include <nccl.h>
+
+#include "../../include/qsim.h"
+#include "engine.h"
+
+struct qsim_ctx {
+  qsim::Engine *eng = nullptr;
+  std::string err;
+};
+
+namespace {
+
+template <typename F>
+qsim_status guard(qsim_ctx *ctx, F &&f) {
+  if (!ctx || !ctx->eng) return QSIM_EINVAL;
+  ctx->err.clear();
+  try {
+    f(*ctx->eng);
+    return QSIM_OK;
+  } catch (const qsim::Error &e) {
+    ctx->err = e.what();
+    return e.code;
+  } catch (const std::bad_alloc &) {
+    ctx->err = "host allocation failed";
+    return QSIM_ENOMEM;
+  } catch (const std::exception &e) {
+    ctx->err = e.what();
+    return QSIM_EINVAL;
+  } catch (...) {
+    ctx->err = "unknown error";
+    return QSIM_EINVAL;
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+const char *qsim_version(void) { return "qsim-b200 0.1 (sm_100a)"; }
+
+qsim_status qsim_create(qsim_ctx **out, qsim_precision prec, int device) {
+  if (!out) return QSIM_EINVAL;
+  *out = nullptr;
+  qsim_ctx *c = new (std::nothrow) qsim_ctx();
+  if (!c) return QSIM_ENOMEM;
+  try {
+    c->eng = new qsim::Engine(prec, device);
+  } catch (const qsim::Error &e) {
+    delete c;
+    return e.code;
+  } catch (...) {
+    delete c;
+    return QSIM_ENOMEM;
+  }
+  *out = c;
+  return QSIM_OK;
+}
+
+void qsim_destroy(qsim_ctx *ctx) {
+  if (!ctx) return;
+  delete ctx->eng;
+  delete ctx;
+}
+
+const char *qsim_last_error(const qsim_ctx *ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+qsim_status qsim_set_option(qsim_ctx *ctx, int key, int64_t value) {
+  return guard(ctx, [&](qsim::Engine &e) { e.set_option(key, value); });
+}
+
+qsim_status qsim_set_stream(qsim_ctx *ctx, void *s) {
+  return guard(ctx, [&](qsim::Engine &e) { e.set_stream(s); });
+}
+
+qsim_status qsim_load_circuit(qsim_ctx *ctx, uint32_t rows, uint32_t cols, uint32_t depth,
+                              const qsim_gate *gates, size_t n_gates, uint32_t cut_row,
+                              const uint32_t *cut_layers, size_t n_cut_layers) {
+  return guard(ctx, [&](qsim::Engine &e) {
+    e.load_circuit(rows, cols, depth, gates, n_gates, cut_row, cut_layers, n_cut_layers);
+  });
+}
+
+qsim_status qsim_partition(qsim_ctx *ctx, uint32_t *n_cuts, uint64_t *n_branches, qsim_cut *cuts) {
+  return guard(ctx, [&](qsim::Engine &e) { e.partition(n_cuts, n_branches, cuts); });
+}
+
+qsim_status qsim_set_blocks(qsim_ctx *ctx, const uint64_t *up, size_t nu, const uint64_t *lo, size_t nl) {
+  return guard(ctx, [&](qsim::Engine &e) { e.set_blocks(up, nu, lo, nl); });
+}
+
+qsim_status qsim_evolve_range(qsim_ctx *ctx, uint64_t b0, uint64_t b1) {
+  return guard(ctx, [&](qsim::Engine &e) { e.evolve_range(b0, b1); });
+}
+
+qsim_status qsim_evolve_halves(qsim_ctx *ctx, const uint64_t *up, size_t nu, const uint64_t *lo, size_t nl) {
+  return guard(ctx, [&](qsim::Engine &e) {
+    e.set_blocks(up, nu, lo, nl);
+    uint64_t b0 = 0, b1 = 0;
+    e.rank_range(&b0, &b1);
+    if (b1 > b0) e.evolve_range(b0, b1);
+  });
+}
+
+qsim_status qsim_reset_block(qsim_ctx *ctx) {
+  return guard(ctx, [&](qsim::Engine &e) { e.reset_block(); });
+}
+
+qsim_status qsim_amplitudes(qsim_ctx *ctx, const uint64_t *up, size_t nu, const uint64_t *lo, size_t nl,
+                            void *amps) {
+  return guard(ctx, [&](qsim::Engine &e) {
+    e.check_blocks(up, nu, lo, nl);
+    e.amplitudes(amps);
+  });
+}
+
+qsim_status qsim_sample(qsim_ctx *ctx, uint64_t seed, size_t n, uint64_t *out, double *mass) {
+  return guard(ctx, [&](qsim::Engine &e) { e.sample(seed, n, out, mass); });
+}
+
+qsim_status qsim_sample_probs(qsim_ctx *ctx, const double *p, const uint64_t *up, size_t nu, const uint64_t *lo,
+                              size_t nl, uint32_t hl, uint64_t seed, size_t n, uint64_t *out, double *mass) {
+  return guard(ctx, [&](qsim::Engine &e) { e.sample_probs(p, up, nu, lo, nl, hl, seed, n, out, mass); });
+}
+
+qsim_status qsim_branch_sum(qsim_ctx *ctx, const void *U, const void *L, size_t nb, size_t nu, size_t nl,
+                            void *A) {
+  return guard(ctx, [&](qsim::Engine &e) { e.branch_sum(U, L, nb, nu, nl, A); });
+}
+
+qsim_status qsim_branch_state(qsim_ctx *ctx, int half, uint64_t b, void *out) {
+  return guard(ctx, [&](qsim::Engine &e) { e.branch_state(half, b, out); });
+}
+
+qsim_status qsim_nccl_unique_id(void *out128) {
+  if (!out128) return QSIM_EINVAL;
+  ncclUniqueId id;
+  if (ncclGetUniqueId(&id) != ncclSuccess) return QSIM_ENCCL;
+  static_assert(sizeof(id) == 128, "ncclUniqueId is 128 bytes");
+  std::memcpy(out128, &id, sizeof(id));
+  return QSIM_OK;
+}
+
+qsim_status qsim_comm_init(qsim_ctx *ctx, int rank, int world, const void *id) {
+  return guard(ctx, [&](qsim::Engine &e) { e.comm_init(rank, world, id); });
+}
+
+qsim_status qsim_rank_range(qsim_ctx *ctx, uint64_t *b0, uint64_t *b1) {
+  return guard(ctx, [&](qsim::Engine &e) {
+    if (!b0 || !b1) throw qsim::Error(QSIM_EINVAL, "null output");
+    e.rank_range(b0, b1);
+  });
+}
+
+qsim_status qsim_stats(qsim_ctx *ctx, qsim_stats_t *out) {
+  return guard(ctx, [&](qsim::Engine &e) {
+    if (!out) throw qsim::Error(QSIM_EINVAL, "null output");
+    e.stats(out);
+  });
+}
+
+qsim_status qsim_stats_reset(qsim_ctx *ctx) {
+  return guard(ctx, [&](qsim::Engine &e) { e.stats_reset(); });
+}
+
+qsim_status qsim_synchronize(qsim_ctx *ctx) {
+  return guard(ctx, [&](qsim::Engine &e) { e.synchronize(); });
+}
+
+}  // extern "C"

@@ -1,0 +1,339 @@
+// Leaf gather, reconstruction contraction A += U^T L on the FP64 tensor pipe (DMMA),
+// |a|^2, prefix tables and the Philox inverse-CDF sampler.
+//
+// "after sampling the data and performing the tensor product, the results are finally
+// added to the resultant vector" (Fig. 1 caption P:175): for sampled
+// blocks this is the complex contraction over the branch index b,
+//     A[i, j] = sum_b U[b, i] * L[b, j].
+#include <algorithm>
+
+#include "kernels.h"
+
+namespace qsim {
+
+template <typename R>
+struct CxT;
+template <>
+struct CxT<float> {
+  using T = float2;
+};
+template <>
+struct CxT<double> {
+  using T = double2;
+};
+
+static __constant__ double c_omega[16] = {1.0, 0.0, 0.70710678118654752440, 0.70710678118654752440, 0.0, 1.0,
+                                   -0.70710678118654752440, 0.70710678118654752440, -1.0, 0.0,
+                                   -0.70710678118654752440, -0.70710678118654752440, 0.0, -1.0,
+                                   0.70710678118654752440, -0.70710678118654752440};
+
+// ---------------------------------------------------------------- gather
+template <typename R>
+__global__ void gather_kernel(const typename CxT<R>::T *__restrict__ psi, const uint64_t *__restrict__ S,
+                              int64_t n, typename CxT<R>::T *__restrict__ out, DiagDev d) {
+  using C = typename CxT<R>::T;
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n;
+       j += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t i = S[j];
+    C x = psi[i];
+    if (d.active) {
+      const uint32_t ii = (uint32_t)i;
+      const int ph = (d.ph0 + __popc(ii & d.t1) + 2 * __popc(ii & d.t2) +
+                      4 * (__popc(ii & d.zm) + __popc(ii & (ii >> 1) & d.hm) +
+                           __popc(ii & (ii >> d.vs) & d.vm))) & 7;
+      const R wr = (R)(c_omega[2 * ph] * d.scale), wi = (R)(c_omega[2 * ph + 1] * d.scale);
+      C y;
+      y.x = x.x * wr - x.y * wi;
+      y.y = x.x * wi + x.y * wr;
+      if ((ii & d.pm) != d.pv) y.x = y.y = (R)0;
+      x = y;
+    }
+    out[j] = x;
+  }
+}
+
+cudaError_t launch_gather(const void *psi, const uint64_t *S, int64_t n, void *out,
+                          const DiagDev &pend, bool c128, cudaStream_t s) {
+  const int threads = 256;
+  const int blocks = (int)std::min<int64_t>((n + threads - 1) / threads, 4096);
+  if (c128)
+    gather_kernel<double><<<blocks, threads, 0, s>>>((const double2 *)psi, S, n, (double2 *)out, pend);
+  else
+    gather_kernel<float><<<blocks, threads, 0, s>>>((const float2 *)psi, S, n, (float2 *)out, pend);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------- branch GEMM (DMMA)
+// CTA tile 64 x 64 (M x N), K step 16, 8 warps as 2 (M) x 4 (N), warp tile 32 x 16 =
+// 4 x 2 m8n8k4 FP64 MMAs.  Complex product with 4 real MMAs per tile and K-step:
+//   Re += Ur Lr + (-Ui) Li,   Im += Ur Li + Ui Lr   (fp64 accumulate for both precisions)
+constexpr int GB_M = 64, GB_N = 64, GB_K = 16, GB_PAD = 8;
+
+__device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d[0]), "+d"(d[1])
+               : "d"(a), "d"(b));
+}
+
+template <typename R>
+__global__ void __launch_bounds__(256) branch_gemm_kernel(const typename CxT<R>::T *__restrict__ U,
+                                                          const typename CxT<R>::T *__restrict__ L,
+                                                          int64_t K, int64_t M, int64_t N,
+                                                          double *__restrict__ A) {
+  using C = typename CxT<R>::T;
+  __shared__ double sUr[GB_K][GB_M + GB_PAD], sUi[GB_K][GB_M + GB_PAD];
+  __shared__ double sLr[GB_K][GB_N + GB_PAD], sLi[GB_K][GB_N + GB_PAD];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = warp >> 2, wn = warp & 3;
+  const int64_t m0 = (int64_t)blockIdx.y * GB_M, n0 = (int64_t)blockIdx.x * GB_N;
+
+  double accr[4][2][2], acci[4][2][2];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 2; ++b) accr[a][b][0] = accr[a][b][1] = acci[a][b][0] = acci[a][b][1] = 0.0;
+
+  // each thread moves 4 elements of the U tile and 4 of the L tile per K step;
+  // the next step is fetched into registers while the current one is multiplied
+  C ru[4], rl[4];
+  auto fetch = [&](int64_t k0) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int e = tid + q * 256;  // 0..1023 = 16 x 64
+      const int kk = e >> 6, mm = e & 63;
+      const int64_t k = k0 + kk;
+      C u{}, l{};
+      if (k < K) {
+        if (m0 + mm < M) u = U[k * M + m0 + mm];
+        if (n0 + mm < N) l = L[k * N + n0 + mm];
+      }
+      ru[q] = u;
+      rl[q] = l;
+    }
+  };
+  auto stash = [&]() {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int e = tid + q * 256;
+      const int kk = e >> 6, mm = e & 63;
+      sUr[kk][mm] = (double)ru[q].x;
+      sUi[kk][mm] = (double)ru[q].y;
+      sLr[kk][mm] = (double)rl[q].x;
+      sLi[kk][mm] = (double)rl[q].y;
+    }
+  };
+
+  const int64_t nk = (K + GB_K - 1) / GB_K;
+  fetch(0);
+  stash();
+  __syncthreads();
+  for (int64_t kb = 0; kb < nk; ++kb) {
+    if (kb + 1 < nk) fetch((kb + 1) * GB_K);
+#pragma unroll
+    for (int ks = 0; ks < GB_K; ks += 4) {
+      const int kr = ks + (lane & 3);
+      double ar[4], ai[4], br[2], bi[2];
+#pragma unroll
+      for (int mt = 0; mt < 4; ++mt) {
+        const int mm = wm * 32 + mt * 8 + (lane >> 2);
+        ar[mt] = sUr[kr][mm];
+        ai[mt] = sUi[kr][mm];
+      }
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt) {
+        const int nn = wn * 16 + nt * 8 + (lane >> 2);
+        br[nt] = sLr[kr][nn];
+        bi[nt] = sLi[kr][nn];
+      }
+#pragma unroll
+      for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt) {
+          dmma(accr[mt][nt], ar[mt], br[nt]);
+          dmma(accr[mt][nt], -ai[mt], bi[nt]);
+          dmma(acci[mt][nt], ar[mt], bi[nt]);
+          dmma(acci[mt][nt], ai[mt], br[nt]);
+        }
+    }
+    __syncthreads();
+    if (kb + 1 < nk) {
+      stash();
+      __syncthreads();
+    }
+  }
+  // epilogue: D fragment row = lane >> 2, cols (lane & 3) * 2 + {0, 1}
+#pragma unroll
+  for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        const int64_t m = m0 + wm * 32 + mt * 8 + (lane >> 2);
+        const int64_t n = n0 + wn * 16 + nt * 8 + (lane & 3) * 2 + c;
+        if (m < M && n < N) {
+          double *a = A + 2 * (m * N + n);
+          a[0] += accr[mt][nt][c];
+          a[1] += acci[mt][nt][c];
+        }
+      }
+}
+
+cudaError_t launch_branch_gemm(const void *U, const void *L, int64_t K, int64_t M, int64_t N,
+                               double *A, bool c128, cudaStream_t s) {
+  if (K <= 0 || M <= 0 || N <= 0) return cudaSuccess;
+  dim3 grid((unsigned)((N + GB_N - 1) / GB_N), (unsigned)((M + GB_M - 1) / GB_M));
+  if (c128)
+    branch_gemm_kernel<double><<<grid, 256, 0, s>>>((const double2 *)U, (const double2 *)L, K, M, N, A);
+  else
+    branch_gemm_kernel<float><<<grid, 256, 0, s>>>((const float2 *)U, (const float2 *)L, K, M, N, A);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------- probabilities
+__global__ void abs2_kernel(const double2 *__restrict__ A, int64_t n, double *__restrict__ p) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const double2 a = A[i];
+    p[i] = fma(a.x, a.x, a.y * a.y);
+  }
+}
+
+cudaError_t launch_abs2(const double *A, int64_t n, double *p, cudaStream_t s) {
+  const int blocks = (int)std::min<int64_t>((n + 255) / 256, 148 * 16);
+  abs2_kernel<<<blocks, 256, 0, s>>>((const double2 *)A, n, p);
+  return cudaGetLastError();
+}
+
+// One warp per 32 rows: 32 x 32 tiles are staged through shared memory so that global
+// access is coalesced while every lane scans its own row strictly left to right.
+__global__ void __launch_bounds__(128) row_scan_kernel(const double *__restrict__ p, int64_t M, int64_t N,
+                                                       double *__restrict__ Cp, double *__restrict__ r) {
+  __shared__ double tile[4][32][33];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t row0 = ((int64_t)blockIdx.x * 4 + w) * 32;
+  if (row0 >= M) return;
+  double run = 0.0;
+  const int64_t myrow = row0 + lane;
+  for (int64_t j0 = 0; j0 < N; j0 += 32) {
+    for (int rr = 0; rr < 32; ++rr) {
+      const int64_t row = row0 + rr, col = j0 + lane;
+      tile[w][rr][lane] = (row < M && col < N) ? p[row * N + col] : 0.0;
+    }
+    __syncwarp();
+    const int lim = (int)std::min<int64_t>(32, N - j0);
+    for (int jj = 0; jj < lim; ++jj) {
+      run = run + tile[w][lane][jj];
+      tile[w][lane][jj] = run;
+    }
+    __syncwarp();
+    for (int rr = 0; rr < 32; ++rr) {
+      const int64_t row = row0 + rr, col = j0 + lane;
+      if (row < M && col < N) Cp[row * N + col] = tile[w][rr][lane];
+    }
+    __syncwarp();
+  }
+  if (myrow < M) r[myrow] = run;
+}
+
+cudaError_t launch_row_scan(const double *p, int64_t M, int64_t N, double *Cp, double *r,
+                            cudaStream_t s) {
+  const int blocks = (int)((M + 127) / 128);
+  row_scan_kernel<<<blocks, 128, 0, s>>>(p, M, N, Cp, r);
+  return cudaGetLastError();
+}
+
+__global__ void row_prefix_kernel(const double *__restrict__ r, int64_t M, double *__restrict__ R,
+                                  double *__restrict__ W) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  double run = 0.0;
+  for (int64_t i = 0; i < M; ++i) {
+    run = run + r[i];
+    R[i] = run;
+  }
+  *W = run;
+}
+
+cudaError_t launch_row_prefix(const double *r, int64_t M, double *R, double *W, cudaStream_t s) {
+  row_prefix_kernel<<<1, 32, 0, s>>>(r, M, R, W);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------- Philox4x32-10 sampler
+__device__ __forceinline__ void philox10(uint32_t (&c)[4], uint32_t k0, uint32_t k1) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    if (r > 0) {
+      k0 += 0x9E3779B9u;
+      k1 += 0xBB67AE85u;
+    }
+    const uint32_t hi0 = __umulhi(0xD2511F53u, c[0]), lo0 = 0xD2511F53u * c[0];
+    const uint32_t hi1 = __umulhi(0xCD9E8D57u, c[2]), lo1 = 0xCD9E8D57u * c[2];
+    const uint32_t n0 = hi1 ^ c[1] ^ k0, n2 = hi0 ^ c[3] ^ k1;
+    c[0] = n0;
+    c[1] = lo1;
+    c[2] = n2;
+    c[3] = lo0;
+  }
+}
+
+// first index in [0, n) with a[idx] > t (n if none); a non-decreasing
+__device__ __forceinline__ int64_t upper_bound(const double *a, int64_t n, double t) {
+  int64_t lo = 0, hi = n;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (a[mid] > t)
+      hi = mid;
+    else
+      lo = mid + 1;
+  }
+  return lo;
+}
+
+__global__ void draws_kernel(const double *__restrict__ p, const double *__restrict__ Cp,
+                             const double *__restrict__ r, const double *__restrict__ R,
+                             const double *__restrict__ Wp, int64_t M, int64_t N,
+                             const uint64_t *__restrict__ Su, const uint64_t *__restrict__ Sl,
+                             uint32_t hl, uint64_t seed, int64_t n, uint64_t *__restrict__ out) {
+  const double W = *Wp;
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t c[4] = {(uint32_t)k, (uint32_t)((uint64_t)k >> 32), 0u, 0u};
+    philox10(c, (uint32_t)seed, (uint32_t)(seed >> 32));
+    const uint64_t v = ((uint64_t)c[1] << 32) | c[0];
+    const double u = (double)(v >> 11) * 0x1.0p-53;
+    const double t = u * W;
+    int64_t i = upper_bound(R, M, t);
+    if (i >= M) {
+      i = M - 1;
+      while (i > 0 && !(r[i] > 0.0)) --i;
+    }
+    const double t2 = t - (i > 0 ? R[i - 1] : 0.0);
+    int64_t j = upper_bound(Cp + i * N, N, t2);
+    if (j >= N) {
+      j = N - 1;
+      while (j > 0 && !(p[i * N + j] > 0.0)) --j;
+    }
+    out[k] = (Su[i] << hl) | Sl[j];
+  }
+}
+
+cudaError_t launch_draws(const double *p, const double *Cp, const double *r, const double *R,
+                         const double *W, int64_t M, int64_t N, const uint64_t *Su,
+                         const uint64_t *Sl, uint32_t hl, uint64_t seed, int64_t n,
+                         uint64_t *out, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  const int blocks = (int)std::min<int64_t>((n + 255) / 256, 148 * 8);
+  draws_kernel<<<blocks, 256, 0, s>>>(p, Cp, r, R, W, M, N, Su, Sl, hl, seed, n, out);
+  return cudaGetLastError();
+}
+
+__global__ void cast_kernel(const double *__restrict__ A, int64_t n, float *__restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = (float)A[i];
+}
+
+cudaError_t launch_cast_c128_to_c64(const double *A, int64_t n, float *out, cudaStream_t s) {
+  const int blocks = (int)std::min<int64_t>((n + 255) / 256, 148 * 16);
+  cast_kernel<<<blocks, 256, 0, s>>>(A, n, out);
+  return cudaGetLastError();
+}
+
+}  // namespace qsim

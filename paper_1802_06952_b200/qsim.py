@@ -1,0 +1,281 @@
+"""Thin ctypes binding of the C-ABI in ``include/qsim.h`` (argument marshalling only).
+
+Every function has the C name and forwards to ``libqsim.so``; every step of the hot
+path runs in the library's CUDA kernels.  There is no CPU fallback: importing this
+module fails loudly when the library has not been built, and every compute call
+raises ``QsimError`` when no B200 is present.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libqsim.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"{LIB_PATH} is missing: build it with `python -m paper_1802_06952_b200.build` "
+                      "(there is no CPU fallback)")
+
+_lib = C.CDLL(LIB_PATH)
+
+QSIM_OK, QSIM_EINVAL, QSIM_ENOMEM, QSIM_ENUMERIC, QSIM_ECUDA, QSIM_ENCCL, QSIM_ESTATE = 0, 2, 3, 4, 5, 6, 7
+STATUS_NAMES = {0: "QSIM_OK", 2: "QSIM_EINVAL", 3: "QSIM_ENOMEM", 4: "QSIM_ENUMERIC", 5: "QSIM_ECUDA",
+                6: "QSIM_ENCCL", 7: "QSIM_ESTATE"}
+QSIM_C64, QSIM_C128 = 0, 1
+QSIM_SX, QSIM_SY, QSIM_T, QSIM_CZ = 1, 2, 3, 4
+QSIM_NO_QUBIT = 0xFFFFFFFF
+QSIM_OPT_TIME_SWEEPS, QSIM_OPT_MODE, QSIM_OPT_MEM_BUDGET = 1, 2, 3
+
+EXPORTED = ["qsim_create", "qsim_destroy", "qsim_last_error", "qsim_version", "qsim_set_option",
+            "qsim_set_stream", "qsim_load_circuit", "qsim_partition", "qsim_set_blocks",
+            "qsim_evolve_range", "qsim_evolve_halves", "qsim_reset_block", "qsim_amplitudes",
+            "qsim_sample", "qsim_sample_probs", "qsim_branch_sum", "qsim_branch_state",
+            "qsim_nccl_unique_id", "qsim_comm_init", "qsim_rank_range", "qsim_stats",
+            "qsim_stats_reset", "qsim_synchronize"]
+
+
+class qsim_cut(C.Structure):
+    _fields_ = [("layer", C.c_uint32), ("q_upper", C.c_uint32), ("q_lower", C.c_uint32)]
+
+
+class qsim_stats_t(C.Structure):
+    _fields_ = [("kernel_launches", C.c_uint64), ("sweeps", C.c_uint64), ("sweep_states", C.c_uint64),
+                ("sweep_bytes", C.c_double), ("sweep_ms", C.c_double), ("timed_sweeps", C.c_uint64),
+                ("gemm_flops", C.c_double), ("gemm_ms", C.c_double), ("branches_evolved", C.c_uint64)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+_P = C.c_void_p
+_sig = {
+    "qsim_create": (C.c_int, [C.POINTER(_P), C.c_int, C.c_int]),
+    "qsim_destroy": (None, [_P]),
+    "qsim_last_error": (C.c_char_p, [_P]),
+    "qsim_version": (C.c_char_p, []),
+    "qsim_set_option": (C.c_int, [_P, C.c_int, C.c_int64]),
+    "qsim_set_stream": (C.c_int, [_P, _P]),
+    "qsim_load_circuit": (C.c_int, [_P, C.c_uint32, C.c_uint32, C.c_uint32, _P, C.c_size_t, C.c_uint32,
+                                    _P, C.c_size_t]),
+    "qsim_partition": (C.c_int, [_P, C.POINTER(C.c_uint32), C.POINTER(C.c_uint64), _P]),
+    "qsim_set_blocks": (C.c_int, [_P, _P, C.c_size_t, _P, C.c_size_t]),
+    "qsim_evolve_range": (C.c_int, [_P, C.c_uint64, C.c_uint64]),
+    "qsim_evolve_halves": (C.c_int, [_P, _P, C.c_size_t, _P, C.c_size_t]),
+    "qsim_reset_block": (C.c_int, [_P]),
+    "qsim_amplitudes": (C.c_int, [_P, _P, C.c_size_t, _P, C.c_size_t, _P]),
+    "qsim_sample": (C.c_int, [_P, C.c_uint64, C.c_size_t, _P, _P]),
+    "qsim_sample_probs": (C.c_int, [_P, _P, _P, C.c_size_t, _P, C.c_size_t, C.c_uint32, C.c_uint64,
+                                    C.c_size_t, _P, _P]),
+    "qsim_branch_sum": (C.c_int, [_P, _P, _P, C.c_size_t, C.c_size_t, C.c_size_t, _P]),
+    "qsim_branch_state": (C.c_int, [_P, C.c_int, C.c_uint64, _P]),
+    "qsim_nccl_unique_id": (C.c_int, [_P]),
+    "qsim_comm_init": (C.c_int, [_P, C.c_int, C.c_int, _P]),
+    "qsim_rank_range": (C.c_int, [_P, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
+    "qsim_stats": (C.c_int, [_P, C.POINTER(qsim_stats_t)]),
+    "qsim_stats_reset": (C.c_int, [_P]),
+    "qsim_synchronize": (C.c_int, [_P]),
+}
+for _name, (_res, _args) in _sig.items():
+    _f = getattr(_lib, _name)
+    _f.restype = _res
+    _f.argtypes = _args
+
+
+class QsimError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(f"{STATUS_NAMES.get(status, status)}: {msg}")
+        self.status = status
+
+
+def _ptr(a):
+    return None if a is None else a.ctypes.data_as(_P)
+
+
+def _u64(a):
+    return np.ascontiguousarray(np.asarray(a, dtype=np.uint64))
+
+
+def _check(ctx, status):
+    if status != QSIM_OK:
+        msg = _lib.qsim_last_error(ctx).decode() if ctx else ""
+        raise QsimError(status, msg)
+
+
+def qsim_version() -> str:
+    return _lib.qsim_version().decode()
+
+
+def qsim_create(prec: int = QSIM_C64, device: int = 0):
+    ctx = _P()
+    _check(None, _lib.qsim_create(C.byref(ctx), prec, device))
+    return ctx
+
+
+def qsim_destroy(ctx):
+    _lib.qsim_destroy(ctx)
+
+
+def qsim_last_error(ctx) -> str:
+    return _lib.qsim_last_error(ctx).decode()
+
+
+def qsim_set_option(ctx, key: int, value: int):
+    _check(ctx, _lib.qsim_set_option(ctx, key, value))
+
+
+def qsim_set_stream(ctx, cuda_stream: int | None):
+    _check(ctx, _lib.qsim_set_stream(ctx, cuda_stream or None))
+
+
+def qsim_load_circuit(ctx, rows, cols, depth, gates, cut_row=0, cut_layers=None):
+    g = np.ascontiguousarray(np.asarray(gates, dtype=np.uint32).reshape(-1, 4))
+    cl = None if cut_layers is None else np.ascontiguousarray(np.asarray(cut_layers, dtype=np.uint32))
+    _check(ctx, _lib.qsim_load_circuit(ctx, rows, cols, depth, _ptr(g), g.shape[0], cut_row,
+                                       _ptr(cl), 0 if cl is None else cl.size))
+
+
+def qsim_partition(ctx):
+    """Returns (c, n_branches, cuts[c, 3] as (layer, q_upper, q_lower))."""
+    nc, nb = C.c_uint32(), C.c_uint64()
+    _check(ctx, _lib.qsim_partition(ctx, C.byref(nc), C.byref(nb), None))
+    cuts = np.zeros((nc.value, 3), dtype=np.uint32)
+    if nc.value:
+        _check(ctx, _lib.qsim_partition(ctx, C.byref(nc), C.byref(nb), _ptr(cuts)))
+    return nc.value, nb.value, cuts
+
+
+def qsim_set_blocks(ctx, upper_block, lower_block):
+    u, l = _u64(upper_block), _u64(lower_block)
+    _check(ctx, _lib.qsim_set_blocks(ctx, _ptr(u), u.size, _ptr(l), l.size))
+
+
+def qsim_evolve_range(ctx, branch_begin: int, branch_end: int):
+    _check(ctx, _lib.qsim_evolve_range(ctx, branch_begin, branch_end))
+
+
+def qsim_evolve_halves(ctx, upper_block, lower_block):
+    u, l = _u64(upper_block), _u64(lower_block)
+    _check(ctx, _lib.qsim_evolve_halves(ctx, _ptr(u), u.size, _ptr(l), l.size))
+
+
+def qsim_reset_block(ctx):
+    _check(ctx, _lib.qsim_reset_block(ctx))
+
+
+def qsim_amplitudes(ctx, upper_block, lower_block, prec: int, out=None, write=True):
+    """Reconstructed block [n_u, n_l] (complex64 / complex128 by ``prec``)."""
+    u, l = _u64(upper_block), _u64(lower_block)
+    if write and out is None:
+        out = np.empty((u.size, l.size), dtype=np.complex128 if prec == QSIM_C128 else np.complex64)
+    _check(ctx, _lib.qsim_amplitudes(ctx, _ptr(u), u.size, _ptr(l), l.size, _ptr(out) if write else None))
+    return out
+
+
+def qsim_sample(ctx, seed: int, n_draws: int, to_host: bool = True):
+    out = np.empty(n_draws, dtype=np.uint64) if to_host else None
+    mass = C.c_double(0.0)
+    _check(ctx, _lib.qsim_sample(ctx, seed, n_draws, _ptr(out), C.byref(mass) if to_host else None))
+    return out, mass.value
+
+
+def qsim_sample_probs(ctx, p, upper_block, lower_block, h_lower: int, seed: int, n_draws: int):
+    p = np.ascontiguousarray(np.asarray(p, dtype=np.float64))
+    u, l = _u64(upper_block), _u64(lower_block)
+    assert p.size == u.size * l.size
+    out = np.empty(n_draws, dtype=np.uint64)
+    mass = C.c_double(0.0)
+    _check(ctx, _lib.qsim_sample_probs(ctx, _ptr(p), _ptr(u), u.size, _ptr(l), l.size, h_lower, seed, n_draws,
+                                       _ptr(out), C.byref(mass)))
+    return out, mass.value
+
+
+def qsim_branch_sum(ctx, U, L, prec: int):
+    dt = np.complex128 if prec == QSIM_C128 else np.complex64
+    U = np.ascontiguousarray(np.asarray(U, dtype=dt))
+    L = np.ascontiguousarray(np.asarray(L, dtype=dt))
+    A = np.empty((U.shape[1], L.shape[1]), dtype=np.complex128)
+    _check(ctx, _lib.qsim_branch_sum(ctx, _ptr(U), _ptr(L), U.shape[0], U.shape[1], L.shape[1], _ptr(A)))
+    return A
+
+
+def qsim_branch_state(ctx, half: int, branch: int, h: int, prec: int):
+    out = np.empty(1 << h, dtype=np.complex128 if prec == QSIM_C128 else np.complex64)
+    _check(ctx, _lib.qsim_branch_state(ctx, half, branch, _ptr(out)))
+    return out
+
+
+def qsim_nccl_unique_id() -> bytes:
+    buf = (C.c_ubyte * 128)()
+    _check(None, _lib.qsim_nccl_unique_id(C.cast(buf, _P)))
+    return bytes(buf)
+
+
+def qsim_comm_init(ctx, rank: int, world: int, unique_id: bytes):
+    buf = (C.c_ubyte * 128).from_buffer_copy(unique_id)
+    _check(ctx, _lib.qsim_comm_init(ctx, rank, world, C.cast(buf, _P)))
+
+
+def qsim_rank_range(ctx):
+    b0, b1 = C.c_uint64(), C.c_uint64()
+    _check(ctx, _lib.qsim_rank_range(ctx, C.byref(b0), C.byref(b1)))
+    return b0.value, b1.value
+
+
+def qsim_stats(ctx) -> dict:
+    s = qsim_stats_t()
+    _check(ctx, _lib.qsim_stats(ctx, C.byref(s)))
+    return s.as_dict()
+
+
+def qsim_stats_reset(ctx):
+    _check(ctx, _lib.qsim_stats_reset(ctx))
+
+
+def qsim_synchronize(ctx):
+    _check(ctx, _lib.qsim_synchronize(ctx))
+
+
+class Simulator:
+    """Convenience owner of a context (the same calls, bound to one ctx)."""
+
+    def __init__(self, prec: int = QSIM_C64, device: int = 0):
+        self.prec = prec
+        self.ctx = qsim_create(prec, device)
+        self.h_u = self.h_l = None
+
+    def close(self):
+        if self.ctx:
+            qsim_destroy(self.ctx)
+            self.ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def load(self, circuit, cut_layers=None):
+        qsim_load_circuit(self.ctx, circuit.rows, circuit.cols, circuit.depth, circuit.gate_array(),
+                          circuit.cut_row, cut_layers)
+        self.h_u, self.h_l = circuit.h_upper, circuit.h_lower
+        return self
+
+    def partition(self):
+        return qsim_partition(self.ctx)
+
+    def amplitudes(self, S_u, S_l):
+        qsim_evolve_halves(self.ctx, S_u, S_l)
+        return qsim_amplitudes(self.ctx, S_u, S_l, self.prec)
+
+    def sample(self, seed, n):
+        return qsim_sample(self.ctx, seed, n)
+
+    def set_option(self, key, value):
+        qsim_set_option(self.ctx, key, value)
+        return self
+
+    def stats(self):
+        return qsim_stats(self.ctx)
