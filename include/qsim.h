@@ -82,7 +82,8 @@ typedef enum {
   QSIM_OPT_TIME_SWEEPS = 1, /* 1: bracket each sweep/GEMM launch with CUDA events (default 0) */
   QSIM_OPT_MODE = 2,        /* 0: auto, 1: flat in-shared-memory per-branch kernel (h <= 12),
                                2: prefix-shared branch tree of tile sweeps (h >= 13)          */
-  QSIM_OPT_MEM_BUDGET = 3     /* cap in bytes on device memory for half-state buffers (0 = free memory) */
+  QSIM_OPT_MEM_BUDGET = 3,  /* cap in bytes on device memory for half-state buffers (0 = free memory) */
+  QSIM_OPT_SWEEP_KERNEL = 4 /* 0: TMA-pipelined sweep (default), 1: register-only sweep (comparison) */
 } qsim_option;
 
 /* Create a context bound to CUDA device `device` (no device call is made until the

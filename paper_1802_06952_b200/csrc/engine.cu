@@ -62,6 +62,49 @@ static DiagDev to_dev(const Diag &d, int vs, bool force_active = false) {
   return o;
 }
 
+// DiagSplit of a diagonal for the register slots at global bit positions regpos
+// (slot index bit j <-> regpos[j]); see kernels.h.
+static DiagSplit make_split(const Diag &d, int vs, const std::vector<int> &regpos) {
+  DiagSplit s;
+  std::memset(&s, 0, sizeof(s));
+  const DiagDev dd = to_dev(d, vs, true);
+  uint32_t Rbits = 0;
+  for (int p : regpos) Rbits |= 1u << p;
+  const int nslots = 1 << regpos.size();
+  for (int idx = 0; idx < nslots; ++idx) {
+    uint32_t R = 0;
+    for (size_t j = 0; j < regpos.size(); ++j)
+      if ((idx >> j) & 1) R |= 1u << regpos[j];
+    const int ph = dd.ph0 + __builtin_popcount(R & dd.t1) + 2 * __builtin_popcount(R & dd.t2) +
+                   4 * (__builtin_popcount(R & dd.zm) + __builtin_popcount(R & (R >> 1) & dd.hm) +
+                        __builtin_popcount(R & (R >> dd.vs) & dd.vm));
+    const bool okR = (R & dd.pm & Rbits) == (dd.pv & dd.pm & Rbits);
+    s.P[idx] = (uint8_t)((ph & 7) << 3);
+    if (!okR) s.notok |= 1u << idx;
+  }
+  s.has_proj = (dd.pm != 0) ? 1 : 0;
+  for (size_t j = 0; j < regpos.size(); ++j) {
+    const int p = regpos[j];
+    uint32_t N = 0;
+    if (((dd.hm >> p) & 1u) && p + 1 < 32) N |= 1u << (p + 1);
+    if (p >= 1 && ((dd.hm >> (p - 1)) & 1u)) N |= 1u << (p - 1);
+    if (((dd.vm >> p) & 1u) && p + dd.vs < 32) N |= 1u << (p + dd.vs);
+    if (p >= dd.vs && ((dd.vm >> (p - dd.vs)) & 1u)) N |= 1u << (p - dd.vs);
+    s.N[j] = N & ~Rbits;
+  }
+  s.Bpm = dd.pm & ~Rbits;
+  s.Bpv = dd.pv & ~Rbits;
+  if ((dd.pv & ~dd.pm) & ~Rbits) s.Bpv = dd.pv & ~Rbits;  // allzero encoding: never matches
+  return s;
+}
+
+static std::vector<int> reg_positions(const TileSweepParams &p, int pass, bool c128) {
+  std::vector<int> pos;
+  if (!c128) pos.push_back(0);  // the vector bit (c64: 2 amplitudes per 16 bytes)
+  for (int s = 0; s < 4; ++s) pos.push_back(p.hb[p.gsel[pass][s]]);
+  return pos;
+}
+
 // ---------------------------------------------------------------- construction
 Engine::Engine(qsim_precision prec, int device) : prec_(prec), device_(device) {
   if (prec != QSIM_C64 && prec != QSIM_C128) throw Error(QSIM_EINVAL, "precision must be QSIM_C64 or QSIM_C128");
@@ -115,6 +158,7 @@ void Engine::ensure_device() {
   check(cudaStreamCreateWithFlags(&own_stream_, cudaStreamNonBlocking), "cudaStreamCreate");
   if (!stream_) stream_ = own_stream_;
   check(tile_sweep_setup(&occ1_, &occ2_, c128_), "tile sweep setup");
+  check(tile_sweep_tma_setup(c128_), "tma sweep setup");
   occ1_ = std::max(occ1_, 1);
   occ2_ = std::max(occ2_, 1);
   inited_ = true;
@@ -138,6 +182,10 @@ void Engine::set_option(int key, int64_t value) {
     case QSIM_OPT_MEM_BUDGET:
       if (value < 0) throw Error(QSIM_EINVAL, "memory budget must be >= 0");
       mem_budget_ = value;
+      return;
+    case QSIM_OPT_SWEEP_KERNEL:
+      if (value < 0 || value > 1) throw Error(QSIM_EINVAL, "QSIM_OPT_SWEEP_KERNEL must be 0 or 1");
+      sweep_kernel_ = (int)value;
       return;
     default:
       throw Error(QSIM_EINVAL, "unknown option key");
@@ -242,6 +290,15 @@ void Engine::compile_plans(HalfExec &he) {
         }
         if (ci == 0)
           for (auto &g : low) tp.p.lowkind[g.bit] = g.kind;
+        {
+          const int VB = c128_ ? 0 : 1;
+          for (int b = VB; b < VB + 5; ++b)
+            if (tp.p.lowkind[b]) {
+              tp.p.lane_bit[tp.p.n_lane] = (uint8_t)(b - VB);
+              tp.p.lane_kind[tp.p.n_lane] = tp.p.lowkind[b];
+              tp.p.n_lane++;
+            }
+        }
         // outer runs
         int nr = 0;
         for (int b = L; b < hp.h;) {
@@ -261,7 +318,12 @@ void Engine::compile_plans(HalfExec &he) {
         tp.use_pre = ci == 0;
         tp.gen = sw.gen && ci == 0;
         tp.pre = sw.pre;
-        tp.p.post = to_dev(ci == nchunks - 1 ? sw.post : Diag(), hp.vs);
+        const Diag post = ci == nchunks - 1 ? sw.post : Diag();
+        tp.p.post = to_dev(post, hp.vs);
+        tp.p.post_s = make_split(post, hp.vs, reg_positions(tp.p, tp.npass - 1, c128_));
+        int m = 0;
+        while (m < kHiBits && hb[m] == L + m) ++m;
+        tp.p.run_m = m;
         he.plans[l][s].push_back(tp);
       }
     }
@@ -409,7 +471,9 @@ void Engine::launch_plan(const TilePlan &tp, const Diag &fork, bool first, const
   p.job_pv[0] = p.pre.pv;
   p.job_zm[0] = p.pre.zm;
   const uint64_t tiles = (1ull << p.log2_ntiles) * (uint64_t)p.njobs;
-  const int occ = tp.npass == 1 ? occ1_ : occ2_;
+  const bool tma = sweep_kernel_ == 0 && pre_mode != 2 && p.njobs == 1;
+  if (tma && pre_mode == 1) p.pre_s = make_split(pre, vs, reg_positions(p, 0, c128_));
+  const int occ = tma ? 1 : (tp.npass == 1 ? occ1_ : occ2_);
   const int grid = (int)std::min<uint64_t>(tiles, (uint64_t)num_sms_ * occ);
   const bool timed = time_sweeps_;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
@@ -418,7 +482,10 @@ void Engine::launch_plan(const TilePlan &tp, const Diag &fork, bool first, const
     e1 = get_event();
     check(cudaEventRecord(e0, stream_), "cudaEventRecord");
   }
-  check(launch_tile_sweep(p, c128_, pre_mode, tp.npass, grid, stream_), "tile sweep launch");
+  if (tma)
+    check(launch_tile_sweep_tma(p, c128_, pre_mode, tp.npass, grid, stream_), "tma sweep launch");
+  else
+    check(launch_tile_sweep(p, c128_, pre_mode, tp.npass, grid, stream_), "tile sweep launch");
   if (timed) {
     check(cudaEventRecord(e1, stream_), "cudaEventRecord");
     ev_sweep_.emplace_back(e0, e1);

@@ -96,6 +96,7 @@ class Engine {
   int occ1_ = 2, occ2_ = 2;
   int mode_ = 0;
   int64_t mem_budget_ = 0;
+  int sweep_kernel_ = 0;  // 0: TMA-pipelined sweep, 1: register-only sweep
   bool time_sweeps_ = false;
 
   bool have_circuit_ = false;

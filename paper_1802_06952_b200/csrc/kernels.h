@@ -30,6 +30,21 @@ struct DiagDev {
 constexpr int kMaxJobs = 16;
 constexpr int kHiBits = 7;
 
+// Phase decomposition used by the TMA sweep (host precomputed).  For an element
+// i = B | R_r, where B holds the thread / tile bits and R_r the register-slot bits,
+//   ph(i) = ph_B(B) + P[r] + 4 * sum_j r_j * (popc(B & N[j]) & 1)        (mod 8)
+//   ok(i) = ((B & Bpm) == Bpv) && !(P[r] & 8)
+// ph_B is the full phase formula on B without ph0; P[r] carries ph0, every term of R_r
+// alone and bit 3 = "projector fails on the register bits"; N[j] are the B-side
+// partner bits of the CZ pairs of register bit j.
+struct DiagSplit {
+  uint8_t P[32];      // phase of R_r (+ph0) mod 8, times 8 (byte offset into a float2 table)
+  uint32_t N[5];
+  uint32_t Bpm, Bpv;
+  uint32_t notok;     // bit r: the projector fails on the register bits of slot r
+  int32_t has_proj;   // any projector at all (else the zeroing is skipped)
+};
+
 struct TileSweepParams {
   const void *src[kMaxJobs];
   void *dst[kMaxJobs];
@@ -45,12 +60,24 @@ struct TileSweepParams {
   uint8_t gkind[2][4];                 // gate kind (0 none, 1 SX', 2 SY') per register bit
   uint8_t lowkind[6];                  // gate kind per low bit (lane / vector bits), pass 0
   DiagDev pre, post;
+  DiagSplit pre_s, post_s;  // TMA sweep: pre uses the pass-0 registers, post the last pass's
+  int32_t run_m;            // hb[0..run_m-1] == L..L+run_m-1: contiguous run of 2^(L+m) amps
+  int32_t n_lane;           // TMA sweep: compact list of the lane-bit targets (pass 0)
+  uint8_t lane_bit[5], lane_kind[5];
 };
 
 // pre_mode: 0 none, 1 apply pre diagonal to loaded values, 2 generate (no load)
 // c128: amplitudes are double2, else float2.
 cudaError_t launch_tile_sweep(const TileSweepParams &p, bool c128, int pre_mode, int npass,
                               int grid, cudaStream_t s);
+// TMA-pipelined sweep (single job, pre_mode 0/1): one CTA per SM, 3 shared-memory tile
+// stages filled by cp.async.bulk under mbarriers, 1 producer warp + two ping-pong groups
+// of 8 consumer warps (each group owns alternate tiles).
+cudaError_t launch_tile_sweep_tma(const TileSweepParams &p, bool c128, int pre_mode, int npass,
+                                  int grid, cudaStream_t s);
+cudaError_t tile_sweep_tma_setup(bool c128);
+constexpr int kTmaStages = 2;  // one stage per consumer group
+constexpr int kTileBytes = 65536;
 int tile_low_bits(bool c128);  // L: 6 (c64) or 5 (c128); tile T = L + 7
 cudaError_t tile_sweep_setup(int *blocks_per_sm_1pass, int *blocks_per_sm_2pass, bool c128);
 

@@ -1,0 +1,359 @@
+// TMA-pipelined gate sweep for sm_100a (the hot loop of SURVEY §8(a) a3/a4).
+//
+// One persistent CTA per SM: warp 8 is the producer, which streams each 64 KB tile
+// (2^T amplitudes gathered from 2^(7-m) contiguous runs) into one of 3 shared-memory
+// stages with cp.async.bulk, completing on the stage's "full" mbarrier.  Warps 0-7
+// consume: they move the tile from shared memory into registers (16-byte vectors,
+// conflict-free), apply every X^1/2 / Y^1/2 target of the layer (registers, warp
+// shuffles for lane bits, a second register mapping through the same stage when more
+// than 4 high targets), release the stage on its "empty" mbarrier as soon as the last
+// shared-memory read is done, apply the fused diagonal and store straight to HBM.
+// Loads of the next two tiles are therefore always in flight while a tile is computed.
+//
+// The fused diagonal (§2.4, Eqs. 3-6) is evaluated through the host-computed
+// DiagSplit decomposition: per element one add, one table lookup and one complex
+// multiply instead of the full popcount formula.
+#include "sweep_common.cuh"
+
+namespace qsim {
+
+__device__ __forceinline__ uint32_t smem_addr(const void *p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_addr(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_addr(dst)),
+      "l"(src), "r"(bytes), "r"(smem_addr(bar))
+      : "memory");
+}
+
+// Fused diagonal through the DiagSplit decomposition (kernels.h).  The phase table
+// holds w^k * scale at byte offset 8k (float2) / 16k (double2); the cross terms of
+// register bits with their B-side CZ partners are a per-tile parity mask over the slots.
+template <typename R, int NV>
+__device__ __forceinline__ void apply_split(typename Cx2<R>::T (&v)[16][NV], const uint32_t B, const DiagDev &d,
+                                            const DiagSplit &sp, const typename Cx2<R>::T *tab) {
+  using C = typename Cx2<R>::T;
+  constexpr int VB = NV == 2 ? 1 : 0;
+  constexpr uint32_t pat[5] = {0xAAAAAAAAu, 0xCCCCCCCCu, 0xF0F0F0F0u, 0xFF00FF00u, 0xFFFF0000u};
+  const uint32_t pB8 = (uint32_t)(diag_phase_b(B, d) & 7) << 3;
+  uint32_t cpm = 0;
+#pragma unroll
+  for (int j = 0; j < VB + 4; ++j)
+    if (__popc(B & sp.N[j]) & 1) cpm ^= pat[j];
+  const char *tb = reinterpret_cast<const char *>(tab);
+#pragma unroll
+  for (int s = 0; s < 16; ++s)
+#pragma unroll
+    for (int e = 0; e < NV; ++e) {
+      const int idx = (s << VB) | e;
+      const uint32_t cross = (idx <= 5 ? (cpm << (5 - idx)) : (cpm >> (idx - 5))) & 32u;
+      const uint32_t off = (pB8 + sp.P[idx] + cross) & 56u;
+      const C w = *reinterpret_cast<const C *>(tb + off * (uint32_t)(sizeof(C) / 8));
+      v[s][e] = cmul(v[s][e], w);
+    }
+  if (sp.has_proj) {
+    const bool okB = (B & sp.Bpm) == sp.Bpv;
+#pragma unroll
+    for (int s = 0; s < 16; ++s)
+#pragma unroll
+      for (int e = 0; e < NV; ++e) {
+        const int idx = (s << VB) | e;
+        if (!okB || ((sp.notok >> idx) & 1u)) v[s][e].x = v[s][e].y = (R)0;
+      }
+  }
+}
+
+// gates on the 4 register hi bits of a pass (kinds are uniform: branch outside the loops)
+template <typename R, int NV>
+__device__ __forceinline__ void reg_gates(typename Cx2<R>::T (&v)[16][NV], const uint8_t *kinds) {
+#pragma unroll
+  for (int s = 0; s < 4; ++s) {
+    const int k = kinds[s];
+    if (k == 1) {
+#pragma unroll
+      for (int r = 0; r < 16; ++r) {
+        if (r & (1 << s)) continue;
+#pragma unroll
+        for (int e = 0; e < NV; ++e) {
+          auto &a = v[r][e];
+          auto &b = v[r | (1 << s)][e];
+          const R ax = a.x, ay = a.y;
+          a.x = ax + b.y;
+          a.y = ay - b.x;
+          b.x = b.x + ay;
+          b.y = b.y - ax;
+        }
+      }
+    } else if (k == 2) {
+#pragma unroll
+      for (int r = 0; r < 16; ++r) {
+        if (r & (1 << s)) continue;
+#pragma unroll
+        for (int e = 0; e < NV; ++e) {
+          auto &a = v[r][e];
+          auto &b = v[r | (1 << s)][e];
+          const R ax = a.x, ay = a.y;
+          a.x = ax - b.x;
+          a.y = ay - b.y;
+          b.x = ax + b.x;
+          b.y = ay + b.y;
+        }
+      }
+    }
+  }
+}
+
+// gates on the vector bit (c64, in registers) and on lane bits (warp shuffles)
+template <typename R, int NV>
+__device__ __forceinline__ void low_gates(typename Cx2<R>::T (&v)[16][NV], const TileSweepParams &p, int lane) {
+  using C = typename Cx2<R>::T;
+  if constexpr (NV == 2) {
+    const int k = p.lowkind[0];
+    if (k == 1) {
+#pragma unroll
+      for (int r = 0; r < 16; ++r) {
+        C &a = v[r][0], &b = v[r][1];
+        const R ax = a.x, ay = a.y;
+        a.x = ax + b.y;
+        a.y = ay - b.x;
+        b.x = b.x + ay;
+        b.y = b.y - ax;
+      }
+    } else if (k == 2) {
+#pragma unroll
+      for (int r = 0; r < 16; ++r) {
+        C &a = v[r][0], &b = v[r][1];
+        const R ax = a.x, ay = a.y;
+        a.x = ax - b.x;
+        a.y = ay - b.y;
+        b.x = ax + b.x;
+        b.y = ay + b.y;
+      }
+    }
+  }
+  for (int i = 0; i < p.n_lane; ++i) {
+    const int lb = p.lane_bit[i];
+    const int mask = 1 << lb;
+    if (p.lane_kind[i] == 1) {  // both partners: v - i w
+#pragma unroll
+      for (int r = 0; r < 16; ++r)
+#pragma unroll
+        for (int e = 0; e < NV; ++e) {
+          const R wx = __shfl_xor_sync(0xffffffffu, v[r][e].x, mask);
+          const R wy = __shfl_xor_sync(0xffffffffu, v[r][e].y, mask);
+          v[r][e].x += wy;
+          v[r][e].y -= wx;
+        }
+    } else {  // SY': lo = a - b, hi = a + b
+      const R sg = ((lane >> lb) & 1) ? (R)1 : (R)-1;
+#pragma unroll
+      for (int r = 0; r < 16; ++r)
+#pragma unroll
+        for (int e = 0; e < NV; ++e) {
+          const R wx = __shfl_xor_sync(0xffffffffu, v[r][e].x, mask);
+          const R wy = __shfl_xor_sync(0xffffffffu, v[r][e].y, mask);
+          v[r][e].x = fma(sg, wx, v[r][e].x);
+          v[r][e].y = fma(sg, wy, v[r][e].y);
+        }
+    }
+  }
+}
+
+// shared-memory slot index of register slot r for pass q (incrementally OR-ed)
+__device__ __forceinline__ uint32_t slot_smem(uint32_t base, const uint8_t *gsel, int r) {
+  uint32_t si = base;
+#pragma unroll
+  for (int k = 0; k < 4; ++k)
+    if (r & (1 << k)) si |= 1u << (5 + gsel[k]);
+  return si;
+}
+
+template <typename R, int PRE, int NPASS>
+__global__ void __launch_bounds__(544, 1) tile_sweep_tma_kernel(const __grid_constant__ TileSweepParams p) {
+  using C = typename Cx2<R>::T;
+  using V = typename Cx2<R>::V;
+  constexpr int VB = sizeof(R) == 4 ? 1 : 0;
+  constexpr int NV = 1 << VB;
+  constexpr int L = 5 + VB;
+  constexpr int NVEC = kTileBytes / 16;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  V *stages = reinterpret_cast<V *>(smem_raw);
+  __shared__ __align__(8) uint64_t full_bar[kTmaStages], empty_bar[kTmaStages];
+  __shared__ __align__(16) C tab_pre[8], tab_post[8];
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid < 8) {
+    tab_pre[tid].x = (R)(c_omega[2 * tid] * p.pre.scale);
+    tab_pre[tid].y = (R)(c_omega[2 * tid + 1] * p.pre.scale);
+    tab_post[tid].x = (R)(c_omega[2 * tid] * p.post.scale);
+    tab_post[tid].y = (R)(c_omega[2 * tid + 1] * p.post.scale);
+  }
+  if (tid == 0) {
+    for (int s = 0; s < kTmaStages; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], 8);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  const uint64_t ntiles = 1ull << p.log2_ntiles;
+  auto tile_outer = [&](uint64_t t64) {
+    uint32_t t = (uint32_t)t64, outer = 0;
+    for (int q = 0; q < p.nruns; ++q) {
+      outer |= (t & ((1u << p.run_len[q]) - 1u)) << p.run_start[q];
+      t >>= p.run_len[q];
+    }
+    return outer;
+  };
+
+  if (warp == 16) {
+    // ------------------------------------------------ producer: TMA bulk copies
+    const int m = p.run_m;
+    const int rbits = kHiBits - m;
+    const int nruns = 1 << rbits;
+    const uint32_t run_log2 = L + m;
+    const uint32_t run_bytes = (uint32_t)sizeof(C) << run_log2;
+    const char *src = reinterpret_cast<const char *>(p.src[0]);
+    for (int it = 0;; ++it) {
+      const uint64_t t = blockIdx.x + (uint64_t)it * gridDim.x;
+      if (t >= ntiles) break;
+      const int s = it & 1;
+      const uint32_t par = (uint32_t)(it >> 1) & 1u;
+      mbar_wait(&empty_bar[s], par ^ 1u);
+      if (lane == 0) mbar_arrive_expect_tx(&full_bar[s], kTileBytes);
+      __syncwarp();
+      const uint32_t outer = tile_outer(t);
+      char *stage = reinterpret_cast<char *>(stages + (size_t)s * NVEC);
+      for (int q = lane; q < nruns; q += 32) {
+        uint32_t gi = outer;
+        for (int j = 0; j < rbits; ++j)
+          if ((q >> j) & 1) gi |= 1u << p.hb[m + j];
+        bulk_g2s(stage + ((size_t)q << run_log2) * sizeof(C), src + (size_t)gi * sizeof(C), run_bytes,
+                 &full_bar[s]);
+      }
+    }
+    return;
+  }
+
+  // -------------------------------------------------- two ping-pong consumer groups
+  const int grp = warp >> 3, wl = warp & 7;
+  V *tile = stages + (size_t)grp * NVEC;
+  V *dst = reinterpret_cast<V *>(p.dst[0]);
+  for (int k = 0;; ++k) {
+    const int it = 2 * k + grp;
+    const uint64_t t = blockIdx.x + (uint64_t)it * gridDim.x;
+    if (t >= ntiles) break;
+    const uint32_t outer = tile_outer(t);
+    C v[16][NV];
+    mbar_wait(&full_bar[grp], (uint32_t)k & 1u);
+
+    // pass 0: shared -> registers
+    uint32_t ts = (uint32_t)lane, tg = outer | ((uint32_t)lane << VB);
+#pragma unroll
+    for (int s = 0; s < 3; ++s)
+      if ((wl >> s) & 1) {
+        ts |= 1u << (5 + p.wsel[0][s]);
+        tg |= 1u << p.hb[p.wsel[0][s]];
+      }
+#pragma unroll
+    for (int r = 0; r < 16; ++r) unpack<R, NV>(tile[slot_smem(ts, p.gsel[0], r)], v[r]);
+    if constexpr (PRE == 1) apply_split<R, NV>(v, tg, p.pre, p.pre_s, tab_pre);
+    low_gates<R, NV>(v, p, lane);
+    reg_gates<R, NV>(v, p.gkind[0]);
+
+    if constexpr (NPASS == 2) {
+#pragma unroll
+      for (int r = 0; r < 16; ++r) tile[slot_smem(ts, p.gsel[0], r)] = pack<R, NV>(v[r]);
+      asm volatile("bar.sync %0, 256;" ::"r"(1 + grp) : "memory");
+      ts = (uint32_t)lane;
+      tg = outer | ((uint32_t)lane << VB);
+#pragma unroll
+      for (int s = 0; s < 3; ++s)
+        if ((wl >> s) & 1) {
+          ts |= 1u << (5 + p.wsel[1][s]);
+          tg |= 1u << p.hb[p.wsel[1][s]];
+        }
+#pragma unroll
+      for (int r = 0; r < 16; ++r) unpack<R, NV>(tile[slot_smem(ts, p.gsel[1], r)], v[r]);
+      // the stage is rewritten by TMA next: order our generic-proxy writes before it
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty_bar[grp]);
+    if constexpr (NPASS == 2) reg_gates<R, NV>(v, p.gkind[1]);
+
+    constexpr int QL = NPASS - 1;
+    if (p.post.active) apply_split<R, NV>(v, tg, p.post, p.post_s, tab_post);
+    V *d0 = dst + (tg >> VB);
+#pragma unroll
+    for (int r = 0; r < 16; ++r) {
+      uint32_t off = 0;
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk)
+        if (r & (1 << kk)) off |= 1u << (p.hb[p.gsel[QL][kk]] - VB);
+      d0[off] = pack<R, NV>(v[r]);
+    }
+  }
+}
+
+template <typename R, int PRE, int NPASS>
+static cudaError_t launch_tma_t(const TileSweepParams &p, int grid, cudaStream_t s) {
+  tile_sweep_tma_kernel<R, PRE, NPASS><<<grid, 544, (size_t)kTmaStages * kTileBytes, s>>>(p);
+  return cudaGetLastError();
+}
+
+template <typename R>
+static cudaError_t launch_tma_r(const TileSweepParams &p, int pre_mode, int npass, int grid, cudaStream_t s) {
+  if (npass == 1) return pre_mode ? launch_tma_t<R, 1, 1>(p, grid, s) : launch_tma_t<R, 0, 1>(p, grid, s);
+  return pre_mode ? launch_tma_t<R, 1, 2>(p, grid, s) : launch_tma_t<R, 0, 2>(p, grid, s);
+}
+
+cudaError_t launch_tile_sweep_tma(const TileSweepParams &p, bool c128, int pre_mode, int npass, int grid,
+                                  cudaStream_t s) {
+  return c128 ? launch_tma_r<double>(p, pre_mode, npass, grid, s)
+              : launch_tma_r<float>(p, pre_mode, npass, grid, s);
+}
+
+template <typename R>
+static cudaError_t tma_setup_r() {
+  const int bytes = kTmaStages * kTileBytes;
+  cudaError_t e;
+  if ((e = cudaFuncSetAttribute(tile_sweep_tma_kernel<R, 0, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                bytes)) != cudaSuccess)
+    return e;
+  if ((e = cudaFuncSetAttribute(tile_sweep_tma_kernel<R, 1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                bytes)) != cudaSuccess)
+    return e;
+  if ((e = cudaFuncSetAttribute(tile_sweep_tma_kernel<R, 0, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                bytes)) != cudaSuccess)
+    return e;
+  return cudaFuncSetAttribute(tile_sweep_tma_kernel<R, 1, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+}
+
+cudaError_t tile_sweep_tma_setup(bool c128) { return c128 ? tma_setup_r<double>() : tma_setup_r<float>(); }
+
+}  // namespace qsim

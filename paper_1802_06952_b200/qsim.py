@@ -27,7 +27,7 @@ STATUS_NAMES = {0: "QSIM_OK", 2: "QSIM_EINVAL", 3: "QSIM_ENOMEM", 4: "QSIM_ENUME
 QSIM_C64, QSIM_C128 = 0, 1
 QSIM_SX, QSIM_SY, QSIM_T, QSIM_CZ = 1, 2, 3, 4
 QSIM_NO_QUBIT = 0xFFFFFFFF
-QSIM_OPT_TIME_SWEEPS, QSIM_OPT_MODE, QSIM_OPT_MEM_BUDGET = 1, 2, 3
+QSIM_OPT_TIME_SWEEPS, QSIM_OPT_MODE, QSIM_OPT_MEM_BUDGET, QSIM_OPT_SWEEP_KERNEL = 1, 2, 3, 4
 
 EXPORTED = ["qsim_create", "qsim_destroy", "qsim_last_error", "qsim_version", "qsim_set_option",
             "qsim_set_stream", "qsim_load_circuit", "qsim_partition", "qsim_set_blocks",
@@ -174,8 +174,12 @@ def qsim_amplitudes(ctx, upper_block, lower_block, prec: int, out=None, write=Tr
     return out
 
 
-def qsim_sample(ctx, seed: int, n_draws: int, to_host: bool = True):
-    out = np.empty(n_draws, dtype=np.uint64) if to_host else None
+def qsim_sample(ctx, seed: int, n_draws: int, to_host: bool = True, out=None):
+    if to_host and out is None:
+        out = np.empty(n_draws, dtype=np.uint64)
+    if not to_host:
+        out = None
+    assert out is None or (out.dtype == np.uint64 and out.size >= n_draws)
     mass = C.c_double(0.0)
     _check(ctx, _lib.qsim_sample(ctx, seed, n_draws, _ptr(out), C.byref(mass) if to_host else None))
     return out, mass.value
