@@ -76,6 +76,7 @@ typedef struct {
   double gemm_flops;         /* 8*M*N*K of the reconstruction GEMMs                      */
   double gemm_ms;            /* CUDA-event time of GEMM launches (QSIM_OPT_TIME_SWEEPS)  */
   uint64_t branches_evolved; /* branch pairs whose slices were gathered                  */
+  uint64_t lazy_gathers;     /* leaves whose last sweep was evaluated at the sampled indices only */
 } qsim_stats_t;
 
 typedef enum {
@@ -83,7 +84,9 @@ typedef enum {
   QSIM_OPT_MODE = 2,        /* 0: auto, 1: flat in-shared-memory per-branch kernel (h <= 12),
                                2: prefix-shared branch tree of tile sweeps (h >= 13)          */
   QSIM_OPT_MEM_BUDGET = 3,  /* cap in bytes on device memory for half-state buffers (0 = free memory) */
-  QSIM_OPT_SWEEP_KERNEL = 4 /* 0: TMA-pipelined sweep (default), 1: register-only sweep (comparison) */
+  QSIM_OPT_SWEEP_KERNEL = 4, /* 0: TMA-pipelined sweep (default), 1: register-only sweep (comparison) */
+  QSIM_OPT_LAZY_LAST = 5     /* 1 (default): each leaf's last sweep is evaluated only at the sampled
+                                indices during the gather (2^k reads per index instead of a 2^h pass) */
 } qsim_option;
 
 /* Create a context bound to CUDA device `device` (no device call is made until the

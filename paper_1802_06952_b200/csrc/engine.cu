@@ -183,6 +183,10 @@ void Engine::set_option(int key, int64_t value) {
       if (value < 0) throw Error(QSIM_EINVAL, "memory budget must be >= 0");
       mem_budget_ = value;
       return;
+    case QSIM_OPT_LAZY_LAST:
+      if (value < 0 || value > 1) throw Error(QSIM_EINVAL, "QSIM_OPT_LAZY_LAST must be 0 or 1");
+      lazy_last_ = value != 0;
+      return;
     case QSIM_OPT_SWEEP_KERNEL:
       if (value < 0 || value > 1) throw Error(QSIM_EINVAL, "QSIM_OPT_SWEEP_KERNEL must be 0 or 1");
       sweep_kernel_ = (int)value;
@@ -498,26 +502,50 @@ void Engine::launch_plan(const TilePlan &tp, const Diag &fork, bool first, const
   st_.sweep_bytes += (tp.gen ? 1.0 : 2.0) * std::ldexp(1.0, h) * (double)amp_ * p.njobs;
 }
 
-// Runs the sweeps of `level` for fork child `child`; returns where the state ended.
-void Engine::run_level(int half, int level, uint64_t child, const void *src, void *dst) {
+// Runs the sweeps of `level` for fork child `child` (all but the last with skip_last);
+// returns where the state ended (src when no sweep ran).
+const void *Engine::run_level(int half, int level, uint64_t child, const void *src, void *dst, bool skip_last) {
   HalfExec &he = half_[half];
   const Level &lev = he.prog.levels[level];
   const Diag fork = he.prog.fork_diag(level, child);
-  for (size_t s = 0; s < lev.sweeps.size(); ++s) {
+  const size_t n = lev.sweeps.size() - (skip_last && !lev.sweeps.empty() ? 1 : 0);
+  for (size_t s = 0; s < n; ++s) {
     const auto &chunks = he.plans[level][s];
     for (size_t ci = 0; ci < chunks.size(); ++ci) {
       const bool first = s == 0 && ci == 0;
       launch_plan(chunks[ci], first ? fork : Diag(), first, first ? src : dst, dst, he.prog.h);
     }
   }
+  return n ? dst : src;
 }
 
+// Leaf gather.  lazy: the leaf level's last sweep is evaluated only at the sampled
+// indices (gather_layer); else psi is the complete leaf (pending fork diagonal applied).
 void Engine::gather_leaf(int half, uint64_t child_last, const void *psi, const uint64_t *dS, int64_t nS,
-                         void *out_row) {
+                         void *out_row, bool lazy) {
   HalfExec &he = half_[half];
   const int F = (int)he.prog.levels.size() - 1;
+  const Level &lev = he.prog.levels[F];
+  if (lazy) {
+    const Sweep &sw = lev.sweeps.back();
+    LazyLayer ll;
+    std::memset(&ll, 0, sizeof(ll));
+    ll.k = (int)sw.gates.size();
+    for (size_t t = 0; t < sw.gates.size(); ++t) {
+      ll.bit[t] = sw.gates[t].bit;
+      ll.tmask |= 1u << sw.gates[t].bit;
+      (sw.gates[t].kind == 1 ? ll.sxmask : ll.symask) |= 1u << sw.gates[t].bit;
+    }
+    const Diag pre = lev.sweeps.size() == 1 ? Diag::merge(he.prog.fork_diag(F, child_last), sw.pre) : sw.pre;
+    ll.pre = to_dev(pre, he.prog.vs);
+    ll.post = to_dev(sw.post, he.prog.vs, true);
+    check(launch_gather_layer(psi, dS, nS, out_row, ll, c128_, stream_), "gather_layer launch");
+    st_.kernel_launches++;
+    st_.lazy_gathers++;
+    return;
+  }
   Diag pend;
-  if (F >= 1 && he.prog.levels[F].sweeps.empty()) pend = he.prog.fork_diag(F, child_last);
+  if (F >= 1 && lev.sweeps.empty()) pend = he.prog.fork_diag(F, child_last);
   check(launch_gather(psi, dS, nS, out_row, to_dev(pend, he.prog.vs), c128_, stream_), "gather launch");
   st_.kernel_launches++;
 }
@@ -590,14 +618,18 @@ void Engine::evolve_half(int half, uint64_t b0, uint64_t b1, void *slice, const 
   std::vector<int> sbits(F + 1, 0);  // cut bits consumed up to and including level l
   for (int l = 1; l <= F; ++l) sbits[l] = sbits[l - 1] + hp.levels[l].k;
   auto buf = [&](int l) { return states_[std::max(l, m0) - m0]->ptr; };
+  // lazy last layer: skip the leaf level's last sweep, evaluate it at the sampled indices
+  const bool lazy = lazy_last_ && !full_leaf_ && F >= 1 && !hp.levels[F].sweeps.empty() &&
+                    hp.levels[F].sweeps.back().gates.size() <= 12;
+  auto skip = [&](int l) { return lazy && l == F; };
 
   // recompute levels 0..lt along the path of prefix `cp` in place in buf(m0)
   auto recompute_path = [&](int lt, uint64_t cp) {
     void *b = buf(m0);
-    run_level(half, 0, 0, nullptr, b);
+    run_level(half, 0, 0, nullptr, b, skip(0));
     for (int l = 1; l <= lt; ++l) {
       const uint64_t ch = (cp >> (sbits[lt] - sbits[l])) & ((1ull << hp.levels[l].k) - 1ull);
-      run_level(half, l, ch, b, b);
+      run_level(half, l, ch, b, b, skip(l));
     }
   };
 
@@ -605,7 +637,7 @@ void Engine::evolve_half(int half, uint64_t b0, uint64_t b1, void *slice, const 
     if (l == F) {
       const uint64_t b = prefix;
       const uint64_t ch = F >= 1 ? (b & ((1ull << hp.levels[F].k) - 1ull)) : 0;
-      gather_leaf(half, ch, state, dS, nS, (char *)slice + (b - b0) * (uint64_t)nS * amp_);
+      gather_leaf(half, ch, state, dS, nS, (char *)slice + (b - b0) * (uint64_t)nS * amp_, lazy);
       return;
     }
     const int k = hp.levels[l + 1].k;
@@ -620,15 +652,12 @@ void Engine::evolve_half(int half, uint64_t b0, uint64_t b1, void *slice, const 
         recompute_path(m0, cp);
         node(m0, cp, buf(m0));
       } else {
-        void *dst = buf(l + 1);
-        run_level(half, l + 1, ch, state, dst);
-        node(l + 1, cp, hp.levels[l + 1].sweeps.empty() ? state : dst);
+        node(l + 1, cp, run_level(half, l + 1, ch, state, buf(l + 1), skip(l + 1)));
       }
     }
   };
   if (m0 == 0) {
-    run_level(half, 0, 0, nullptr, buf(0));
-    node(0, 0, buf(0));
+    node(0, 0, run_level(half, 0, 0, nullptr, buf(0), false));
   } else {
     node(0, 0, nullptr);
   }
@@ -814,7 +843,14 @@ void Engine::branch_state(int half, uint64_t b, void *out) {
   check(cudaMemcpyAsync(tmp_.ptr, all.data(), n * 8, cudaMemcpyHostToDevice, stream_), "upload S");
   DevBuf slice;
   slice.reserve(n * amp_);
-  evolve_half(half, b, b + 1, slice.ptr, tmp_.as<uint64_t>(), (int64_t)n);
+  full_leaf_ = true;
+  try {
+    evolve_half(half, b, b + 1, slice.ptr, tmp_.as<uint64_t>(), (int64_t)n);
+  } catch (...) {
+    full_leaf_ = false;
+    throw;
+  }
+  full_leaf_ = false;
   check(cudaMemcpyAsync(out, slice.ptr, n * amp_, cudaMemcpyDeviceToHost, stream_), "D2H state");
   check(cudaStreamSynchronize(stream_), "branch_state");
 }

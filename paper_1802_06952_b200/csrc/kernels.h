@@ -116,6 +116,18 @@ int small_max_h(bool c128);
 // out[j] = psi[S[j]] * pend(S[j])
 cudaError_t launch_gather(const void *psi, const uint64_t *S, int64_t n, void *out,
                           const DiagDev &pend, bool c128, cudaStream_t s);
+
+// Lazy last layer: the leaf's final sweep evaluated only at the sampled indices,
+//   out[j] = post(x) * sum_y  prod_t M'_t[x_t, y_t] * pre(y) * psi[y],   x = S[j],
+// y ranging over the 2^k values of the sweep's target bits (others equal to x).
+struct LazyLayer {
+  int32_t k;
+  uint8_t bit[24];
+  uint32_t sxmask, symask, tmask;
+  DiagDev pre, post;
+};
+cudaError_t launch_gather_layer(const void *psi, const uint64_t *S, int64_t n, void *out,
+                                const LazyLayer &ll, bool c128, cudaStream_t s);
 // A[m, n] += sum_k U[k, m] * L[k, n]   (complex; U, L of the ctx precision, A double2)
 cudaError_t launch_branch_gemm(const void *U, const void *L, int64_t K, int64_t M, int64_t N,
                                double *A, bool c128, cudaStream_t s);

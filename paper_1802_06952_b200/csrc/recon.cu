@@ -7,7 +7,7 @@
 //     A[i, j] = sum_b U[b, i] * L[b, j].
 #include <algorithm>
 
-#include "kernels.h"
+#include "sweep_common.cuh"
 
 namespace qsim {
 
@@ -22,10 +22,6 @@ struct CxT<double> {
   using T = double2;
 };
 
-static __constant__ double c_omega[16] = {1.0, 0.0, 0.70710678118654752440, 0.70710678118654752440, 0.0, 1.0,
-                                   -0.70710678118654752440, 0.70710678118654752440, -1.0, 0.0,
-                                   -0.70710678118654752440, -0.70710678118654752440, 0.0, -1.0,
-                                   0.70710678118654752440, -0.70710678118654752440};
 
 // ---------------------------------------------------------------- gather
 template <typename R>
@@ -60,6 +56,67 @@ cudaError_t launch_gather(const void *psi, const uint64_t *S, int64_t n, void *o
     gather_kernel<double><<<blocks, threads, 0, s>>>((const double2 *)psi, S, n, (double2 *)out, pend);
   else
     gather_kernel<float><<<blocks, threads, 0, s>>>((const float2 *)psi, S, n, (float2 *)out, pend);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------- lazy last layer
+// One warp per sampled index x: lanes split the 2^k input combinations y, each term is
+// w^{ph(x,y)} pre(y) psi[y] with ph = 6 popc((x^y) & SX) + 4 popc(~x & y & SY) (the
+// factored matrices SX' = [[1,-i],[-i,1]], SY' = [[1,-1],[1,1]]); warp sum, then post(x).
+template <typename R>
+__global__ void __launch_bounds__(256) gather_layer_kernel(const typename CxT<R>::T *__restrict__ psi,
+                                                           const uint64_t *__restrict__ S, int64_t n,
+                                                           typename CxT<R>::T *__restrict__ out,
+                                                           const __grid_constant__ LazyLayer ll) {
+  using C = typename CxT<R>::T;
+  const int lane = threadIdx.x & 31;
+  const int64_t j = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (j >= n) return;
+  const uint32_t x = (uint32_t)S[j];
+  const uint32_t base = x & ~ll.tmask;
+  const uint32_t nterm = 1u << ll.k;
+  R sr = 0, si = 0;
+  for (uint32_t m = lane; m < nterm; m += 32) {
+    uint32_t y = base;
+#pragma unroll 4
+    for (int t = 0; t < ll.k; ++t) y |= ((m >> t) & 1u) << ll.bit[t];
+    C v = psi[y];
+    int ph = 6 * __popc((x ^ y) & ll.sxmask) + 4 * __popc(~x & y & ll.symask);
+    if (ll.pre.active) {
+      ph += diag_phase(y, ll.pre, ll.pre.zm);
+      if ((y & ll.pre.pm) != ll.pre.pv) v.x = v.y = (R)0;
+    }
+    ph &= 7;
+    const R wr = (R)c_omega[2 * ph], wi = (R)c_omega[2 * ph + 1];
+    sr += v.x * wr - v.y * wi;
+    si += v.x * wi + v.y * wr;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    sr += __shfl_xor_sync(0xffffffffu, sr, o);
+    si += __shfl_xor_sync(0xffffffffu, si, o);
+  }
+  if (lane == 0) {
+    const double pre_scale = ll.pre.active ? ll.pre.scale : 1.0;
+    const int ph = diag_phase(x, ll.post, ll.post.zm);
+    const double sc = ll.post.scale * pre_scale;
+    const R wr = (R)(c_omega[2 * ph] * sc), wi = (R)(c_omega[2 * ph + 1] * sc);
+    C o;
+    o.x = sr * wr - si * wi;
+    o.y = sr * wi + si * wr;
+    if ((x & ll.post.pm) != ll.post.pv) o.x = o.y = (R)0;
+    out[j] = o;
+  }
+}
+
+cudaError_t launch_gather_layer(const void *psi, const uint64_t *S, int64_t n, void *out, const LazyLayer &ll,
+                                bool c128, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  const int64_t blocks = (n * 32 + 255) / 256;
+  if (c128)
+    gather_layer_kernel<double><<<(unsigned)blocks, 256, 0, s>>>((const double2 *)psi, S, n, (double2 *)out, ll);
+  else
+    gather_layer_kernel<float><<<(unsigned)blocks, 256, 0, s>>>((const float2 *)psi, S, n, (float2 *)out, ll);
   return cudaGetLastError();
 }
 

@@ -27,7 +27,7 @@ STATUS_NAMES = {0: "QSIM_OK", 2: "QSIM_EINVAL", 3: "QSIM_ENOMEM", 4: "QSIM_ENUME
 QSIM_C64, QSIM_C128 = 0, 1
 QSIM_SX, QSIM_SY, QSIM_T, QSIM_CZ = 1, 2, 3, 4
 QSIM_NO_QUBIT = 0xFFFFFFFF
-QSIM_OPT_TIME_SWEEPS, QSIM_OPT_MODE, QSIM_OPT_MEM_BUDGET, QSIM_OPT_SWEEP_KERNEL = 1, 2, 3, 4
+QSIM_OPT_TIME_SWEEPS, QSIM_OPT_MODE, QSIM_OPT_MEM_BUDGET, QSIM_OPT_SWEEP_KERNEL, QSIM_OPT_LAZY_LAST = 1, 2, 3, 4, 5
 
 EXPORTED = ["qsim_create", "qsim_destroy", "qsim_last_error", "qsim_version", "qsim_set_option",
             "qsim_set_stream", "qsim_load_circuit", "qsim_partition", "qsim_set_blocks",
@@ -44,7 +44,8 @@ class qsim_cut(C.Structure):
 class qsim_stats_t(C.Structure):
     _fields_ = [("kernel_launches", C.c_uint64), ("sweeps", C.c_uint64), ("sweep_states", C.c_uint64),
                 ("sweep_bytes", C.c_double), ("sweep_ms", C.c_double), ("timed_sweeps", C.c_uint64),
-                ("gemm_flops", C.c_double), ("gemm_ms", C.c_double), ("branches_evolved", C.c_uint64)]
+                ("gemm_flops", C.c_double), ("gemm_ms", C.c_double), ("branches_evolved", C.c_uint64),
+                ("lazy_gathers", C.c_uint64)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}

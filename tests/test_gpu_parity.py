@@ -31,13 +31,15 @@ def assert_close(a, ref, prec, what=""):
         assert rel <= 1e-5, f"{what} c64 max abs err / max|a| {rel:.3e}"
 
 
-def run_block(circ, S_u, S_l, prec, mode=0, budget=0, ranges=None):
+def run_block(circ, S_u, S_l, prec, mode=0, budget=0, ranges=None, opts=None):
     ctx = Q.qsim_create(prec, 0)
     try:
         if mode:
             Q.qsim_set_option(ctx, Q.QSIM_OPT_MODE, mode)
         if budget:
             Q.qsim_set_option(ctx, Q.QSIM_OPT_MEM_BUDGET, budget)
+        for k, v in (opts or {}).items():
+            Q.qsim_set_option(ctx, k, v)
         Q.qsim_load_circuit(ctx, circ.rows, circ.cols, circ.depth, circ.gate_array(), circ.cut_row)
         if ranges is None:
             Q.qsim_evolve_halves(ctx, S_u, S_l)
@@ -124,6 +126,15 @@ def h14_reference():
 def test_tree_mode_h14(prec, h14_reference):
     circ, Su, Sl, ref = h14_reference
     assert_close(run_block(circ, Su, Sl, prec), ref, prec, "h14 tree")
+
+
+@pytest.mark.parametrize("prec", PRECS, ids=PNAME.get)
+@pytest.mark.parametrize("lazy,kernel", [(0, 0), (1, 1), (0, 1)])
+def test_tree_mode_h14_variants(prec, lazy, kernel, h14_reference):
+    """Full last sweep instead of the lazy gather; register-only sweep kernel instead of TMA."""
+    circ, Su, Sl, ref = h14_reference
+    A = run_block(circ, Su, Sl, prec, opts={Q.QSIM_OPT_LAZY_LAST: lazy, Q.QSIM_OPT_SWEEP_KERNEL: kernel})
+    assert_close(A, ref, prec, f"h14 lazy={lazy} kernel={kernel}")
 
 
 @pytest.mark.parametrize("prec", PRECS, ids=PNAME.get)
