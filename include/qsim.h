@@ -84,7 +84,8 @@ typedef enum {
   QSIM_OPT_MODE = 2,        /* 0: auto, 1: flat in-shared-memory per-branch kernel (h <= 12),
                                2: prefix-shared branch tree of tile sweeps (h >= 13)          */
   QSIM_OPT_MEM_BUDGET = 3,  /* cap in bytes on device memory for half-state buffers (0 = free memory) */
-  QSIM_OPT_SWEEP_KERNEL = 4, /* 0: TMA-pipelined sweep (default), 1: register-only sweep (comparison) */
+  QSIM_OPT_SWEEP_KERNEL = 4, /* 0: TMA-pipelined sweep, 2 smem stages (default); 1: register-only sweep;
+                                2: TMA-pipelined sweep, 3 smem stages                                   */
   QSIM_OPT_LAZY_LAST = 5     /* 1 (default): each leaf's last sweep is evaluated only at the sampled
                                 indices during the gather (2^k reads per index instead of a 2^h pass) */
 } qsim_option;

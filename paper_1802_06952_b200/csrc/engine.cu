@@ -3,6 +3,8 @@
 #include "engine.h"
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <functional>
 #include <sstream>
@@ -188,7 +190,7 @@ void Engine::set_option(int key, int64_t value) {
       lazy_last_ = value != 0;
       return;
     case QSIM_OPT_SWEEP_KERNEL:
-      if (value < 0 || value > 1) throw Error(QSIM_EINVAL, "QSIM_OPT_SWEEP_KERNEL must be 0 or 1");
+      if (value < 0 || value > 2) throw Error(QSIM_EINVAL, "QSIM_OPT_SWEEP_KERNEL must be 0, 1 or 2");
       sweep_kernel_ = (int)value;
       return;
     default:
@@ -328,6 +330,12 @@ void Engine::compile_plans(HalfExec &he) {
         int m = 0;
         while (m < kHiBits && hb[m] == L + m) ++m;
         tp.p.run_m = m;
+        if (std::getenv("QSIM_DEBUG_PLANS")) {
+          std::fprintf(stderr, "%s L%zu S%zu c%d layers %d-%d: npass %d hi[", hp.upper ? "U" : "D", l, s, ci,
+                       sw.first_layer, sw.last_layer, tp.npass);
+          for (int j = 0; j < kHiBits; ++j) std::fprintf(stderr, "%s%d%s", j ? " " : "", hb[j], kind_of(hb[j]) ? "*" : "");
+          std::fprintf(stderr, "] run_m %d lanes %d low0 %d\n", m, tp.p.n_lane, tp.p.lowkind[0]);
+        }
         he.plans[l][s].push_back(tp);
       }
     }
@@ -475,7 +483,7 @@ void Engine::launch_plan(const TilePlan &tp, const Diag &fork, bool first, const
   p.job_pv[0] = p.pre.pv;
   p.job_zm[0] = p.pre.zm;
   const uint64_t tiles = (1ull << p.log2_ntiles) * (uint64_t)p.njobs;
-  const bool tma = sweep_kernel_ == 0 && pre_mode != 2 && p.njobs == 1;
+  const bool tma = sweep_kernel_ != 1 && pre_mode != 2 && p.njobs == 1;
   if (tma && pre_mode == 1) p.pre_s = make_split(pre, vs, reg_positions(p, 0, c128_));
   const int occ = tma ? 1 : (tp.npass == 1 ? occ1_ : occ2_);
   const int grid = (int)std::min<uint64_t>(tiles, (uint64_t)num_sms_ * occ);
@@ -487,7 +495,8 @@ void Engine::launch_plan(const TilePlan &tp, const Diag &fork, bool first, const
     check(cudaEventRecord(e0, stream_), "cudaEventRecord");
   }
   if (tma)
-    check(launch_tile_sweep_tma(p, c128_, pre_mode, tp.npass, grid, stream_), "tma sweep launch");
+    check(launch_tile_sweep_tma(p, c128_, pre_mode, tp.npass, grid, stream_, sweep_kernel_ == 2 ? 3 : 2),
+          "tma sweep launch");
   else
     check(launch_tile_sweep(p, c128_, pre_mode, tp.npass, grid, stream_), "tile sweep launch");
   if (timed) {

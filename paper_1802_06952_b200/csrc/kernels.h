@@ -74,9 +74,8 @@ cudaError_t launch_tile_sweep(const TileSweepParams &p, bool c128, int pre_mode,
 // stages filled by cp.async.bulk under mbarriers, 1 producer warp + two ping-pong groups
 // of 8 consumer warps (each group owns alternate tiles).
 cudaError_t launch_tile_sweep_tma(const TileSweepParams &p, bool c128, int pre_mode, int npass,
-                                  int grid, cudaStream_t s);
+                                  int grid, cudaStream_t s, int stages);
 cudaError_t tile_sweep_tma_setup(bool c128);
-constexpr int kTmaStages = 2;  // one stage per consumer group
 constexpr int kTileBytes = 65536;
 int tile_low_bits(bool c128);  // L: 6 (c64) or 5 (c128); tile T = L + 7
 cudaError_t tile_sweep_setup(int *blocks_per_sm_1pass, int *blocks_per_sm_2pass, bool c128);

@@ -1,14 +1,15 @@
 // TMA-pipelined gate sweep for sm_100a (the hot loop of SURVEY §8(a) a3/a4).
 //
-// One persistent CTA per SM: warp 8 is the producer, which streams each 64 KB tile
-// (2^T amplitudes gathered from 2^(7-m) contiguous runs) into one of 3 shared-memory
-// stages with cp.async.bulk, completing on the stage's "full" mbarrier.  Warps 0-7
-// consume: they move the tile from shared memory into registers (16-byte vectors,
-// conflict-free), apply every X^1/2 / Y^1/2 target of the layer (registers, warp
-// shuffles for lane bits, a second register mapping through the same stage when more
-// than 4 high targets), release the stage on its "empty" mbarrier as soon as the last
-// shared-memory read is done, apply the fused diagonal and store straight to HBM.
-// Loads of the next two tiles are therefore always in flight while a tile is computed.
+// One persistent CTA per SM (544 threads): warp 16 is the producer, which streams each
+// 64 KB tile (2^T amplitudes gathered from 2^(7-m) contiguous runs) into one of 3
+// shared-memory stages with cp.async.bulk, completing on a "full" mbarrier.  Warps 0-15
+// are two ping-pong consumer groups of 8 warps taking alternate tiles: a group moves
+// its tile from shared memory into registers (16-byte vectors, conflict-free), applies
+// every X^1/2 / Y^1/2 target of the layer (registers, warp shuffles for lane bits, a
+// second register mapping through the same stage when more than 4 high targets),
+// releases the stage on its "empty" mbarrier as soon as its last shared-memory read is
+// done, applies the fused diagonal and stores straight to HBM.  While one group waits
+// or computes, the other group and the next tile's TMA keep the memory system busy.
 //
 // The fused diagonal (§2.4, Eqs. 3-6) is evaluated through the host-computed
 // DiagSplit decomposition: per element one add, one table lookup and one complex
@@ -191,7 +192,7 @@ __device__ __forceinline__ uint32_t slot_smem(uint32_t base, const uint8_t *gsel
   return si;
 }
 
-template <typename R, int PRE, int NPASS>
+template <typename R, int PRE, int NPASS, int NST>
 __global__ void __launch_bounds__(544, 1) tile_sweep_tma_kernel(const __grid_constant__ TileSweepParams p) {
   using C = typename Cx2<R>::T;
   using V = typename Cx2<R>::V;
@@ -201,7 +202,7 @@ __global__ void __launch_bounds__(544, 1) tile_sweep_tma_kernel(const __grid_con
   constexpr int NVEC = kTileBytes / 16;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   V *stages = reinterpret_cast<V *>(smem_raw);
-  __shared__ __align__(8) uint64_t full_bar[kTmaStages], empty_bar[kTmaStages];
+  __shared__ __align__(8) uint64_t full_bar[NST][2], empty_bar[NST];
   __shared__ __align__(16) C tab_pre[8], tab_post[8];
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -211,9 +212,13 @@ __global__ void __launch_bounds__(544, 1) tile_sweep_tma_kernel(const __grid_con
     tab_post[tid].x = (R)(c_omega[2 * tid] * p.post.scale);
     tab_post[tid].y = (R)(c_omega[2 * tid + 1] * p.post.scale);
   }
+  // long contiguous runs: one cp.async.bulk per run (1 arrival + tx bytes); short runs
+  // (< 2 KB): per-lane 16-byte cp.async, a warp instruction per 512-byte row (32 arrivals)
+  const bool bulk = p.run_m >= 2;
   if (tid == 0) {
-    for (int s = 0; s < kTmaStages; ++s) {
-      mbar_init(&full_bar[s], 1);
+    for (int s = 0; s < NST; ++s) {
+      mbar_init(&full_bar[s][0], bulk ? 1 : 32);
+      mbar_init(&full_bar[s][1], bulk ? 1 : 32);
       mbar_init(&empty_bar[s], 8);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -241,19 +246,36 @@ __global__ void __launch_bounds__(544, 1) tile_sweep_tma_kernel(const __grid_con
     for (int it = 0;; ++it) {
       const uint64_t t = blockIdx.x + (uint64_t)it * gridDim.x;
       if (t >= ntiles) break;
-      const int s = it & 1;
-      const uint32_t par = (uint32_t)(it >> 1) & 1u;
+      const int s = it % NST;
+      const uint32_t par = (uint32_t)(it / NST) & 1u;
       mbar_wait(&empty_bar[s], par ^ 1u);
-      if (lane == 0) mbar_arrive_expect_tx(&full_bar[s], kTileBytes);
-      __syncwarp();
+      uint64_t *fb = &full_bar[s][it & 1];
       const uint32_t outer = tile_outer(t);
       char *stage = reinterpret_cast<char *>(stages + (size_t)s * NVEC);
-      for (int q = lane; q < nruns; q += 32) {
-        uint32_t gi = outer;
-        for (int j = 0; j < rbits; ++j)
-          if ((q >> j) & 1) gi |= 1u << p.hb[m + j];
-        bulk_g2s(stage + ((size_t)q << run_log2) * sizeof(C), src + (size_t)gi * sizeof(C), run_bytes,
-                 &full_bar[s]);
+      if (bulk) {
+        if (lane == 0) mbar_arrive_expect_tx(fb, kTileBytes);
+        __syncwarp();
+        for (int q = lane; q < nruns; q += 32) {
+          uint32_t gi = outer;
+          for (int j = 0; j < rbits; ++j)
+            if ((q >> j) & 1) gi |= 1u << p.hb[m + j];
+          bulk_g2s(stage + ((size_t)q << run_log2) * sizeof(C), src + (size_t)gi * sizeof(C), run_bytes, fb);
+        }
+      } else {
+        // vector vi = lane + 32 q: row q of the tile = deposit of q's 7 bits on hb[]
+        uint32_t hmask = 0;
+        for (int j = 0; j < kHiBits; ++j) hmask |= 1u << p.hb[j];
+        const char *srcl = src + (size_t)(outer | ((uint32_t)lane << VB)) * sizeof(C);
+        char *dstl = stage + (size_t)lane * 16;
+        uint32_t d = 0;
+#pragma unroll 8
+        for (int q = 0; q < NVEC / 32; ++q) {
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_addr(dstl + (size_t)q * 512)),
+                       "l"(srcl + (size_t)d * sizeof(C))
+                       : "memory");
+          d = ((d | ~hmask) + 1u) & hmask;
+        }
+        asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_addr(fb)) : "memory");
       }
     }
     return;
@@ -261,15 +283,20 @@ __global__ void __launch_bounds__(544, 1) tile_sweep_tma_kernel(const __grid_con
 
   // -------------------------------------------------- two ping-pong consumer groups
   const int grp = warp >> 3, wl = warp & 7;
-  V *tile = stages + (size_t)grp * NVEC;
   V *dst = reinterpret_cast<V *>(p.dst[0]);
   for (int k = 0;; ++k) {
-    const int it = 2 * k + grp;
+    const int it = 2 * k + grp;  // global tile order: the groups alternate
     const uint64_t t = blockIdx.x + (uint64_t)it * gridDim.x;
     if (t >= ntiles) break;
+    const int s = it % NST;
+    V *tile = stages + (size_t)s * NVEC;
     const uint32_t outer = tile_outer(t);
     C v[16][NV];
-    mbar_wait(&full_bar[grp], (uint32_t)k & 1u);
+    // full_bar[s][grp] is used by this group only, once per use of stage s: with 2 stages
+    // the group always uses stage grp (k-th use); with 3 its tiles cycle the stages
+    // (2k + grp mod 3), so the k-th tile is the (k / 3)-th use of its stage
+    const uint32_t use = NST == 2 ? (uint32_t)k : (uint32_t)(k / 3);
+    mbar_wait(&full_bar[s][grp], use & 1u);
 
     // pass 0: shared -> registers
     uint32_t ts = (uint32_t)lane, tg = outer | ((uint32_t)lane << VB);
@@ -303,7 +330,7 @@ __global__ void __launch_bounds__(544, 1) tile_sweep_tma_kernel(const __grid_con
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     }
     __syncwarp();
-    if (lane == 0) mbar_arrive(&empty_bar[grp]);
+    if (lane == 0) mbar_arrive(&empty_bar[s]);
     if constexpr (NPASS == 2) reg_gates<R, NV>(v, p.gkind[1]);
 
     constexpr int QL = NPASS - 1;
@@ -320,40 +347,44 @@ __global__ void __launch_bounds__(544, 1) tile_sweep_tma_kernel(const __grid_con
   }
 }
 
-template <typename R, int PRE, int NPASS>
+template <typename R, int PRE, int NPASS, int NST>
 static cudaError_t launch_tma_t(const TileSweepParams &p, int grid, cudaStream_t s) {
-  tile_sweep_tma_kernel<R, PRE, NPASS><<<grid, 544, (size_t)kTmaStages * kTileBytes, s>>>(p);
+  tile_sweep_tma_kernel<R, PRE, NPASS, NST><<<grid, 544, (size_t)NST * kTileBytes, s>>>(p);
   return cudaGetLastError();
 }
 
-template <typename R>
+template <typename R, int NST>
 static cudaError_t launch_tma_r(const TileSweepParams &p, int pre_mode, int npass, int grid, cudaStream_t s) {
-  if (npass == 1) return pre_mode ? launch_tma_t<R, 1, 1>(p, grid, s) : launch_tma_t<R, 0, 1>(p, grid, s);
-  return pre_mode ? launch_tma_t<R, 1, 2>(p, grid, s) : launch_tma_t<R, 0, 2>(p, grid, s);
+  if (npass == 1)
+    return pre_mode ? launch_tma_t<R, 1, 1, NST>(p, grid, s) : launch_tma_t<R, 0, 1, NST>(p, grid, s);
+  return pre_mode ? launch_tma_t<R, 1, 2, NST>(p, grid, s) : launch_tma_t<R, 0, 2, NST>(p, grid, s);
 }
 
 cudaError_t launch_tile_sweep_tma(const TileSweepParams &p, bool c128, int pre_mode, int npass, int grid,
-                                  cudaStream_t s) {
-  return c128 ? launch_tma_r<double>(p, pre_mode, npass, grid, s)
-              : launch_tma_r<float>(p, pre_mode, npass, grid, s);
+                                  cudaStream_t s, int stages) {
+  if (stages == 3)
+    return c128 ? launch_tma_r<double, 3>(p, pre_mode, npass, grid, s)
+                : launch_tma_r<float, 3>(p, pre_mode, npass, grid, s);
+  return c128 ? launch_tma_r<double, 2>(p, pre_mode, npass, grid, s)
+              : launch_tma_r<float, 2>(p, pre_mode, npass, grid, s);
 }
 
-template <typename R>
+template <typename R, int NST>
 static cudaError_t tma_setup_r() {
-  const int bytes = kTmaStages * kTileBytes;
-  cudaError_t e;
-  if ((e = cudaFuncSetAttribute(tile_sweep_tma_kernel<R, 0, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                bytes)) != cudaSuccess)
-    return e;
-  if ((e = cudaFuncSetAttribute(tile_sweep_tma_kernel<R, 1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                bytes)) != cudaSuccess)
-    return e;
-  if ((e = cudaFuncSetAttribute(tile_sweep_tma_kernel<R, 0, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                bytes)) != cudaSuccess)
-    return e;
-  return cudaFuncSetAttribute(tile_sweep_tma_kernel<R, 1, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  const int bytes = NST * kTileBytes;
+  const void *fns[4] = {(const void *)tile_sweep_tma_kernel<R, 0, 1, NST>, (const void *)tile_sweep_tma_kernel<R, 1, 1, NST>,
+                        (const void *)tile_sweep_tma_kernel<R, 0, 2, NST>, (const void *)tile_sweep_tma_kernel<R, 1, 2, NST>};
+  for (const void *f : fns) {
+    cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
 }
 
-cudaError_t tile_sweep_tma_setup(bool c128) { return c128 ? tma_setup_r<double>() : tma_setup_r<float>(); }
+cudaError_t tile_sweep_tma_setup(bool c128) {
+  cudaError_t e = c128 ? tma_setup_r<double, 2>() : tma_setup_r<float, 2>();
+  if (e != cudaSuccess) return e;
+  return c128 ? tma_setup_r<double, 3>() : tma_setup_r<float, 3>();
+}
 
 }  // namespace qsim

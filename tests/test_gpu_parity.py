@@ -129,7 +129,7 @@ def test_tree_mode_h14(prec, h14_reference):
 
 
 @pytest.mark.parametrize("prec", PRECS, ids=PNAME.get)
-@pytest.mark.parametrize("lazy,kernel", [(0, 0), (1, 1), (0, 1)])
+@pytest.mark.parametrize("lazy,kernel", [(0, 0), (1, 1), (0, 1), (1, 2)])
 def test_tree_mode_h14_variants(prec, lazy, kernel, h14_reference):
     """Full last sweep instead of the lazy gather; register-only sweep kernel instead of TMA."""
     circ, Su, Sl, ref = h14_reference
