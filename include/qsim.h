@@ -180,7 +180,9 @@ qsim_status qsim_branch_sum(qsim_ctx *ctx, const void *U, const void *L, size_t 
 qsim_status qsim_branch_state(qsim_ctx *ctx, int half, uint64_t branch, void *out);
 
 /* Multi-GPU (one process per GPU).  qsim_nccl_unique_id writes 128 bytes
- * (ncclUniqueId) on rank 0; every rank passes the same bytes to qsim_comm_init. */
+ * (ncclUniqueId) on rank 0; every rank passes the same bytes to qsim_comm_init, which records
+ * rank / world (EINVAL if out of range) — the NCCL communicator is created at the first
+ * collective (qsim_amplitudes / qsim_sample, called by every rank), ENCCL on failure. */
 qsim_status qsim_nccl_unique_id(void *out128);
 qsim_status qsim_comm_init(qsim_ctx *ctx, int rank, int world, const void *unique_id128);
 /* This rank's share [*begin, *end) of the 2^c branches (contiguous, prefix aligned). */

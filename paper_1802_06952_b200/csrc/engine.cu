@@ -731,6 +731,7 @@ double *Engine::reduced_block() {
   const size_t n = Su_.size() * Sl_.size();
   if (world_ == 1) return A_acc_.as<double>();
   if (!reduced_) {
+    ensure_comm();
     if (rank_ == 0) A_tot_.reserve(n * 16);
     ncclResult_t r = ncclReduce(A_acc_.ptr, rank_ == 0 ? A_tot_.ptr : nullptr, 2 * n, ncclDouble, ncclSum,
                                 0, comm_, stream_);
@@ -865,22 +866,28 @@ void Engine::branch_state(int half, uint64_t b, void *out) {
 }
 
 // ---------------------------------------------------------------- multi-GPU
+// Records rank / world / id; the communicator itself is created at the first collective
+// (ensure_comm), so the sharding logic works without a GPU.
 void Engine::comm_init(int rank, int world, const void *id) {
   if (world < 1 || rank < 0 || rank >= world || !id) throw Error(QSIM_EINVAL, "bad rank / world / id");
-  ensure_device();
   if (comm_) {
     ncclCommDestroy(comm_);
     comm_ = nullptr;
   }
-  if (world > 1) {
-    ncclUniqueId uid;
-    std::memcpy(&uid, id, sizeof(uid));
-    ncclResult_t r = ncclCommInitRank(&comm_, world, uid, rank);
-    if (r != ncclSuccess) throw Error(QSIM_ENCCL, std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
-  }
+  std::memcpy(uid_, id, sizeof(uid_));
   rank_ = rank;
   world_ = world;
   reduced_ = false;
+}
+
+void Engine::ensure_comm() {
+  if (comm_ || world_ == 1) return;
+  ensure_device();
+  ncclUniqueId uid;
+  static_assert(sizeof(uid) == sizeof(uid_), "ncclUniqueId size");
+  std::memcpy(&uid, uid_, sizeof(uid));
+  ncclResult_t r = ncclCommInitRank(&comm_, world_, uid, rank_);
+  if (r != ncclSuccess) throw Error(QSIM_ENCCL, std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
 }
 
 void Engine::rank_range(uint64_t *b0, uint64_t *b1) const {

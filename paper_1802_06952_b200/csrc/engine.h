@@ -120,6 +120,8 @@ class Engine {
   // comm
   ncclComm_t comm_ = nullptr;
   int rank_ = 0, world_ = 1;
+  unsigned char uid_[128] = {};
+  void ensure_comm();
 
   // stats
   qsim_stats_t st_{};
