@@ -86,8 +86,9 @@ typedef enum {
   QSIM_OPT_MEM_BUDGET = 3,  /* cap in bytes on device memory for half-state buffers (0 = free memory) */
   QSIM_OPT_SWEEP_KERNEL = 4, /* 0: TMA-pipelined sweep, 2 smem stages (default); 1: register-only sweep;
                                 2: TMA-pipelined sweep, 3 smem stages                                   */
-  QSIM_OPT_LAZY_LAST = 5     /* 1 (default): each leaf's last sweep is evaluated only at the sampled
-                                indices during the gather (2^k reads per index instead of a 2^h pass) */
+  QSIM_OPT_LAZY_LAST = 5     /* lazy tail of each leaf, evaluated only at the sampled indices during the
+                                gather instead of full 2^h passes: 0 off, 1 the last sweep, 2 (default)
+                                the last one or two by a cost model, 3 always two when possible      */
 } qsim_option;
 
 /* Create a context bound to CUDA device `device` (no device call is made until the

@@ -22,8 +22,17 @@ BUILD = os.path.join(HERE, "_build")
 LIB = os.path.join(HERE, "libqsim.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+# NCCL: the copy bundled with torch (same SONAME libnccl.so.2 as the one torch loads, so the
+# process holds a single NCCL whichever of torch / libqsim is loaded first)
+try:
+    import nvidia.nccl as _nccl
+    NCCL_DIR = os.path.dirname(_nccl.__file__) if _nccl.__file__ else list(_nccl.__path__)[0]
+except Exception:  # fall back to the system NCCL
+    NCCL_DIR = None
+NCCL_INC = os.path.join(NCCL_DIR, "include") if NCCL_DIR else "/usr/include"
+NCCL_LIB = os.path.join(NCCL_DIR, "lib") if NCCL_DIR else "/usr/lib/x86_64-linux-gnu"
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3", "--expt-relaxed-constexpr",
-         "-I", os.path.join(ROOT, "include")]
+         "-I", NCCL_INC, "-I", os.path.join(ROOT, "include")]
 
 
 def _sources():
@@ -65,7 +74,9 @@ def build(verbose: bool = False, force: bool = False) -> str:
     with cf.ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1)) as ex:
         objs = list(ex.map(compile_one, _sources() + cpp))
     tmp = LIB + ".tmp"
-    cmd = [NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-lnccl", "-Xlinker", "-rpath=/usr/lib/x86_64-linux-gnu"]
+    nccl_so = os.path.join(NCCL_LIB, "libnccl.so.2")
+    link_nccl = ["-L", NCCL_LIB, "-Xlinker", "-l:libnccl.so.2"] if os.path.exists(nccl_so) else ["-lnccl"]
+    cmd = [NVCC, *ARCH, "-shared", "-o", tmp, *objs, *link_nccl, "-Xlinker", f"-rpath={NCCL_LIB}"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stderr}")

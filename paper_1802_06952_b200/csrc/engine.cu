@@ -186,8 +186,8 @@ void Engine::set_option(int key, int64_t value) {
       mem_budget_ = value;
       return;
     case QSIM_OPT_LAZY_LAST:
-      if (value < 0 || value > 1) throw Error(QSIM_EINVAL, "QSIM_OPT_LAZY_LAST must be 0 or 1");
-      lazy_last_ = value != 0;
+      if (value < 0 || value > 3) throw Error(QSIM_EINVAL, "QSIM_OPT_LAZY_LAST must be 0, 1, 2 or 3");
+      lazy_depth_ = (int)value;
       return;
     case QSIM_OPT_SWEEP_KERNEL:
       if (value < 0 || value > 2) throw Error(QSIM_EINVAL, "QSIM_OPT_SWEEP_KERNEL must be 0, 1 or 2");
@@ -511,13 +511,13 @@ void Engine::launch_plan(const TilePlan &tp, const Diag &fork, bool first, const
   st_.sweep_bytes += (tp.gen ? 1.0 : 2.0) * std::ldexp(1.0, h) * (double)amp_ * p.njobs;
 }
 
-// Runs the sweeps of `level` for fork child `child` (all but the last with skip_last);
-// returns where the state ended (src when no sweep ran).
-const void *Engine::run_level(int half, int level, uint64_t child, const void *src, void *dst, bool skip_last) {
+// Runs the sweeps of `level` for fork child `child`, all but the last `skip` of them
+// (the lazily evaluated tail); returns where the state ended (src when no sweep ran).
+const void *Engine::run_level(int half, int level, uint64_t child, const void *src, void *dst, int skip) {
   HalfExec &he = half_[half];
   const Level &lev = he.prog.levels[level];
   const Diag fork = he.prog.fork_diag(level, child);
-  const size_t n = lev.sweeps.size() - (skip_last && !lev.sweeps.empty() ? 1 : 0);
+  const size_t n = lev.sweeps.size() - std::min<size_t>(lev.sweeps.size(), (size_t)skip);
   for (size_t s = 0; s < n; ++s) {
     const auto &chunks = he.plans[level][s];
     for (size_t ci = 0; ci < chunks.size(); ++ci) {
@@ -528,34 +528,76 @@ const void *Engine::run_level(int half, int level, uint64_t child, const void *s
   return n ? dst : src;
 }
 
-// Leaf gather.  lazy: the leaf level's last sweep is evaluated only at the sampled
-// indices (gather_layer); else psi is the complete leaf (pending fork diagonal applied).
+static LazyLayer lazy_layer(const Sweep &sw, const Diag &pre, int vs) {
+  LazyLayer ll;
+  std::memset(&ll, 0, sizeof(ll));
+  ll.k = (int)sw.gates.size();
+  for (size_t t = 0; t < sw.gates.size(); ++t) {
+    ll.bit[t] = sw.gates[t].bit;
+    ll.tmask |= 1u << sw.gates[t].bit;
+    (sw.gates[t].kind == 1 ? ll.sxmask : ll.symask) |= 1u << sw.gates[t].bit;
+  }
+  ll.pre = to_dev(pre, vs);
+  ll.post = to_dev(sw.post, vs, true);
+  return ll;
+}
+
+// Number of the leaf level's trailing sweeps evaluated lazily at the sampled indices
+// (0, 1 or 2; at most lazy_depth_).  Cost model in bytes: a sweep moves 2 * 2^h * amp;
+// a lazy layer costs ~96 bytes per scattered read (32-byte sector, ~3x random-access
+// inefficiency); depth 2 reads n_S * 2^(k_d + k_(d-1)) values.
+int Engine::lazy_depth(int half, int64_t nS) const {
+  const HalfProgram &hp = half_[half].prog;
+  const int F = (int)hp.levels.size() - 1;
+  if (full_leaf_ || F < 1 || lazy_depth_ < 1) return 0;
+  const auto &sw = hp.levels[F].sweeps;
+  if (sw.empty() || sw.back().gates.size() > 12) return 0;
+  if (lazy_depth_ < 2 || sw.size() < 2) return 1;
+  const int kd = (int)sw.back().gates.size(), kd1 = (int)sw[sw.size() - 2].gates.size();
+  if (kd + kd1 > 20 || ((double)nS * std::ldexp(1.0, kd)) > (double)(1 << 26)) return 1;
+  const double sweep = 2.0 * std::ldexp(1.0, hp.h) * (double)amp_;
+  const double lazy1 = 96.0 * (double)nS * std::ldexp(1.0, kd);
+  const double lazy2 = 96.0 * (double)nS * std::ldexp(1.0, kd + kd1) + 2.0 * lazy1;
+  if (lazy_depth_ == 3) return 2;  // forced (tests)
+  return lazy2 < sweep + lazy1 ? 2 : 1;
+}
+
+// Leaf gather.  depth 0: psi is the complete leaf (a pending fork diagonal is applied);
+// depth 1: the leaf level's last sweep is evaluated at the sampled indices; depth 2: its
+// last two sweeps, the earlier one on the cone of the last one (compact buffer).
 void Engine::gather_leaf(int half, uint64_t child_last, const void *psi, const uint64_t *dS, int64_t nS,
-                         void *out_row, bool lazy) {
+                         void *out_row, int depth) {
   HalfExec &he = half_[half];
   const int F = (int)he.prog.levels.size() - 1;
   const Level &lev = he.prog.levels[F];
-  if (lazy) {
-    const Sweep &sw = lev.sweeps.back();
-    LazyLayer ll;
-    std::memset(&ll, 0, sizeof(ll));
-    ll.k = (int)sw.gates.size();
-    for (size_t t = 0; t < sw.gates.size(); ++t) {
-      ll.bit[t] = sw.gates[t].bit;
-      ll.tmask |= 1u << sw.gates[t].bit;
-      (sw.gates[t].kind == 1 ? ll.sxmask : ll.symask) |= 1u << sw.gates[t].bit;
+  const int vs = he.prog.vs;
+  if (depth >= 1) {
+    const size_t n = lev.sweeps.size();
+    auto pre_of = [&](size_t s) {
+      return s == 0 ? Diag::merge(he.prog.fork_diag(F, child_last), lev.sweeps[0].pre) : lev.sweeps[s].pre;
+    };
+    const LazyLayer lld = lazy_layer(lev.sweeps[n - 1], pre_of(n - 1), vs);
+    if (depth == 1) {
+      check(launch_gather_layer(psi, dS, nS, out_row, lld, c128_, stream_), "gather_layer launch");
+      st_.kernel_launches++;
+    } else {
+      const LazyLayer ll1 = lazy_layer(lev.sweeps[n - 2], pre_of(n - 2), vs);
+      const int64_t ncone = nS << lld.k;
+      cone_idx_.reserve((size_t)ncone * 8);
+      cone_val_.reserve((size_t)ncone * amp_);
+      check(launch_cone_indices(dS, nS, lld, cone_idx_.as<uint64_t>(), stream_), "cone launch");
+      check(launch_gather_layer(psi, cone_idx_.as<uint64_t>(), ncone, cone_val_.ptr, ll1, c128_, stream_),
+            "gather_layer launch");
+      check(launch_gather_layer_compact(cone_val_.ptr, dS, nS, out_row, lld, c128_, stream_),
+            "gather_layer_compact launch");
+      st_.kernel_launches += 3;
     }
-    const Diag pre = lev.sweeps.size() == 1 ? Diag::merge(he.prog.fork_diag(F, child_last), sw.pre) : sw.pre;
-    ll.pre = to_dev(pre, he.prog.vs);
-    ll.post = to_dev(sw.post, he.prog.vs, true);
-    check(launch_gather_layer(psi, dS, nS, out_row, ll, c128_, stream_), "gather_layer launch");
-    st_.kernel_launches++;
     st_.lazy_gathers++;
     return;
   }
   Diag pend;
   if (F >= 1 && lev.sweeps.empty()) pend = he.prog.fork_diag(F, child_last);
-  check(launch_gather(psi, dS, nS, out_row, to_dev(pend, he.prog.vs), c128_, stream_), "gather launch");
+  check(launch_gather(psi, dS, nS, out_row, to_dev(pend, vs), c128_, stream_), "gather launch");
   st_.kernel_launches++;
 }
 
@@ -627,10 +669,9 @@ void Engine::evolve_half(int half, uint64_t b0, uint64_t b1, void *slice, const 
   std::vector<int> sbits(F + 1, 0);  // cut bits consumed up to and including level l
   for (int l = 1; l <= F; ++l) sbits[l] = sbits[l - 1] + hp.levels[l].k;
   auto buf = [&](int l) { return states_[std::max(l, m0) - m0]->ptr; };
-  // lazy last layer: skip the leaf level's last sweep, evaluate it at the sampled indices
-  const bool lazy = lazy_last_ && !full_leaf_ && F >= 1 && !hp.levels[F].sweeps.empty() &&
-                    hp.levels[F].sweeps.back().gates.size() <= 12;
-  auto skip = [&](int l) { return lazy && l == F; };
+  // lazy tail: the leaf level's last `lazy` sweeps are evaluated at the sampled indices
+  const int lazy = lazy_depth(half, nS);
+  auto skip = [&](int l) { return l == F ? lazy : 0; };
 
   // recompute levels 0..lt along the path of prefix `cp` in place in buf(m0)
   auto recompute_path = [&](int lt, uint64_t cp) {
@@ -666,7 +707,7 @@ void Engine::evolve_half(int half, uint64_t b0, uint64_t b1, void *slice, const 
     }
   };
   if (m0 == 0) {
-    node(0, 0, run_level(half, 0, 0, nullptr, buf(0), false));
+    node(0, 0, run_level(half, 0, 0, nullptr, buf(0), skip(0)));
   } else {
     node(0, 0, nullptr);
   }

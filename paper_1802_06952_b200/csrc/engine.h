@@ -97,7 +97,7 @@ class Engine {
   int mode_ = 0;
   int64_t mem_budget_ = 0;
   int sweep_kernel_ = 0;  // 0: TMA-pipelined sweep, 1: register-only sweep
-  bool lazy_last_ = true;  // evaluate each leaf's last sweep only at the sampled indices
+  int lazy_depth_ = 2;      // up to this many trailing leaf sweeps evaluated at the sampled indices
   bool full_leaf_ = false; // qsim_branch_state: materialise the complete leaf
   bool time_sweeps_ = false;
 
@@ -112,6 +112,7 @@ class Engine {
   DevBuf A_tot_;  // reduced block (rank 0 with a communicator)
   bool reduced_ = false;
   DevBuf U_, L_;  // slices
+  DevBuf cone_idx_, cone_val_;  // two-layer lazy tail
   std::vector<DevBuf *> states_;
   size_t state_bytes_ = 0;
   // sampler
@@ -137,11 +138,12 @@ class Engine {
 
   // executor
   void evolve_half(int half, uint64_t b0, uint64_t b1, void *slice, const uint64_t *dS, int64_t nS);
-  const void *run_level(int half, int level, uint64_t child, const void *src, void *dst, bool skip_last);
+  const void *run_level(int half, int level, uint64_t child, const void *src, void *dst, int skip);
+  int lazy_depth(int half, int64_t nS) const;
   void launch_plan(const TilePlan &tp, const Diag &fork, bool first_chunk_of_level, const void *src,
                    void *dst, int h);
   void gather_leaf(int half, uint64_t child_last, const void *psi, const uint64_t *dS, int64_t nS,
-                   void *out_row, bool lazy);
+                   void *out_row, int depth);
   void gemm(const void *U, const void *L, int64_t K, int64_t M, int64_t N, double *A);
   double *reduced_block();
   void run_sampler(const double *p, int64_t M, int64_t N, const uint64_t *dSu, const uint64_t *dSl,

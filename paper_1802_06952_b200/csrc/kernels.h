@@ -127,6 +127,13 @@ struct LazyLayer {
 };
 cudaError_t launch_gather_layer(const void *psi, const uint64_t *S, int64_t n, void *out,
                                 const LazyLayer &ll, bool c128, cudaStream_t s);
+// Two lazy layers: the cone of the last layer, cone[j * 2^k + m] = (S[j] & ~tmask) | deposit(m),
+// is where layer d-1 is needed; launch_gather_layer(psi, cone) evaluates it there, and the
+// compact variant applies layer d reading V[j * 2^k + m] instead of psi[y].
+cudaError_t launch_cone_indices(const uint64_t *S, int64_t n, const LazyLayer &ll, uint64_t *cone,
+                                cudaStream_t s);
+cudaError_t launch_gather_layer_compact(const void *V, const uint64_t *S, int64_t n, void *out,
+                                        const LazyLayer &ll, bool c128, cudaStream_t s);
 // A[m, n] += sum_k U[k, m] * L[k, n]   (complex; U, L of the ctx precision, A double2)
 cudaError_t launch_branch_gemm(const void *U, const void *L, int64_t K, int64_t M, int64_t N,
                                double *A, bool c128, cudaStream_t s);

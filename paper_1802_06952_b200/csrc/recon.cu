@@ -120,6 +120,84 @@ cudaError_t launch_gather_layer(const void *psi, const uint64_t *S, int64_t n, v
   return cudaGetLastError();
 }
 
+__global__ void cone_kernel(const uint64_t *__restrict__ S, int64_t n, const __grid_constant__ LazyLayer ll,
+                            uint64_t *__restrict__ cone) {
+  const int64_t per = 1ll << ll.k;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n * per; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = e >> ll.k;
+    const uint32_t m = (uint32_t)(e & (per - 1));
+    uint32_t z = (uint32_t)S[j] & ~ll.tmask;
+    for (int t = 0; t < ll.k; ++t) z |= ((m >> t) & 1u) << ll.bit[t];
+    cone[e] = z;
+  }
+}
+
+cudaError_t launch_cone_indices(const uint64_t *S, int64_t n, const LazyLayer &ll, uint64_t *cone, cudaStream_t s) {
+  const int64_t tot = n << ll.k;
+  const int blocks = (int)std::min<int64_t>((tot + 255) / 256, 148 * 16);
+  cone_kernel<<<blocks, 256, 0, s>>>(S, n, ll, cone);
+  return cudaGetLastError();
+}
+
+// layer d from the compact cone values V[j * 2^k + m] (same warp-per-output scheme)
+template <typename R>
+__global__ void __launch_bounds__(256) gather_layer_compact_kernel(const typename CxT<R>::T *__restrict__ V,
+                                                                   const uint64_t *__restrict__ S, int64_t n,
+                                                                   typename CxT<R>::T *__restrict__ out,
+                                                                   const __grid_constant__ LazyLayer ll) {
+  using C = typename CxT<R>::T;
+  const int lane = threadIdx.x & 31;
+  const int64_t j = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (j >= n) return;
+  const uint32_t x = (uint32_t)S[j];
+  const uint32_t base = x & ~ll.tmask;
+  const uint32_t nterm = 1u << ll.k;
+  const C *Vj = V + ((size_t)j << ll.k);
+  R sr = 0, si = 0;
+  for (uint32_t m = lane; m < nterm; m += 32) {
+    uint32_t y = base;
+    for (int t = 0; t < ll.k; ++t) y |= ((m >> t) & 1u) << ll.bit[t];
+    C v = Vj[m];
+    int ph = 6 * __popc((x ^ y) & ll.sxmask) + 4 * __popc(~x & y & ll.symask);
+    if (ll.pre.active) {
+      ph += diag_phase(y, ll.pre, ll.pre.zm);
+      if ((y & ll.pre.pm) != ll.pre.pv) v.x = v.y = (R)0;
+    }
+    ph &= 7;
+    const R wr = (R)c_omega[2 * ph], wi = (R)c_omega[2 * ph + 1];
+    sr += v.x * wr - v.y * wi;
+    si += v.x * wi + v.y * wr;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    sr += __shfl_xor_sync(0xffffffffu, sr, o);
+    si += __shfl_xor_sync(0xffffffffu, si, o);
+  }
+  if (lane == 0) {
+    const double pre_scale = ll.pre.active ? ll.pre.scale : 1.0;
+    const int ph = diag_phase(x, ll.post, ll.post.zm);
+    const double sc = ll.post.scale * pre_scale;
+    const R wr = (R)(c_omega[2 * ph] * sc), wi = (R)(c_omega[2 * ph + 1] * sc);
+    C o;
+    o.x = sr * wr - si * wi;
+    o.y = sr * wi + si * wr;
+    if ((x & ll.post.pm) != ll.post.pv) o.x = o.y = (R)0;
+    out[j] = o;
+  }
+}
+
+cudaError_t launch_gather_layer_compact(const void *V, const uint64_t *S, int64_t n, void *out, const LazyLayer &ll,
+                                        bool c128, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  const int64_t blocks = (n * 32 + 255) / 256;
+  if (c128)
+    gather_layer_compact_kernel<double>
+        <<<(unsigned)blocks, 256, 0, s>>>((const double2 *)V, S, n, (double2 *)out, ll);
+  else
+    gather_layer_compact_kernel<float><<<(unsigned)blocks, 256, 0, s>>>((const float2 *)V, S, n, (float2 *)out, ll);
+  return cudaGetLastError();
+}
+
 // ---------------------------------------------------------------- branch GEMM (DMMA)
 // CTA tile 64 x 64 (M x N), K step 16, 8 warps as 2 (M) x 4 (N), warp tile 32 x 16 =
 // 4 x 2 m8n8k4 FP64 MMAs.  Complex product with 4 real MMAs per tile and K-step:

@@ -15,6 +15,24 @@ def pytest_configure(config):
     config.addinivalue_line("markers", "slow: long-running (minutes)")
 
 
+def _cuda_available():
+    try:
+        import torch
+        return torch.cuda.is_available()
+    except Exception:
+        return False
+
+
+def pytest_collection_modifyitems(config, items):
+    """`gpu` tests need a CUDA device; without one (the CPU build box) they are skipped."""
+    if _cuda_available():
+        return
+    skip = pytest.mark.skip(reason="no CUDA device (run with -m gpu on a B200)")
+    for item in items:
+        if "gpu" in item.keywords:
+            item.add_marker(skip)
+
+
 def golden(name):
     import json
     with open(os.path.join(GOLDEN, name)) as f:

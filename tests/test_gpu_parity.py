@@ -129,7 +129,7 @@ def test_tree_mode_h14(prec, h14_reference):
 
 
 @pytest.mark.parametrize("prec", PRECS, ids=PNAME.get)
-@pytest.mark.parametrize("lazy,kernel", [(0, 0), (1, 1), (0, 1), (1, 2)])
+@pytest.mark.parametrize("lazy,kernel", [(0, 0), (1, 1), (0, 1), (1, 2), (3, 0), (3, 1)])
 def test_tree_mode_h14_variants(prec, lazy, kernel, h14_reference):
     """Full last sweep instead of the lazy gather; register-only sweep kernel instead of TMA."""
     circ, Su, Sl, ref = h14_reference
@@ -145,6 +145,18 @@ def test_tree_recompute_path_and_ranges(prec, h14_reference):
     A = run_block(circ, Su, Sl, prec, budget=2 * (1 << 14) * amp + 1,
                   ranges=[(0, 5), (5, 64), (64, 128)])
     assert_close(A, ref, prec, "h14 budget")
+
+
+@pytest.mark.parametrize("prec", PRECS, ids=PNAME.get)
+def test_lazy_tail_full_size_consistency(prec):
+    """C3 size (h = 21), 256 branches: lazy tail depth 2 and 1 agree with full leaf sweeps."""
+    circ = generate(6, 7, 22, 4)
+    Su = sample_block(21, 512, 8)
+    Sl = sample_block(21, 384, 9)
+    ref = run_block(circ, Su, Sl, prec, ranges=[(0, 256)], opts={Q.QSIM_OPT_LAZY_LAST: 0})
+    for lazy in (1, 3):
+        A = run_block(circ, Su, Sl, prec, ranges=[(0, 256)], opts={Q.QSIM_OPT_LAZY_LAST: lazy})
+        assert_close(A, ref, prec, f"lazy {lazy}")
 
 
 @pytest.mark.parametrize("prec", PRECS, ids=PNAME.get)
