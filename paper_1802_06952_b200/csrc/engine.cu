@@ -190,7 +190,7 @@ void Engine::set_option(int key, int64_t value) {
       lazy_depth_ = (int)value;
       return;
     case QSIM_OPT_SWEEP_KERNEL:
-      if (value < 0 || value > 2) throw Error(QSIM_EINVAL, "QSIM_OPT_SWEEP_KERNEL must be 0, 1 or 2");
+      if (value < 0 || value > 3) throw Error(QSIM_EINVAL, "QSIM_OPT_SWEEP_KERNEL must be 0..3");
       sweep_kernel_ = (int)value;
       return;
     default:
@@ -495,7 +495,7 @@ void Engine::launch_plan(const TilePlan &tp, const Diag &fork, bool first, const
     check(cudaEventRecord(e0, stream_), "cudaEventRecord");
   }
   if (tma)
-    check(launch_tile_sweep_tma(p, c128_, pre_mode, tp.npass, grid, stream_, sweep_kernel_ == 2 ? 3 : 2),
+    check(launch_tile_sweep_tma(p, c128_, pre_mode, tp.npass, grid, stream_, (sweep_kernel_ == 2 || (sweep_kernel_ == 3 && tp.npass == 2)) ? 3 : 2),
           "tma sweep launch");
   else
     check(launch_tile_sweep(p, c128_, pre_mode, tp.npass, grid, stream_), "tile sweep launch");
