@@ -245,7 +245,7 @@ def test_end_to_end_sampling(prec):
 
 # ------------------------------------------------------------------ full-size properties
 @pytest.mark.parametrize("prec", PRECS, ids=PNAME.get)
-@pytest.mark.parametrize("grid", [(8, 7), (6, 7)])
+@pytest.mark.parametrize("grid", [(8, 7), (6, 7), (8, 8)])
 def test_depth3_closed_form_full_size(prec, grid):
     """Depth <= 3 circuits are diagonal: a(x) = 2^{-n/2} w^{m1(x)} (-1)^{m2(x)} at 42/56 qubits."""
     rows, cols = grid
