@@ -77,6 +77,7 @@ typedef struct {
   double gemm_ms;            /* CUDA-event time of GEMM launches (QSIM_OPT_TIME_SWEEPS)  */
   uint64_t branches_evolved; /* branch pairs whose slices were gathered                  */
   uint64_t lazy_gathers;     /* leaves whose last sweep was evaluated at the sampled indices only */
+  uint64_t layers_applied;   /* gate layers completed by the sweeps (> sweeps when layers are fused) */
 } qsim_stats_t;
 
 typedef enum {
@@ -84,11 +85,13 @@ typedef enum {
   QSIM_OPT_MODE = 2,        /* 0: auto, 1: flat in-shared-memory per-branch kernel (h <= 12),
                                2: prefix-shared branch tree of tile sweeps (h >= 13)          */
   QSIM_OPT_MEM_BUDGET = 3,  /* cap in bytes on device memory for half-state buffers (0 = free memory) */
-  QSIM_OPT_SWEEP_KERNEL = 4, /* 0: TMA-pipelined sweep, 2 smem stages (default); 1: register-only sweep;
-                                2: TMA-pipelined sweep, 3 smem stages                                   */
+  QSIM_OPT_SWEEP_KERNEL = 4, /* 0: fused TMA-pipelined sweep (default); 1: register-only one-layer sweep;
+                                (comparison)                                                            */
   QSIM_OPT_LAZY_LAST = 5     /* lazy tail of each leaf, evaluated only at the sampled indices during the
                                 gather instead of full 2^h passes: 0 off, 1 the last sweep, 2 (default)
-                                the last one or two by a cost model, 3 always two when possible      */
+                                the last one or two by a cost model, 3 always two when possible      */,
+  QSIM_OPT_FUSE_LAYERS = 6   /* 1: consecutive layers whose high targets fit one tile share one HBM
+                                pass (up to 3 register passes per tile); 0 (default): one layer per pass */
 } qsim_option;
 
 /* Create a context bound to CUDA device `device` (no device call is made until the

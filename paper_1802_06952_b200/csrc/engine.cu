@@ -161,6 +161,7 @@ void Engine::ensure_device() {
   if (!stream_) stream_ = own_stream_;
   check(tile_sweep_setup(&occ1_, &occ2_, c128_), "tile sweep setup");
   check(tile_sweep_tma_setup(c128_), "tma sweep setup");
+  check(fused_sweep_setup(c128_), "fused sweep setup");
   occ1_ = std::max(occ1_, 1);
   occ2_ = std::max(occ2_, 1);
   inited_ = true;
@@ -189,9 +190,17 @@ void Engine::set_option(int key, int64_t value) {
       if (value < 0 || value > 3) throw Error(QSIM_EINVAL, "QSIM_OPT_LAZY_LAST must be 0, 1, 2 or 3");
       lazy_depth_ = (int)value;
       return;
+    case QSIM_OPT_FUSE_LAYERS:
+      if (value < 0 || value > 1) throw Error(QSIM_EINVAL, "QSIM_OPT_FUSE_LAYERS must be 0 or 1");
+      fuse_layers_ = value != 0;
+      if (have_circuit_)
+        for (int h = 0; h < 2; ++h) compile_plans(half_[h]);
+      return;
     case QSIM_OPT_SWEEP_KERNEL:
-      if (value < 0 || value > 3) throw Error(QSIM_EINVAL, "QSIM_OPT_SWEEP_KERNEL must be 0..3");
+      if (value < 0 || value > 1) throw Error(QSIM_EINVAL, "QSIM_OPT_SWEEP_KERNEL must be 0 or 1");
       sweep_kernel_ = (int)value;
+      if (have_circuit_)
+        for (int h = 0; h < 2; ++h) compile_plans(half_[h]);
       return;
     default:
       throw Error(QSIM_EINVAL, "unknown option key");
@@ -230,7 +239,192 @@ void Engine::partition(uint32_t *n_cuts, uint64_t *n_branches, qsim_cut *cuts) c
     for (size_t g = 0; g < c; ++g) cuts[g] = circ_.cuts[g];
 }
 
-// Tile plan of every sweep (host only; precision-dependent tile geometry).
+// ---------------------------------------------------------------- sweep planning
+static void outer_runs(const std::vector<int> &hb, int L, int h, uint8_t *run_start, uint8_t *run_len,
+                       int32_t *nruns) {
+  int nr = 0;
+  for (int b = L; b < h;) {
+    if (std::find(hb.begin(), hb.end(), b) != hb.end()) {
+      ++b;
+      continue;
+    }
+    int e = b;
+    while (e < h && std::find(hb.begin(), hb.end(), e) == hb.end()) ++e;
+    run_start[nr] = (uint8_t)b;
+    run_len[nr] = (uint8_t)(e - b);
+    ++nr;
+    b = e;
+  }
+  *nruns = nr;
+}
+
+// Plans one fused launch over `stages` (kernels.h FusedSweepParams); false if the high
+// targets exceed the tile or the pass / op / diagonal budgets.
+bool Engine::plan_fused(const HalfProgram &hp, const std::vector<Stage> &stages, const Diag &pre, TilePlan &tp) {
+  const int L = tile_low_bits(c128_), T = L + kHiBits, VB = c128_ ? 0 : 1;
+  std::vector<int> hb;
+  for (auto &st : stages)
+    for (auto &g : st.gates)
+      if (g.bit >= L && std::find(hb.begin(), hb.end(), (int)g.bit) == hb.end()) hb.push_back(g.bit);
+  if ((int)hb.size() > kHiBits) return false;
+  for (int b = L; (int)hb.size() < kHiBits && b < hp.h; ++b)
+    if (std::find(hb.begin(), hb.end(), b) == hb.end()) hb.push_back(b);
+  std::sort(hb.begin(), hb.end());
+  auto idx_of = [&](int bit) { return (int)(std::find(hb.begin(), hb.end(), bit) - hb.begin()); };
+  FusedSweepParams &f = tp.f;
+  std::memset(&f, 0, sizeof(f));
+  std::vector<std::vector<int>> R(1);
+  std::vector<int> diag_pass;
+  std::vector<Diag> diags;
+  int cur = 0;
+  // the open stage of pass `cur` (diag == -1); a stage is closed by its diagonal (>= 0) or
+  // when a bit would get a second gate (-2)
+  auto open = [&]() -> SweepStage * {
+    if (f.nstage[cur] == 0 || f.stage[cur][f.nstage[cur] - 1].diag != -1) {
+      if (f.nstage[cur] >= kMaxStage) return nullptr;
+      SweepStage &s = f.stage[cur][f.nstage[cur]++];
+      std::memset(&s, 0, sizeof(s));
+      s.diag = -1;
+    }
+    return &f.stage[cur][f.nstage[cur] - 1];
+  };
+  for (auto &st : stages) {
+    for (auto &g : st.gates) {
+      SweepStage *S = nullptr;
+      if (g.bit < L) {
+        if (!(S = open())) return false;
+        if (VB && g.bit == 0) {
+          if (S->vkind) {
+            S->diag = -2;
+            if (!(S = open())) return false;
+          }
+          S->vkind = g.kind;
+        } else {
+          const int lb = g.bit - VB;
+          if (std::find(S->lane_bit, S->lane_bit + S->nlane, lb) != S->lane_bit + S->nlane) {
+            S->diag = -2;
+            if (!(S = open())) return false;
+          }
+          S->lane_bit[S->nlane] = (uint8_t)lb;
+          S->lane_kind[S->nlane++] = g.kind;
+        }
+      } else {
+        const int j = idx_of(g.bit);
+        auto it = std::find(R[cur].begin(), R[cur].end(), j);
+        if (it == R[cur].end()) {
+          if (R[cur].size() == 4) {
+            if (++cur >= kMaxPass) return false;
+            R.emplace_back();
+          }
+          R[cur].push_back(j);
+          it = R[cur].end() - 1;
+        }
+        const int slot = (int)(it - R[cur].begin());
+        if (!(S = open())) return false;
+        if (S->gkind[slot]) {
+          S->diag = -2;
+          if (!(S = open())) return false;
+        }
+        S->gkind[slot] = g.kind;
+      }
+    }
+    if (!st.diag.identity()) {
+      if ((int)diags.size() >= kMaxDiag) return false;
+      SweepStage *S = open();
+      if (!S) return false;
+      S->diag = (int8_t)diags.size();
+      diags.push_back(st.diag);
+      diag_pass.push_back(cur);
+    }
+  }
+  f.npass = cur + 1;
+  for (int q = 0; q < f.npass; ++q) {
+    for (int j = 0; j < kHiBits && R[q].size() < 4; ++j)
+      if (std::find(R[q].begin(), R[q].end(), j) == R[q].end()) R[q].push_back(j);
+    std::vector<int> warps;
+    for (int j = 0; j < kHiBits; ++j)
+      if (std::find(R[q].begin(), R[q].end(), j) == R[q].end()) warps.push_back(j);
+    for (int s = 0; s < 4; ++s) f.gsel[q][s] = (uint8_t)R[q][s];
+    for (int w = 0; w < 3; ++w) f.wsel[q][w] = (uint8_t)warps[w];
+  }
+  for (int j = 0; j < kHiBits; ++j) f.hb[j] = (uint8_t)hb[j];
+  auto regpos = [&](int q) {
+    std::vector<int> pos;
+    if (VB) pos.push_back(0);
+    for (int s = 0; s < 4; ++s) pos.push_back(hb[R[q][s]]);
+    return pos;
+  };
+  f.ndiag = (int)diags.size();
+  for (size_t d = 0; d < diags.size(); ++d) {
+    f.diag[d] = to_dev(diags[d], hp.vs, true);
+    f.diag_s[d] = make_split(diags[d], hp.vs, regpos(diag_pass[d]));
+  }
+  outer_runs(hb, L, hp.h, f.run_start, f.run_len, &f.nruns);
+  f.log2_ntiles = hp.h - T;
+  int m = 0;
+  while (m < kHiBits && hb[m] == L + m) ++m;
+  f.run_m = m;
+  tp.fused = true;
+  tp.multi_layer = stages.size() > 1;
+  tp.npass = f.npass;
+  tp.use_pre = true;
+  tp.pre = pre;
+  tp.pass0_regs = regpos(0);
+  return true;
+}
+
+// The launches of `n` leading sweeps of a level: consecutive layers are fused into one
+// HBM pass while their high targets fit the tile (plan_fused); the root's generated first
+// sweep and the register-only kernel (QSIM_OPT_SWEEP_KERNEL 1) use per-sweep legacy plans.
+std::vector<TilePlan> Engine::level_launches(const HalfProgram &hp, const Level &lev, size_t n) {
+  std::vector<TilePlan> out;
+  const int L = tile_low_bits(c128_);
+  auto nhi = [&](const Sweep &sw) {
+    int c = 0;
+    for (auto &g : sw.gates) c += g.bit >= L;
+    return c;
+  };
+  size_t s = 0;
+  while (s < n) {
+    const Sweep &sw = lev.sweeps[s];
+    // single layers (and layers wider than the tile, split into chunks) use the
+    // single-layer kernels; only multi-layer groups use the fused kernel
+    auto single = [&]() {
+      auto v = legacy_plans(hp, sw);
+      out.insert(out.end(), v.begin(), v.end());
+      ++s;
+    };
+    if (sweep_kernel_ == 1 || sw.gen || !fuse_layers_ || nhi(sw) > kHiBits) {
+      single();
+      continue;
+    }
+    std::vector<Stage> stages{Stage{sw.gates, sw.post}};
+    TilePlan best;
+    if (!plan_fused(hp, stages, sw.pre, best)) throw Error(QSIM_EINVAL, "sweep plan");
+    size_t e = s + 1;
+    while (fuse_layers_ && e < n && !lev.sweeps[e].gen && lev.sweeps[e].pre.identity() &&
+           nhi(lev.sweeps[e]) <= kHiBits) {
+      std::vector<Stage> more = stages;
+      more.push_back(Stage{lev.sweeps[e].gates, lev.sweeps[e].post});
+      TilePlan tp;
+      if (!plan_fused(hp, more, sw.pre, tp)) break;
+      stages.swap(more);
+      best = tp;
+      ++e;
+    }
+    if (e == s + 1) {
+      single();
+      continue;
+    }
+    best.layers = (int)(e - s);
+    out.push_back(best);
+    s = e;
+  }
+  return out;
+}
+
+// Tile plans of every level (host only; precision-dependent tile geometry).  The leaf
+// level gets one launch list per lazy-tail depth (0, 1, 2 trailing sweeps left out).
 void Engine::compile_plans(HalfExec &he) {
   const HalfProgram &hp = he.prog;
   const int L = tile_low_bits(c128_), T = L + kHiBits;
@@ -244,12 +438,31 @@ void Engine::compile_plans(HalfExec &he) {
   he.plans.clear();
   if ((he.tree && !can_tree) || (!he.tree && !can_small)) return;  // reported at evolve time
   if (!he.tree) return;
+  const size_t F = hp.levels.size() - 1;
   he.plans.resize(hp.levels.size());
-  for (size_t l = 0; l < hp.levels.size(); ++l) {
+  for (size_t l = 0; l <= F; ++l) {
     const Level &lev = hp.levels[l];
-    he.plans[l].resize(lev.sweeps.size());
-    for (size_t s = 0; s < lev.sweeps.size(); ++s) {
-      const Sweep &sw = lev.sweeps[s];
+    const size_t nskip = l == F ? 3 : 1;
+    for (size_t skip = 0; skip < nskip; ++skip) {
+      const size_t n = lev.sweeps.size() - std::min(skip, lev.sweeps.size());
+      he.plans[l].push_back(level_launches(hp, lev, n));
+      if (std::getenv("QSIM_DEBUG_PLANS")) {
+        std::fprintf(stderr, "%s level %zu skip %zu: %zu sweeps ->", hp.upper ? "U" : "D", l, skip, n);
+        for (auto &tp : he.plans[l].back())
+          std::fprintf(stderr, " [%s x%d p%d m%d]", tp.fused ? "F" : "legacy", tp.layers, tp.npass,
+                       tp.fused ? tp.f.run_m : tp.p.run_m);
+        std::fprintf(stderr, "\n");
+      }
+    }
+  }
+}
+
+// Legacy per-sweep plans (register-only kernel; the generated root sweep).
+std::vector<TilePlan> Engine::legacy_plans(const HalfProgram &hp, const Sweep &sw) {
+  std::vector<TilePlan> out;
+  const int L = tile_low_bits(c128_), T = L + kHiBits;
+  {
+    {
       std::vector<Gate1> low, high;
       for (auto &g : sw.gates) (g.bit < L ? low : high).push_back(g);
       const int nchunks = std::max<int>(1, (int)((high.size() + kHiBits - 1) / kHiBits));
@@ -321,6 +534,8 @@ void Engine::compile_plans(HalfExec &he) {
         }
         tp.p.nruns = nr;
         tp.p.log2_ntiles = hp.h - T;
+        tp.fused = false;
+        tp.layers = ci == nchunks - 1 ? 1 : 0;
         tp.use_pre = ci == 0;
         tp.gen = sw.gen && ci == 0;
         tp.pre = sw.pre;
@@ -330,16 +545,11 @@ void Engine::compile_plans(HalfExec &he) {
         int m = 0;
         while (m < kHiBits && hb[m] == L + m) ++m;
         tp.p.run_m = m;
-        if (std::getenv("QSIM_DEBUG_PLANS")) {
-          std::fprintf(stderr, "%s L%zu S%zu c%d layers %d-%d: npass %d hi[", hp.upper ? "U" : "D", l, s, ci,
-                       sw.first_layer, sw.last_layer, tp.npass);
-          for (int j = 0; j < kHiBits; ++j) std::fprintf(stderr, "%s%d%s", j ? " " : "", hb[j], kind_of(hb[j]) ? "*" : "");
-          std::fprintf(stderr, "] run_m %d lanes %d low0 %d\n", m, tp.p.n_lane, tp.p.lowkind[0]);
-        }
-        he.plans[l][s].push_back(tp);
+        out.push_back(tp);
       }
     }
   }
+  return out;
 }
 
 void Engine::upload_small(HalfExec &he) {
@@ -465,7 +675,6 @@ void Engine::resolve_events() {
 // ---------------------------------------------------------------- executor
 void Engine::launch_plan(const TilePlan &tp, const Diag &fork, bool first, const void *src, void *dst,
                          int h) {
-  TileSweepParams p = tp.p;
   int pre_mode = 0;
   Diag pre;
   if (tp.use_pre) {
@@ -476,17 +685,6 @@ void Engine::launch_plan(const TilePlan &tp, const Diag &fork, bool first, const
       pre_mode = 1;
   }
   const int vs = half_[0].prog.vs;
-  p.pre = to_dev(pre, vs, pre_mode != 0);
-  p.njobs = 1;
-  p.src[0] = tp.gen ? nullptr : src;
-  p.dst[0] = dst;
-  p.job_pv[0] = p.pre.pv;
-  p.job_zm[0] = p.pre.zm;
-  const uint64_t tiles = (1ull << p.log2_ntiles) * (uint64_t)p.njobs;
-  const bool tma = sweep_kernel_ != 1 && pre_mode != 2 && p.njobs == 1;
-  if (tma && pre_mode == 1) p.pre_s = make_split(pre, vs, reg_positions(p, 0, c128_));
-  const int occ = tma ? 1 : (tp.npass == 1 ? occ1_ : occ2_);
-  const int grid = (int)std::min<uint64_t>(tiles, (uint64_t)num_sms_ * occ);
   const bool timed = time_sweeps_;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (timed) {
@@ -494,11 +692,34 @@ void Engine::launch_plan(const TilePlan &tp, const Diag &fork, bool first, const
     e1 = get_event();
     check(cudaEventRecord(e0, stream_), "cudaEventRecord");
   }
-  if (tma)
-    check(launch_tile_sweep_tma(p, c128_, pre_mode, tp.npass, grid, stream_, (sweep_kernel_ == 2 || (sweep_kernel_ == 3 && tp.npass == 2)) ? 3 : 2),
-          "tma sweep launch");
-  else
-    check(launch_tile_sweep(p, c128_, pre_mode, tp.npass, grid, stream_), "tile sweep launch");
+  if (tp.fused) {
+    FusedSweepParams f = tp.f;
+    f.pre = to_dev(pre, vs, pre_mode != 0);
+    if (pre_mode == 1) f.pre_s = make_split(pre, vs, tp.pass0_regs);
+    f.src = src;
+    f.dst = dst;
+    const int grid = (int)std::min<uint64_t>(1ull << f.log2_ntiles, (uint64_t)num_sms_);
+    check(launch_fused_sweep(f, c128_, pre_mode, grid, stream_, tp.multi_layer), "fused sweep launch");
+  } else {
+    TileSweepParams p = tp.p;
+    p.pre = to_dev(pre, vs, pre_mode != 0);
+    p.njobs = 1;
+    p.src[0] = tp.gen ? nullptr : src;
+    p.dst[0] = dst;
+    p.job_pv[0] = p.pre.pv;
+    p.job_zm[0] = p.pre.zm;
+    const uint64_t tiles = 1ull << p.log2_ntiles;
+    const bool tma = sweep_kernel_ != 1 && pre_mode != 2;
+    if (tma) {
+      if (pre_mode == 1) p.pre_s = make_split(pre, vs, reg_positions(p, 0, c128_));
+      const int grid = (int)std::min<uint64_t>(tiles, (uint64_t)num_sms_);
+      check(launch_tile_sweep_tma(p, c128_, pre_mode, tp.npass, grid, stream_, sweep_kernel_ == 2 ? 3 : 2),
+            "tma sweep launch");
+    } else {
+      const int grid = (int)std::min<uint64_t>(tiles, (uint64_t)num_sms_ * (tp.npass == 1 ? occ1_ : occ2_));
+      check(launch_tile_sweep(p, c128_, pre_mode, tp.npass, grid, stream_), "tile sweep launch");
+    }
+  }
   if (timed) {
     check(cudaEventRecord(e1, stream_), "cudaEventRecord");
     ev_sweep_.emplace_back(e0, e1);
@@ -507,8 +728,9 @@ void Engine::launch_plan(const TilePlan &tp, const Diag &fork, bool first, const
   (void)first;
   st_.kernel_launches++;
   st_.sweeps++;
-  st_.sweep_states += (uint64_t)p.njobs;
-  st_.sweep_bytes += (tp.gen ? 1.0 : 2.0) * std::ldexp(1.0, h) * (double)amp_ * p.njobs;
+  st_.sweep_states += 1;
+  st_.layers_applied += (uint64_t)tp.layers;
+  st_.sweep_bytes += (tp.gen ? 1.0 : 2.0) * std::ldexp(1.0, h) * (double)amp_;
 }
 
 // Runs the sweeps of `level` for fork child `child`, all but the last `skip` of them
@@ -517,14 +739,11 @@ const void *Engine::run_level(int half, int level, uint64_t child, const void *s
   HalfExec &he = half_[half];
   const Level &lev = he.prog.levels[level];
   const Diag fork = he.prog.fork_diag(level, child);
-  const size_t n = lev.sweeps.size() - std::min<size_t>(lev.sweeps.size(), (size_t)skip);
-  for (size_t s = 0; s < n; ++s) {
-    const auto &chunks = he.plans[level][s];
-    for (size_t ci = 0; ci < chunks.size(); ++ci) {
-      const bool first = s == 0 && ci == 0;
-      launch_plan(chunks[ci], first ? fork : Diag(), first, first ? src : dst, dst, he.prog.h);
-    }
-  }
+  (void)lev;
+  const auto &launches = he.plans[level][std::min<size_t>((size_t)skip, he.plans[level].size() - 1)];
+  const size_t n = launches.size();
+  for (size_t i = 0; i < n; ++i)
+    launch_plan(launches[i], i == 0 ? fork : Diag(), i == 0, i == 0 ? src : dst, dst, he.prog.h);
   return n ? dst : src;
 }
 

@@ -35,20 +35,32 @@ struct DevBuf {
   DevBuf &operator=(const DevBuf &) = delete;
 };
 
-// One planned launch of the tile sweep (a Sweep may split into several when it has
-// more than 7 high target bits).
+// One planned sweep launch: a fused multi-layer TMA sweep (FusedSweepParams) or a legacy
+// single-layer register sweep (TileSweepParams; the generated root sweep, or
+// QSIM_OPT_SWEEP_KERNEL 1).  A layer wider than the tile is split into several launches.
 struct TilePlan {
-  TileSweepParams p;  // src/dst/job fields filled at launch
+  bool fused = false;
+  bool multi_layer = false;  // several layers (stage lists) in this launch
+  FusedSweepParams f;        // src/dst/pre filled at launch
+  TileSweepParams p;   // src/dst/job fields filled at launch
   int npass = 1;
-  bool use_pre = false;  // first chunk of a sweep: the sweep's pre diagonal applies
+  int layers = 1;        // gate layers completed by this launch
+  bool use_pre = false;  // the launch applies its pre diagonal (fork diagonal merged at launch)
   bool gen = false;
-  Diag pre;              // the sweep's pre diagonal (fork diagonal merged at launch)
+  Diag pre;
+  std::vector<int> pass0_regs;  // global bits of the pass-0 register slots (pre DiagSplit)
+};
+
+// A stage of a fused sweep: some gates of one layer, then (optionally) a diagonal.
+struct Stage {
+  std::vector<Gate1> gates;
+  Diag diag;
 };
 
 struct HalfExec {
   HalfProgram prog;
   bool tree = false;                                // tile sweeps (true) or the small kernel
-  std::vector<std::vector<std::vector<TilePlan>>> plans;  // [level][sweep][chunk]
+  std::vector<std::vector<std::vector<TilePlan>>> plans;  // [level][lazy skip] -> launches
   // small kernel program on the device
   DevBuf d_levels, d_sweeps;
   bool uploaded = false;
@@ -99,6 +111,8 @@ class Engine {
   int sweep_kernel_ = 0;  // 0: TMA-pipelined sweep, 1: register-only sweep
   int lazy_depth_ = 2;      // up to this many trailing leaf sweeps evaluated at the sampled indices
   bool full_leaf_ = false; // qsim_branch_state: materialise the complete leaf
+  bool fuse_layers_ = false; // fuse consecutive layers into one HBM pass when they fit a tile
+                             // (off by default: multi-pass tiles are not yet faster)
   bool time_sweeps_ = false;
 
   bool have_circuit_ = false;
@@ -132,6 +146,9 @@ class Engine {
   void ensure_device();
   void check(cudaError_t e, const char *what);
   void compile_plans(HalfExec &he);
+  bool plan_fused(const HalfProgram &hp, const std::vector<Stage> &stages, const Diag &pre, TilePlan &tp);
+  std::vector<TilePlan> level_launches(const HalfProgram &hp, const Level &lev, size_t n);
+  std::vector<TilePlan> legacy_plans(const HalfProgram &hp, const Sweep &sw);
   void upload_small(HalfExec &he);
   void ensure_states(int half, int nbuf);
   int materialized_from(int half, size_t free_bytes, int *nbuf);

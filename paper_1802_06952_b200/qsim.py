@@ -13,7 +13,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libqsim.so")
+LIB_PATH = os.environ.get("QSIM_LIB") or os.path.join(_HERE, "libqsim.so")  # QSIM_LIB: A/B builds
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"{LIB_PATH} is missing: build it with `python -m paper_1802_06952_b200.build` "
@@ -28,6 +28,7 @@ QSIM_C64, QSIM_C128 = 0, 1
 QSIM_SX, QSIM_SY, QSIM_T, QSIM_CZ = 1, 2, 3, 4
 QSIM_NO_QUBIT = 0xFFFFFFFF
 QSIM_OPT_TIME_SWEEPS, QSIM_OPT_MODE, QSIM_OPT_MEM_BUDGET, QSIM_OPT_SWEEP_KERNEL, QSIM_OPT_LAZY_LAST = 1, 2, 3, 4, 5
+QSIM_OPT_FUSE_LAYERS = 6
 
 EXPORTED = ["qsim_create", "qsim_destroy", "qsim_last_error", "qsim_version", "qsim_set_option",
             "qsim_set_stream", "qsim_load_circuit", "qsim_partition", "qsim_set_blocks",
@@ -45,7 +46,7 @@ class qsim_stats_t(C.Structure):
     _fields_ = [("kernel_launches", C.c_uint64), ("sweeps", C.c_uint64), ("sweep_states", C.c_uint64),
                 ("sweep_bytes", C.c_double), ("sweep_ms", C.c_double), ("timed_sweeps", C.c_uint64),
                 ("gemm_flops", C.c_double), ("gemm_ms", C.c_double), ("branches_evolved", C.c_uint64),
-                ("lazy_gathers", C.c_uint64)]
+                ("lazy_gathers", C.c_uint64), ("layers_applied", C.c_uint64)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
