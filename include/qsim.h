@@ -192,6 +192,36 @@ qsim_status qsim_comm_init(qsim_ctx *ctx, int rank, int world, const void *uniqu
 /* This rank's share [*begin, *end) of the 2^c branches (contiguous, prefix aligned). */
 qsim_status qsim_rank_range(qsim_ctx *ctx, uint64_t *begin, uint64_t *end);
 
+/* ---------------------------------------------------------------- planner / cost model (f2) */
+
+/* Eq. 2: Time = sum_{i=1..depth} n_i * m * t / s, with n_i the effective
+ * gates of layer i of each half circuit, m the number of half circuits, t the time per gate
+ * and s the number of nodes.  n_i: host array of `depth` values.  EINVAL if s <= 0. */
+qsim_status qsim_eq2_time(const double *n_i, size_t depth, double m, double t, double s, double *seconds);
+
+/* The partition of the loaded circuit and this library's execution plan for it. */
+typedef struct {
+  uint32_t n_qubits;        /* N_r: real qubit count                                    */
+  uint32_t h_upper, h_lower;
+  uint32_t n_cuts;          /* c                                                                */
+  double n_branches;        /* 2^c copies                                                       */
+  double half_circuits;     /* m = 2^(c+1) (Table 2 "equivalent 28-qubit circuits")            */
+  uint32_t N_e;             /* equivalent qubits = max(h_u, h_l) + c + 1 (Table 2)       */
+  uint32_t N_m;             /* largest state the device stores: floor(log2(mem / amp bytes))   */
+  int32_t regime;           /* 0: N_e <= N_m full vectors; 1: N_m < N_e < N_r lossy (sampled);
+                               2: N_e >= N_r no compression                             */
+  double flat_layer_evolutions; /* paper §2.3.1: every copy from scratch, both halves           */
+  double tree_sweeps;       /* this plan: prefix-shared branch tree, both halves, whole job     */
+  double lazy_gathers;      /* leaves whose tail is evaluated at the sampled indices            */
+  double sweep_bytes;       /* algorithmic HBM bytes of tree_sweeps                             */
+  double predicted_s;       /* sweep_bytes / hbm bandwidth (sweeps dominate the run time)       */
+} qsim_cost_t;
+
+/* Cost model of the loaded circuit for sampled blocks of n_upper x n_lower indices on a device
+ * with `hbm_gbps` GB/s of sweep bandwidth.  ESTATE without a circuit; EINVAL if hbm_gbps <= 0. */
+qsim_status qsim_cost_model(qsim_ctx *ctx, uint64_t n_upper, uint64_t n_lower, double hbm_gbps,
+                            qsim_cost_t *out);
+
 /* Counters (see qsim_stats_t).  Synchronises the ctx stream when sweeps are timed. */
 qsim_status qsim_stats(qsim_ctx *ctx, qsim_stats_t *out);
 qsim_status qsim_stats_reset(qsim_ctx *ctx);

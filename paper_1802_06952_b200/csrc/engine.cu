@@ -1159,6 +1159,54 @@ void Engine::rank_range(uint64_t *b0, uint64_t *b1) const {
   *b1 = (uint64_t)(B * (unsigned)(rank_ + 1) / (unsigned)world_);
 }
 
+// ---------------------------------------------------------------- cost model
+void Engine::cost_model(uint64_t nu, uint64_t nl, double hbm_gbps, qsim_cost_t *out) {
+  if (!have_circuit_) throw Error(QSIM_ESTATE, "no circuit loaded");
+  if (!(hbm_gbps > 0.0)) throw Error(QSIM_EINVAL, "hbm_gbps must be > 0");
+  if (!out) throw Error(QSIM_EINVAL, "null output");
+  qsim_cost_t c;
+  std::memset(&c, 0, sizeof(c));
+  const int ncut = (int)circ_.cuts.size();
+  c.n_qubits = circ_.n;
+  c.h_upper = circ_.h_u;
+  c.h_lower = circ_.h_l;
+  c.n_cuts = (uint32_t)ncut;
+  c.n_branches = std::ldexp(1.0, ncut);
+  c.half_circuits = std::ldexp(1.0, ncut + 1);
+  c.N_e = std::max(circ_.h_u, circ_.h_l) + (uint32_t)ncut + 1;
+  double mem = (double)(183359ull << 20);  // B200 (nvidia-smi) when no device is attached yet
+  if (inited_) {
+    size_t f = 0, t = 0;
+    if (cudaMemGetInfo(&f, &t) == cudaSuccess) mem = (double)t;
+  }
+  c.N_m = (uint32_t)std::floor(std::log2(mem / (double)amp_));
+  c.regime = c.N_e <= c.N_m ? 0 : (c.N_e < c.n_qubits ? 1 : 2);
+  c.flat_layer_evolutions = c.n_branches * 2.0 * circ_.depth;
+  for (int h = 0; h < 2; ++h) {
+    const HalfExec &he = half_[h];
+    const HalfProgram &hp = he.prog;
+    const int F = (int)hp.levels.size() - 1;
+    if (!he.tree || he.plans.empty()) continue;  // small states: everything stays in shared memory
+    const int lazy = lazy_depth(h, (int64_t)(h == 0 ? nu : nl));
+    const double state = std::ldexp(1.0, hp.h) * (double)amp_;
+    int m0 = 0;  // levels above m0 are recomputed for every level-m0 node (memory plan)
+    while ((double)(F + 1 - m0) * state > mem - (512.0 * (1 << 20)) && m0 < F) ++m0;
+    std::vector<int> sbits(F + 1, 0);
+    for (int l = 1; l <= F; ++l) sbits[l] = sbits[l - 1] + hp.levels[l].k;
+    for (int l = 0; l <= F; ++l) {
+      const auto &launches = he.plans[l][l == F ? std::min<size_t>(lazy, he.plans[l].size() - 1) : 0];
+      const double nodes = std::ldexp(1.0, sbits[std::max(l, m0)]);
+      for (const TilePlan &tp : launches) {
+        c.tree_sweeps += nodes;
+        c.sweep_bytes += nodes * state * (tp.gen ? 1.0 : 2.0);
+      }
+    }
+    if (lazy > 0) c.lazy_gathers += c.n_branches;
+  }
+  c.predicted_s = c.sweep_bytes / (hbm_gbps * 1e9);
+  *out = c;
+}
+
 // ---------------------------------------------------------------- stats
 void Engine::stats(qsim_stats_t *out) {
   if (inited_) {

@@ -90,6 +90,7 @@ class Engine {
   void branch_state(int half, uint64_t b, void *out);
   void comm_init(int rank, int world, const void *id);
   void rank_range(uint64_t *b0, uint64_t *b1) const;
+  void cost_model(uint64_t nu, uint64_t nl, double hbm_gbps, qsim_cost_t *out);
   void stats(qsim_stats_t *out);
   void stats_reset();
   void synchronize();

@@ -156,6 +156,18 @@ qsim_status qsim_rank_range(qsim_ctx *ctx, uint64_t *b0, uint64_t *b1) {
   });
 }
 
+qsim_status qsim_eq2_time(const double *n_i, size_t depth, double m, double t, double s, double *seconds) {
+  if (!seconds || (depth && !n_i) || !(s > 0.0)) return QSIM_EINVAL;
+  double sum = 0.0;
+  for (size_t i = 0; i < depth; ++i) sum += n_i[i];
+  *seconds = sum * m * t / s;
+  return QSIM_OK;
+}
+
+qsim_status qsim_cost_model(qsim_ctx *ctx, uint64_t nu, uint64_t nl, double hbm_gbps, qsim_cost_t *out) {
+  return guard(ctx, [&](qsim::Engine &e) { e.cost_model(nu, nl, hbm_gbps, out); });
+}
+
 qsim_status qsim_stats(qsim_ctx *ctx, qsim_stats_t *out) {
   return guard(ctx, [&](qsim::Engine &e) {
     if (!out) throw qsim::Error(QSIM_EINVAL, "null output");

@@ -35,7 +35,7 @@ EXPORTED = ["qsim_create", "qsim_destroy", "qsim_last_error", "qsim_version", "q
             "qsim_evolve_range", "qsim_evolve_halves", "qsim_reset_block", "qsim_amplitudes",
             "qsim_sample", "qsim_sample_probs", "qsim_branch_sum", "qsim_branch_state",
             "qsim_nccl_unique_id", "qsim_comm_init", "qsim_rank_range", "qsim_stats",
-            "qsim_stats_reset", "qsim_synchronize"]
+            "qsim_stats_reset", "qsim_synchronize", "qsim_eq2_time", "qsim_cost_model"]
 
 
 class qsim_cut(C.Structure):
@@ -52,8 +52,21 @@ class qsim_stats_t(C.Structure):
         return {k: getattr(self, k) for k, _ in self._fields_}
 
 
+class qsim_cost_t(C.Structure):
+    _fields_ = [("n_qubits", C.c_uint32), ("h_upper", C.c_uint32), ("h_lower", C.c_uint32),
+                ("n_cuts", C.c_uint32), ("n_branches", C.c_double), ("half_circuits", C.c_double),
+                ("N_e", C.c_uint32), ("N_m", C.c_uint32), ("regime", C.c_int32),
+                ("flat_layer_evolutions", C.c_double), ("tree_sweeps", C.c_double),
+                ("lazy_gathers", C.c_double), ("sweep_bytes", C.c_double), ("predicted_s", C.c_double)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
 _P = C.c_void_p
 _sig = {
+    "qsim_eq2_time": (C.c_int, [_P, C.c_size_t, C.c_double, C.c_double, C.c_double, C.POINTER(C.c_double)]),
+    "qsim_cost_model": (C.c_int, [_P, C.c_uint64, C.c_uint64, C.c_double, _P]),
     "qsim_create": (C.c_int, [C.POINTER(_P), C.c_int, C.c_int]),
     "qsim_destroy": (None, [_P]),
     "qsim_last_error": (C.c_char_p, [_P]),
@@ -228,6 +241,20 @@ def qsim_rank_range(ctx):
     b0, b1 = C.c_uint64(), C.c_uint64()
     _check(ctx, _lib.qsim_rank_range(ctx, C.byref(b0), C.byref(b1)))
     return b0.value, b1.value
+
+
+def qsim_eq2_time(n_i, m: float, t: float, s: float) -> float:
+    """Eq. 2: sum(n_i) * m * t / s seconds."""
+    n = np.ascontiguousarray(np.asarray(n_i, dtype=np.float64))
+    out = C.c_double()
+    _check(None, _lib.qsim_eq2_time(_ptr(n), n.size, m, t, s, C.byref(out)))
+    return out.value
+
+
+def qsim_cost_model(ctx, n_upper: int, n_lower: int, hbm_gbps: float) -> dict:
+    c = qsim_cost_t()
+    _check(ctx, _lib.qsim_cost_model(ctx, n_upper, n_lower, hbm_gbps, C.byref(c)))
+    return c.as_dict()
 
 
 def qsim_stats(ctx) -> dict:
