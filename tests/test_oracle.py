@@ -256,3 +256,42 @@ def test_gumbel_eq7():
     rng = np.random.default_rng(0)
     Np = rng.exponential(size=200000)
     assert ST.ks_distance(np.log(Np)) < 0.005
+
+
+def test_ks_distance_vs_scipy():
+    """ks_distance against scipy's one-sample KS with gumbel_l, whose CDF is 1 - exp(-e^z):
+    an independent implementation of both the statistic and Eq. 7's CDF."""
+    from scipy import stats as sps
+    rng = np.random.default_rng(3)
+    for z in (np.log(rng.exponential(size=5000)), rng.normal(size=777), np.array([0.0]), np.array([-1.0, 2.0])):
+        assert ST.ks_distance(z) == pytest.approx(sps.kstest(z, "gumbel_l").statistic, abs=1e-14)
+    assert np.allclose(ST.gumbel_cdf(np.linspace(-30, 3, 99)), sps.gumbel_l.cdf(np.linspace(-30, 3, 99)),
+                       rtol=1e-13, atol=1e-300)
+
+
+def test_porter_thomas_analyzer_oracle():
+    """f1 quantities: Exp(1)-distributed N p gives mean ~ var ~ 1; histogram plus
+    out-of-range counts cover every p > 0 entry; expected counts equal n_pos * P(bin) from
+    scipy's gumbel_l; the degenerate uniform block p = 1/N has z = 0, var 0 and KS distance
+    max(F(0), 1 - F(0)) = 1 - 1/e."""
+    from scipy import stats as sps
+    n = 20
+    rng = np.random.default_rng(11)
+    p = rng.exponential(scale=2.0 ** -n, size=1 << 16)
+    p[:5] = 0.0
+    r = ST.porter_thomas(p, n, -6.0, 2.0, 64)
+    assert r["count"] == 1 << 16 and r["zeros"] == 5
+    assert abs(r["mean_Np"] - 1) < 0.02 and abs(r["var_Np"] - 1) < 0.05
+    assert int(r["hist"].sum()) + r["below"] + r["above"] == (1 << 16) - 5
+    P = np.diff(sps.gumbel_l.cdf(np.linspace(-6.0, 2.0, 65)))
+    assert np.allclose(r["expected"], ((1 << 16) - 5) * P, rtol=1e-10)
+    assert r["ks"] < 0.01
+    # chi-square of the histogram against Eq. 7's counts
+    e = r["expected"]
+    m = e > 20
+    chi2 = float(np.sum((r["hist"][m] - e[m]) ** 2 / e[m]))
+    assert chi2 < m.sum() + 6 * math.sqrt(2 * m.sum())
+    u = ST.porter_thomas(np.full(64, 2.0 ** -6), 6, -1.0, 1.0, 4)
+    assert u["var_Np"] == 0.0 and u["mean_Np"] == 1.0
+    assert list(u["hist"]) == [0, 0, 64, 0]
+    assert u["ks"] == pytest.approx(1 - math.exp(-1), abs=1e-15)
