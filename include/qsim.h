@@ -171,6 +171,38 @@ qsim_status qsim_sample_probs(qsim_ctx *ctx, const double *p, const uint64_t *up
                               uint32_t h_lower, uint64_t seed, size_t n_draws,
                               uint64_t *bitstrings, double *block_mass);
 
+/* ---------------------------------------------------------------- Porter-Thomas analyzer (f1) */
+
+/* Statistics of x = N p, N = 2^n_qubits, over a probability block (Fig. 5).
+ * Porter-Thomas: x ~ Exp(1), so mean ~ 1 and var ~ 1; z = ln x follows Eq. 7 (alpha = 1) with
+ * CDF F(z) = 1 - exp(-e^z) = 1 - exp(-x).  The Kolmogorov-Smirnov distance
+ * D = sup_t |F_emp(t) - t| of u = F(z) over the entries with p > 0 is bracketed from a
+ * 2^20-bin histogram of u: ks_lo <= D <= ks_hi, ks_hi - ks_lo <= 2^-20 + (largest bin)/n_pos. */
+typedef struct {
+  double count;     /* entries analysed (zeros included)                             */
+  double zeros;     /* entries with p == 0 (excluded from z and the KS distance)     */
+  double mean_Np;   /* (1/count) sum N p                                             */
+  double var_Np;    /* (1/count) sum (N p)^2 - mean_Np^2 (population variance)        */
+  double ks_lo, ks_hi;
+  double below, above; /* p > 0 entries with z < z_lo or z >= z_hi (not in hist)     */
+  uint32_t n_qubits;
+  uint32_t n_bins;
+} qsim_pt_t;
+
+/* qsim_porter_thomas — the analyzer on the (reduced) block of the last qsim_evolve_range calls
+ * (p = |a|^2 as qsim_sample computes it) when p == NULL, else on caller-given host
+ * probabilities p[n] (no circuit needed).
+ *  n_qubits: N = 2^n_qubits; 0 = the loaded circuit's qubit count (EINVAL without one).
+ *  z histogram: n_bins (1..8192) equal bins over [z_lo, z_hi); bin = floor((z - z_lo) n_bins /
+ *  (z_hi - z_lo)) in fp64.  hist: host uint64[n_bins] counts (nullable); expected: host
+ *  double[n_bins] (nullable) = (count - zeros) (F(e_{k+1}) - F(e_k)), the Eq. 7 prediction
+ *  for the same bins (Fig. 5's theory curve).  ESTATE with p == NULL and no evolved block;
+ *  EINVAL on n > 2^32 - 1, bad bins or p < 0.  With a communicator the block is reduced
+ *  first (every rank calls) and only rank 0 writes outputs. */
+qsim_status qsim_porter_thomas(qsim_ctx *ctx, const double *p, size_t n, uint32_t n_qubits, double z_lo,
+                               double z_hi, uint32_t n_bins, uint64_t *hist, double *expected,
+                               qsim_pt_t *out);
+
 /* qsim_branch_sum — the reconstruction contraction alone (a6): A[i,j] = sum_b U[b,i] L[b,j]
  * for host slices U[n_branches, n_upper], L[n_branches, n_lower] (complex of the ctx
  * precision); A: host complex double [n_upper, n_lower].  No circuit needed. */

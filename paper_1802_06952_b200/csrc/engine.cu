@@ -1081,6 +1081,72 @@ void Engine::sample_probs(const double *p, const uint64_t *up, size_t nu, const 
   run_sampler(p_.as<double>(), (int64_t)nu, (int64_t)nl, dsu, dsl, hl, seed, n, out, mass ? mass : &W);
 }
 
+void Engine::porter_thomas(const double *p, size_t n, uint32_t nq, double z_lo, double z_hi, uint32_t nb,
+                           uint64_t *hist, double *expected, qsim_pt_t *out) {
+  if (!out) throw Error(QSIM_EINVAL, "null output");
+  if (nb < 1 || nb > (uint32_t)PT_MAX_Z_BINS) throw Error(QSIM_EINVAL, "n_bins must be in 1..8192");
+  if (!(z_hi > z_lo) || !std::isfinite(z_lo) || !std::isfinite(z_hi)) throw Error(QSIM_EINVAL, "bad z range");
+  if (nq == 0) {
+    if (!have_circuit_) throw Error(QSIM_EINVAL, "n_qubits = 0 needs a loaded circuit");
+    nq = circ_.n;
+  }
+  if (nq > 1000) throw Error(QSIM_EINVAL, "n_qubits too large");
+  if (p) {
+    if (n == 0 || n >= (1ull << 32)) throw Error(QSIM_EINVAL, "n must be in 1..2^32-1");
+    for (size_t i = 0; i < n; ++i)
+      if (!(p[i] >= 0.0)) throw Error(QSIM_EINVAL, "probabilities must be >= 0");
+  } else if (!have_blocks_) {
+    throw Error(QSIM_ESTATE, "no blocks evolved");
+  }
+  ensure_device();
+  const void *in = nullptr;
+  if (p) {
+    p_.reserve(n * 8);
+    check(cudaMemcpyAsync(p_.ptr, p, n * 8, cudaMemcpyHostToDevice, stream_), "upload p");
+    in = p_.ptr;
+  } else {
+    in = reduced_block();
+    n = Su_.size() * Sl_.size();
+    if (!in) {  // not rank 0: the reduction is done, nothing to analyse here
+      check(cudaStreamSynchronize(stream_), "porter_thomas");
+      std::memset(out, 0, sizeof(*out));
+      return;
+    }
+    if (n >= (1ull << 32)) throw Error(QSIM_EINVAL, "block larger than 2^32-1 entries");
+  }
+  pt_.reserve(PtScratch::bytes((int)nb));
+  check(launch_porter_thomas(in, p == nullptr, (int64_t)n, (int)nq, z_lo, z_hi, (int)nb, pt_.ptr, stream_),
+        "porter_thomas");
+  st_.kernel_launches += 2;
+  PtResult r;
+  std::vector<unsigned> zh(nb);
+  check(cudaMemcpyAsync(&r, pt_result(pt_.ptr), sizeof(r), cudaMemcpyDeviceToHost, stream_), "D2H pt");
+  check(cudaMemcpyAsync(zh.data(), pt_zhist(pt_.ptr), nb * 4, cudaMemcpyDeviceToHost, stream_), "D2H hist");
+  check(cudaStreamSynchronize(stream_), "porter_thomas");
+  const double cnt = (double)n, npos = (double)(n - r.zeros);
+  out->count = cnt;
+  out->zeros = (double)r.zeros;
+  out->mean_Np = r.s1 / cnt;
+  out->var_Np = r.s2 / cnt - out->mean_Np * out->mean_Np;
+  out->ks_lo = r.ks_lo;
+  out->ks_hi = r.ks_hi;
+  out->below = (double)r.below;
+  out->above = (double)r.above;
+  out->n_qubits = nq;
+  out->n_bins = nb;
+  if (hist)
+    for (uint32_t k = 0; k < nb; ++k) hist[k] = zh[k];
+  if (expected) {  // Eq. 7 with alpha = 1: F(z) = 1 - exp(-e^z)
+    const double w = (z_hi - z_lo) / nb;
+    double F0 = -std::expm1(-std::exp(z_lo));
+    for (uint32_t k = 0; k < nb; ++k) {
+      const double F1 = -std::expm1(-std::exp(z_lo + (k + 1) * w));
+      expected[k] = npos * (F1 - F0);
+      F0 = F1;
+    }
+  }
+}
+
 void Engine::branch_sum(const void *U, const void *L, size_t nb, size_t nu, size_t nl, void *A) {
   if (!U || !L || !A || nb == 0 || nu == 0 || nl == 0) throw Error(QSIM_EINVAL, "empty slices");
   ensure_device();

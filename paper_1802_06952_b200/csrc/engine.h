@@ -86,6 +86,8 @@ class Engine {
   void sample(uint64_t seed, size_t n, uint64_t *out, double *mass);
   void sample_probs(const double *p, const uint64_t *up, size_t nu, const uint64_t *lo, size_t nl,
                     uint32_t hl, uint64_t seed, size_t n, uint64_t *out, double *mass);
+  void porter_thomas(const double *p, size_t n, uint32_t n_qubits, double z_lo, double z_hi, uint32_t n_bins,
+                     uint64_t *hist, double *expected, qsim_pt_t *out);
   void branch_sum(const void *U, const void *L, size_t nb, size_t nu, size_t nl, void *A);
   void branch_state(int half, uint64_t b, void *out);
   void comm_init(int rank, int world, const void *id);
@@ -132,6 +134,7 @@ class Engine {
   size_t state_bytes_ = 0;
   // sampler
   DevBuf p_, C_, r_, R_, W_, draws_, tmp_;
+  DevBuf pt_;  // Porter-Thomas analyzer scratch
 
   // comm
   ncclComm_t comm_ = nullptr;

@@ -194,4 +194,26 @@ cudaError_t launch_draws(const double *p, const double *C, const double *r, cons
                          uint64_t *out, cudaStream_t s);
 cudaError_t launch_cast_c128_to_c64(const double *A, int64_t n, float *out, cudaStream_t s);
 
+// Porter-Thomas analyzer (stats.cu).  Input: complex block A (double2, p = fma(re,re,im*im))
+// when `complex_in`, else probabilities.  Scratch (device, PtScratch::bytes): z / u histograms,
+// per-CTA moment partials; result: PtResult on the device.
+constexpr int PT_U_BINS = 1 << 20;
+constexpr int PT_MAX_Z_BINS = 8192;
+constexpr int PT_CTAS = 148 * 4;
+struct PtResult {
+  unsigned long long zeros, below, above;
+  double s1, s2;      // sum x, sum x^2 (fixed order over CTA partials)
+  double ks_lo, ks_hi;
+};
+struct PtScratch {
+  static size_t bytes(int n_bins) {
+    return (size_t)PT_U_BINS * 4 + (size_t)PT_MAX_Z_BINS * 4 + (size_t)PT_CTAS * 2 * 8 + sizeof(PtResult) + 64;
+  }
+};
+cudaError_t launch_porter_thomas(const void *in, bool complex_in, int64_t n, int n_qubits, double z_lo,
+                                 double z_hi, int n_bins, void *scratch, cudaStream_t s);
+// device pointers into the scratch block
+unsigned *pt_zhist(void *scratch);
+const PtResult *pt_result(void *scratch);
+
 }  // namespace qsim

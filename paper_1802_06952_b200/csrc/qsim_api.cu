@@ -127,6 +127,14 @@ qsim_status qsim_sample_probs(qsim_ctx *ctx, const double *p, const uint64_t *up
   return guard(ctx, [&](qsim::Engine &e) { e.sample_probs(p, up, nu, lo, nl, hl, seed, n, out, mass); });
 }
 
+qsim_status qsim_porter_thomas(qsim_ctx *ctx, const double *p, size_t n, uint32_t n_qubits, double z_lo,
+                               double z_hi, uint32_t n_bins, uint64_t *hist, double *expected,
+                               qsim_pt_t *out) {
+  return guard(ctx, [&](qsim::Engine &e) {
+    e.porter_thomas(p, n, n_qubits, z_lo, z_hi, n_bins, hist, expected, out);
+  });
+}
+
 qsim_status qsim_branch_sum(qsim_ctx *ctx, const void *U, const void *L, size_t nb, size_t nu, size_t nl,
                             void *A) {
   return guard(ctx, [&](qsim::Engine &e) { e.branch_sum(U, L, nb, nu, nl, A); });

@@ -35,7 +35,8 @@ EXPORTED = ["qsim_create", "qsim_destroy", "qsim_last_error", "qsim_version", "q
             "qsim_evolve_range", "qsim_evolve_halves", "qsim_reset_block", "qsim_amplitudes",
             "qsim_sample", "qsim_sample_probs", "qsim_branch_sum", "qsim_branch_state",
             "qsim_nccl_unique_id", "qsim_comm_init", "qsim_rank_range", "qsim_stats",
-            "qsim_stats_reset", "qsim_synchronize", "qsim_eq2_time", "qsim_cost_model"]
+            "qsim_stats_reset", "qsim_synchronize", "qsim_eq2_time", "qsim_cost_model",
+            "qsim_porter_thomas"]
 
 
 class qsim_cut(C.Structure):
@@ -63,8 +64,19 @@ class qsim_cost_t(C.Structure):
         return {k: getattr(self, k) for k, _ in self._fields_}
 
 
+class qsim_pt_t(C.Structure):
+    _fields_ = [("count", C.c_double), ("zeros", C.c_double), ("mean_Np", C.c_double), ("var_Np", C.c_double),
+                ("ks_lo", C.c_double), ("ks_hi", C.c_double), ("below", C.c_double), ("above", C.c_double),
+                ("n_qubits", C.c_uint32), ("n_bins", C.c_uint32)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
 _P = C.c_void_p
 _sig = {
+    "qsim_porter_thomas": (C.c_int, [_P, _P, C.c_size_t, C.c_uint32, C.c_double, C.c_double, C.c_uint32, _P, _P,
+                                     C.POINTER(qsim_pt_t)]),
     "qsim_eq2_time": (C.c_int, [_P, C.c_size_t, C.c_double, C.c_double, C.c_double, C.POINTER(C.c_double)]),
     "qsim_cost_model": (C.c_int, [_P, C.c_uint64, C.c_uint64, C.c_double, _P]),
     "qsim_create": (C.c_int, [C.POINTER(_P), C.c_int, C.c_int]),
@@ -209,6 +221,20 @@ def qsim_sample_probs(ctx, p, upper_block, lower_block, h_lower: int, seed: int,
     _check(ctx, _lib.qsim_sample_probs(ctx, _ptr(p), _ptr(u), u.size, _ptr(l), l.size, h_lower, seed, n_draws,
                                        _ptr(out), C.byref(mass)))
     return out, mass.value
+
+
+def qsim_porter_thomas(ctx, p=None, n_qubits: int = 0, z_lo: float = -12.0, z_hi: float = 4.0,
+                       n_bins: int = 160):
+    """Porter-Thomas / Eq. 7 analyzer (f1).  p=None: the evolved block.  Returns
+    (stats dict, z histogram uint64[n_bins], Eq. 7 expected counts float64[n_bins])."""
+    hist = np.zeros(n_bins, dtype=np.uint64)
+    expected = np.zeros(n_bins, dtype=np.float64)
+    r = qsim_pt_t()
+    if p is not None:
+        p = np.ascontiguousarray(np.asarray(p, dtype=np.float64)).ravel()
+    _check(ctx, _lib.qsim_porter_thomas(ctx, _ptr(p), 0 if p is None else p.size, n_qubits, z_lo, z_hi, n_bins,
+                                        _ptr(hist), _ptr(expected), C.byref(r)))
+    return r.as_dict(), hist, expected
 
 
 def qsim_branch_sum(ctx, U, L, prec: int):
