@@ -85,8 +85,8 @@ typedef enum {
   QSIM_OPT_MODE = 2,        /* 0: auto, 1: flat in-shared-memory per-branch kernel (h <= 12),
                                2: prefix-shared branch tree of tile sweeps (h >= 13)          */
   QSIM_OPT_MEM_BUDGET = 3,  /* cap in bytes on device memory for half-state buffers (0 = free memory) */
-  QSIM_OPT_SWEEP_KERNEL = 4, /* 0: fused TMA-pipelined sweep (default); 1: register-only one-layer sweep;
-                                (comparison)                                                            */
+  QSIM_OPT_SWEEP_KERNEL = 4, /* 0: TMA-pipelined sweep (default); 1: register-only one-layer sweep
+                                (comparison); 2 / 3: the TMA sweep with 2 / 3 shared-memory stages      */
   QSIM_OPT_LAZY_LAST = 5     /* lazy tail of each leaf, evaluated only at the sampled indices during the
                                 gather instead of full 2^h passes: 0 off, 1 the last sweep, 2 (default)
                                 the last one or two by a cost model, 3 always two when possible      */,

@@ -197,7 +197,7 @@ void Engine::set_option(int key, int64_t value) {
         for (int h = 0; h < 2; ++h) compile_plans(half_[h]);
       return;
     case QSIM_OPT_SWEEP_KERNEL:
-      if (value < 0 || value > 1) throw Error(QSIM_EINVAL, "QSIM_OPT_SWEEP_KERNEL must be 0 or 1");
+      if (value < 0 || value > 3) throw Error(QSIM_EINVAL, "QSIM_OPT_SWEEP_KERNEL must be 0, 1, 2 or 3");
       sweep_kernel_ = (int)value;
       if (have_circuit_)
         for (int h = 0; h < 2; ++h) compile_plans(half_[h]);
@@ -673,6 +673,17 @@ void Engine::resolve_events() {
 }
 
 // ---------------------------------------------------------------- executor
+// Shared-memory stages of the TMA sweep (QSIM_OPT_SWEEP_KERNEL 0): two 64 KB stages, or three
+// for the sweeps that hold a stage longer per byte delivered (QSIM_TMA_STAGE_RULE, A/B only:
+// 1 = short runs (< 4 KB) or two passes, 2 = short runs, 3 = two passes).
+int Engine::tma_stages(const TilePlan &tp) const {
+  static const int rule = std::getenv("QSIM_TMA_STAGE_RULE") ? std::atoi(std::getenv("QSIM_TMA_STAGE_RULE")) : 1;
+  if (rule == 1) return (tp.p.run_m < 3 || tp.npass == 2) ? 3 : 2;
+  if (rule == 2) return tp.p.run_m < 3 ? 3 : 2;
+  if (rule == 3) return tp.npass == 2 ? 3 : 2;
+  return 2;
+}
+
 void Engine::launch_plan(const TilePlan &tp, const Diag &fork, bool first, const void *src, void *dst,
                          int h) {
   int pre_mode = 0;
@@ -713,7 +724,8 @@ void Engine::launch_plan(const TilePlan &tp, const Diag &fork, bool first, const
     if (tma) {
       if (pre_mode == 1) p.pre_s = make_split(pre, vs, reg_positions(p, 0, c128_));
       const int grid = (int)std::min<uint64_t>(tiles, (uint64_t)num_sms_);
-      check(launch_tile_sweep_tma(p, c128_, pre_mode, tp.npass, grid, stream_, sweep_kernel_ == 2 ? 3 : 2),
+      const int stages = sweep_kernel_ == 2 ? 2 : sweep_kernel_ == 3 ? 3 : tma_stages(tp);
+      check(launch_tile_sweep_tma(p, c128_, pre_mode, tp.npass, grid, stream_, stages),
             "tma sweep launch");
     } else {
       const int grid = (int)std::min<uint64_t>(tiles, (uint64_t)num_sms_ * (tp.npass == 1 ? occ1_ : occ2_));

@@ -111,7 +111,7 @@ class Engine {
   int occ1_ = 2, occ2_ = 2;
   int mode_ = 0;
   int64_t mem_budget_ = 0;
-  int sweep_kernel_ = 0;  // 0: TMA-pipelined sweep, 1: register-only sweep
+  int sweep_kernel_ = 0;  // 0: TMA sweep (auto stages), 1: register-only, 2 / 3: TMA with 2 / 3 stages
   int lazy_depth_ = 2;      // up to this many trailing leaf sweeps evaluated at the sampled indices
   bool full_leaf_ = false; // qsim_branch_state: materialise the complete leaf
   bool fuse_layers_ = false; // fuse consecutive layers into one HBM pass when they fit a tile
@@ -161,6 +161,7 @@ class Engine {
   void evolve_half(int half, uint64_t b0, uint64_t b1, void *slice, const uint64_t *dS, int64_t nS);
   const void *run_level(int half, int level, uint64_t child, const void *src, void *dst, int skip);
   int lazy_depth(int half, int64_t nS) const;
+  int tma_stages(const TilePlan &tp) const;
   void launch_plan(const TilePlan &tp, const Diag &fork, bool first_chunk_of_level, const void *src,
                    void *dst, int h);
   void gather_leaf(int half, uint64_t child_last, const void *psi, const uint64_t *dS, int64_t nS,
