@@ -42,17 +42,19 @@ void Engine::check(cudaError_t e, const char *what) {
   }
 }
 
-static DiagDev to_dev(const Diag &d, int vs, bool force_active = false) {
+static DiagDev to_dev(const Diag &d, bool force_active = false) {
   DiagDev o;
+  std::memset(&o, 0, sizeof(o));
   o.t1 = d.t1;
   o.t2 = d.t2;
   o.zm = d.zm;
-  o.hm = d.hm;
-  o.vm = d.vm;
   o.pm = d.pm;
   o.pv = d.pv & d.pm;
-  o.vs = vs >= 32 ? 31 : vs;
-  if (vs >= 32) o.vm = 0;
+  for (int k = 1; k < 32; ++k)
+    if (d.cz[k]) {
+      o.czd[o.ncz] = (uint8_t)k;
+      o.czm[o.ncz++] = d.cz[k];
+    }
   o.ph0 = d.ph0 & 7;
   o.active = (force_active || !d.identity()) ? 1 : 0;
   o.scale = d.scale();
@@ -66,10 +68,10 @@ static DiagDev to_dev(const Diag &d, int vs, bool force_active = false) {
 
 // DiagSplit of a diagonal for the register slots at global bit positions regpos
 // (slot index bit j <-> regpos[j]); see kernels.h.
-static DiagSplit make_split(const Diag &d, int vs, const std::vector<int> &regpos) {
+static DiagSplit make_split(const Diag &d, const std::vector<int> &regpos) {
   DiagSplit s;
   std::memset(&s, 0, sizeof(s));
-  const DiagDev dd = to_dev(d, vs, true);
+  const DiagDev dd = to_dev(d, true);
   uint32_t Rbits = 0;
   for (int p : regpos) Rbits |= 1u << p;
   const int nslots = 1 << regpos.size();
@@ -77,9 +79,9 @@ static DiagSplit make_split(const Diag &d, int vs, const std::vector<int> &regpo
     uint32_t R = 0;
     for (size_t j = 0; j < regpos.size(); ++j)
       if ((idx >> j) & 1) R |= 1u << regpos[j];
-    const int ph = dd.ph0 + __builtin_popcount(R & dd.t1) + 2 * __builtin_popcount(R & dd.t2) +
-                   4 * (__builtin_popcount(R & dd.zm) + __builtin_popcount(R & (R >> 1) & dd.hm) +
-                        __builtin_popcount(R & (R >> dd.vs) & dd.vm));
+    int ph = dd.ph0 + __builtin_popcount(R & dd.t1) + 2 * __builtin_popcount(R & dd.t2) +
+             4 * __builtin_popcount(R & dd.zm);
+    for (int k = 1; k < 32; ++k) ph += 4 * __builtin_popcount(R & (R >> k) & d.cz[k]);
     const bool okR = (R & dd.pm & Rbits) == (dd.pv & dd.pm & Rbits);
     s.P[idx] = (uint8_t)((ph & 7) << 3);
     if (!okR) s.notok |= 1u << idx;
@@ -87,11 +89,11 @@ static DiagSplit make_split(const Diag &d, int vs, const std::vector<int> &regpo
   s.has_proj = (dd.pm != 0) ? 1 : 0;
   for (size_t j = 0; j < regpos.size(); ++j) {
     const int p = regpos[j];
-    uint32_t N = 0;
-    if (((dd.hm >> p) & 1u) && p + 1 < 32) N |= 1u << (p + 1);
-    if (p >= 1 && ((dd.hm >> (p - 1)) & 1u)) N |= 1u << (p - 1);
-    if (((dd.vm >> p) & 1u) && p + dd.vs < 32) N |= 1u << (p + dd.vs);
-    if (p >= dd.vs && ((dd.vm >> (p - dd.vs)) & 1u)) N |= 1u << (p - dd.vs);
+    uint32_t N = 0;  // partners of register bit p in CZ pairs
+    for (int k = 1; k < 32; ++k) {
+      if (((d.cz[k] >> p) & 1u) && p + k < 32) N |= 1u << (p + k);
+      if (p >= k && ((d.cz[k] >> (p - k)) & 1u)) N |= 1u << (p - k);
+    }
     s.N[j] = N & ~Rbits;
   }
   s.Bpm = dd.pm & ~Rbits;
@@ -106,6 +108,7 @@ static std::vector<int> reg_positions(const TileSweepParams &p, int pass, bool c
   for (int s = 0; s < 4; ++s) pos.push_back(p.hb[p.gsel[pass][s]]);
   return pos;
 }
+
 
 // ---------------------------------------------------------------- construction
 Engine::Engine(qsim_precision prec, int device) : prec_(prec), device_(device) {
@@ -223,6 +226,15 @@ void Engine::load_circuit(uint32_t rows, uint32_t cols, uint32_t depth, const qs
     half_[h].prog = compile_half(circ_, h == 0);
     half_[h].uploaded = false;
     compile_plans(half_[h]);
+    if (half_[h].tree) {  // relabel qubits to physical bits for long tile runs (choose_perm)
+      const std::vector<int> perm = choose_perm(half_[h]);
+      bool ident = true;
+      for (size_t b = 0; b < perm.size(); ++b) ident = ident && perm[b] == (int)b;
+      if (!ident) {
+        half_[h].prog = compile_half(circ_, h == 0, perm);
+        compile_plans(half_[h]);
+      }
+    }
   }
   have_circuit_ = true;
   have_blocks_ = false;
@@ -356,8 +368,8 @@ bool Engine::plan_fused(const HalfProgram &hp, const std::vector<Stage> &stages,
   };
   f.ndiag = (int)diags.size();
   for (size_t d = 0; d < diags.size(); ++d) {
-    f.diag[d] = to_dev(diags[d], hp.vs, true);
-    f.diag_s[d] = make_split(diags[d], hp.vs, regpos(diag_pass[d]));
+    f.diag[d] = to_dev(diags[d], true);
+    f.diag_s[d] = make_split(diags[d], regpos(diag_pass[d]));
   }
   outer_runs(hb, L, hp.h, f.run_start, f.run_len, &f.nruns);
   f.log2_ntiles = hp.h - T;
@@ -457,6 +469,107 @@ void Engine::compile_plans(HalfExec &he) {
   }
 }
 
+// Qubit-to-bit relabelling of a tree half (program.h HalfProgram::perm).  A tile sweep is fastest
+// when its rows are long: the hi bits of the tile (the layer's targets above the L low bits,
+// padded with the lowest free bits) should start at bit L and be consecutive (run of 2^(L+m)
+// amplitudes), with few hi targets (> 4 need a second register pass) and few targets on lane
+// bits (shuffles).  Speed model from tools/sweep_micro.py on B200 (one layer repeated, GB/s):
+// by m = 0..7 about 4940, 5310, 5680, 5930, 5990, 6020, 6040, 6050; a second pass costs ~3 % (c64)
+// and, in c128 with 6-7 hi targets, ~30 %; each lane-bit target ~2 % (c64) / 3 % (c128).  The cost
+// of a permutation is the sum over the sweeps that run as full passes of (nodes executing the
+// sweep) / speed; a seeded local search over transpositions minimises it.
+// QSIM_PERM = id | rev | rand | auto (default) for tests.
+std::vector<int> Engine::choose_perm(const HalfExec &he) const {
+  const HalfProgram &hp = he.prog;
+  const int h = hp.h, L = tile_low_bits(c128_);
+  std::vector<int> perm(h);
+  for (int b = 0; b < h; ++b) perm[b] = b;
+  const char *mode = std::getenv("QSIM_PERM");
+  const std::string m = mode ? mode : "auto";
+  if (m == "id") return perm;
+  if (m == "rev") {
+    for (int b = 0; b < h; ++b) perm[b] = h - 1 - b;
+    return perm;
+  }
+  uint64_t rng = 0x9E3779B97F4A7C15ull ^ (uint64_t)h;
+  auto next = [&]() {
+    rng ^= rng << 13;
+    rng ^= rng >> 7;
+    rng ^= rng << 17;
+    return rng;
+  };
+  if (m == "rand") {
+    for (int b = h - 1; b > 0; --b) std::swap(perm[b], perm[(int)(next() % (uint64_t)(b + 1))]);
+    return perm;
+  }
+  // sweeps (target canonical bits) and their execution weights
+  struct SW {
+    std::vector<int> bits;
+    double w;
+  };
+  std::vector<SW> sws;
+  const int F = (int)hp.levels.size() - 1;
+  int sbits = 0;
+  for (int l = 0; l <= F; ++l) {
+    sbits += hp.levels[l].k;
+    const auto &sw = hp.levels[l].sweeps;
+    const size_t lazy = (l == F && lazy_depth_ > 0) ? std::min<size_t>(2, sw.size() > 0 ? sw.size() - 1 : 0) : 0;
+    for (size_t i = 0; i + lazy < sw.size(); ++i) {
+      if (sw[i].gen || sw[i].gates.empty()) continue;
+      SW x;
+      for (auto &g : sw[i].gates) x.bits.push_back(g.bit);  // identity program: canonical bits
+      x.w = std::ldexp(1.0, sbits);
+      sws.push_back(x);
+    }
+  }
+  static const double speed[8] = {4940, 5310, 5680, 5930, 5990, 6020, 6040, 6050};
+  const int VB = c128_ ? 0 : 1;
+  auto cost = [&](const std::vector<int> &p) {
+    double c = 0;
+    for (const SW &x : sws) {
+      std::vector<int> hi;
+      int nlane = 0;
+      for (int b : x.bits) {
+        if (p[b] >= L)
+          hi.push_back(p[b]);
+        else if (p[b] >= VB)
+          ++nlane;
+      }
+      std::sort(hi.begin(), hi.end());
+      const size_t nch = std::max<size_t>(1, (hi.size() + kHiBits - 1) / kHiBits);
+      for (size_t ci = 0; ci < nch; ++ci) {
+        std::vector<int> hb;
+        for (size_t i = 0; i < hi.size(); ++i)
+          if (i * nch / std::max<size_t>(1, hi.size()) == ci) hb.push_back(hi[i]);
+        for (int b = L; (int)hb.size() < kHiBits && b < h; ++b)
+          if (std::find(hb.begin(), hb.end(), b) == hb.end()) hb.push_back(b);
+        int mm = 0;
+        while (mm < kHiBits && std::find(hb.begin(), hb.end(), L + mm) != hb.end()) ++mm;
+        const size_t k = hi.size() / nch;
+        double v = speed[std::min(mm, 7)];
+        if (k > 4) v *= c128_ ? (k > 5 ? 0.70 : 0.96) : 0.97;
+        if (ci == 0) v *= 1.0 - (c128_ ? 0.03 : 0.02) * nlane;
+        c += x.w / v;
+      }
+    }
+    return c;
+  };
+  std::vector<int> best = perm;
+  double bc = cost(best);
+  for (int it = 0; it < 6000; ++it) {
+    std::vector<int> q = best;
+    const int i = (int)(next() % (uint64_t)h), j = (int)(next() % (uint64_t)h);
+    if (i == j) continue;
+    std::swap(q[i], q[j]);
+    const double c = cost(q);
+    if (c <= bc) {
+      best = q;
+      bc = c;
+    }
+  }
+  return best;
+}
+
 // Legacy per-sweep plans (register-only kernel; the generated root sweep).
 std::vector<TilePlan> Engine::legacy_plans(const HalfProgram &hp, const Sweep &sw) {
   std::vector<TilePlan> out;
@@ -540,8 +653,8 @@ std::vector<TilePlan> Engine::legacy_plans(const HalfProgram &hp, const Sweep &s
         tp.gen = sw.gen && ci == 0;
         tp.pre = sw.pre;
         const Diag post = ci == nchunks - 1 ? sw.post : Diag();
-        tp.p.post = to_dev(post, hp.vs);
-        tp.p.post_s = make_split(post, hp.vs, reg_positions(tp.p, tp.npass - 1, c128_));
+        tp.p.post = to_dev(post);
+        tp.p.post_s = make_split(post, reg_positions(tp.p, tp.npass - 1, c128_));
         int m = 0;
         while (m < kHiBits && hb[m] == L + m) ++m;
         tp.p.run_m = m;
@@ -569,8 +682,8 @@ void Engine::upload_small(HalfExec &he) {
     for (auto &sw : lev.sweeps) {
       SmallSweepDev s;
       std::memset(&s, 0, sizeof(s));
-      s.pre = to_dev(sw.pre, hp.vs, sw.gen);
-      s.post = to_dev(sw.post, hp.vs);
+      s.pre = to_dev(sw.pre, sw.gen);
+      s.post = to_dev(sw.post);
       s.gen = sw.gen ? 1 : 0;
       s.ngates = (int)sw.gates.size();
       for (size_t g = 0; g < sw.gates.size(); ++g) {
@@ -620,6 +733,14 @@ void Engine::set_blocks(const uint64_t *up, size_t nu, const uint64_t *lo, size_
   d_Sl_.reserve(nl * 8);
   check(cudaMemcpyAsync(d_Su_.ptr, up, nu * 8, cudaMemcpyHostToDevice, stream_), "upload S_u");
   check(cudaMemcpyAsync(d_Sl_.ptr, lo, nl * 8, cudaMemcpyHostToDevice, stream_), "upload S_l");
+  for (int h = 0; h < 2; ++h) {
+    const std::vector<uint64_t> &S = h == 0 ? Su_ : Sl_;
+    std::vector<uint64_t> P(S.size());
+    for (size_t i = 0; i < S.size(); ++i) P[i] = half_[h].prog.phys(S[i]);
+    d_Sp_[h].reserve(P.size() * 8);
+    check(cudaMemcpyAsync(d_Sp_[h].ptr, P.data(), P.size() * 8, cudaMemcpyHostToDevice, stream_), "upload S");
+    check(cudaStreamSynchronize(stream_), "upload S");  // P is a temporary
+  }
   A_acc_.reserve(nu * nl * 16);
   check(cudaMemsetAsync(A_acc_.ptr, 0, nu * nl * 16, stream_), "zero block");
   check(cudaStreamSynchronize(stream_), "set_blocks");
@@ -673,11 +794,11 @@ void Engine::resolve_events() {
 }
 
 // ---------------------------------------------------------------- executor
-// Shared-memory stages of the TMA sweep (QSIM_OPT_SWEEP_KERNEL 0): two 64 KB stages, or three
-// for the sweeps that hold a stage longer per byte delivered (QSIM_TMA_STAGE_RULE, A/B only:
-// 1 = short runs (< 4 KB) or two passes, 2 = short runs, 3 = two passes).
+// Shared-memory stages of the TMA sweep (QSIM_OPT_SWEEP_KERNEL 0): two 64 KB stages, or three for
+// tiles of short runs (< 4 KB: more, smaller requests in flight per byte).  QSIM_TMA_STAGE_RULE
+// (A/B only): 0 = always two, 1 = short runs or two passes, 2 = short runs (default), 3 = two passes.
 int Engine::tma_stages(const TilePlan &tp) const {
-  static const int rule = std::getenv("QSIM_TMA_STAGE_RULE") ? std::atoi(std::getenv("QSIM_TMA_STAGE_RULE")) : 1;
+  static const int rule = std::getenv("QSIM_TMA_STAGE_RULE") ? std::atoi(std::getenv("QSIM_TMA_STAGE_RULE")) : 2;
   if (rule == 1) return (tp.p.run_m < 3 || tp.npass == 2) ? 3 : 2;
   if (rule == 2) return tp.p.run_m < 3 ? 3 : 2;
   if (rule == 3) return tp.npass == 2 ? 3 : 2;
@@ -695,7 +816,6 @@ void Engine::launch_plan(const TilePlan &tp, const Diag &fork, bool first, const
     else if (!pre.identity())
       pre_mode = 1;
   }
-  const int vs = half_[0].prog.vs;
   const bool timed = time_sweeps_;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (timed) {
@@ -705,15 +825,15 @@ void Engine::launch_plan(const TilePlan &tp, const Diag &fork, bool first, const
   }
   if (tp.fused) {
     FusedSweepParams f = tp.f;
-    f.pre = to_dev(pre, vs, pre_mode != 0);
-    if (pre_mode == 1) f.pre_s = make_split(pre, vs, tp.pass0_regs);
+    f.pre = to_dev(pre, pre_mode != 0);
+    if (pre_mode == 1) f.pre_s = make_split(pre, tp.pass0_regs);
     f.src = src;
     f.dst = dst;
     const int grid = (int)std::min<uint64_t>(1ull << f.log2_ntiles, (uint64_t)num_sms_);
     check(launch_fused_sweep(f, c128_, pre_mode, grid, stream_, tp.multi_layer), "fused sweep launch");
   } else {
     TileSweepParams p = tp.p;
-    p.pre = to_dev(pre, vs, pre_mode != 0);
+    p.pre = to_dev(pre, pre_mode != 0);
     p.njobs = 1;
     p.src[0] = tp.gen ? nullptr : src;
     p.dst[0] = dst;
@@ -722,7 +842,7 @@ void Engine::launch_plan(const TilePlan &tp, const Diag &fork, bool first, const
     const uint64_t tiles = 1ull << p.log2_ntiles;
     const bool tma = sweep_kernel_ != 1 && pre_mode != 2;
     if (tma) {
-      if (pre_mode == 1) p.pre_s = make_split(pre, vs, reg_positions(p, 0, c128_));
+      if (pre_mode == 1) p.pre_s = make_split(pre, reg_positions(p, 0, c128_));
       const int grid = (int)std::min<uint64_t>(tiles, (uint64_t)num_sms_);
       const int stages = sweep_kernel_ == 2 ? 2 : sweep_kernel_ == 3 ? 3 : tma_stages(tp);
       check(launch_tile_sweep_tma(p, c128_, pre_mode, tp.npass, grid, stream_, stages),
@@ -759,7 +879,7 @@ const void *Engine::run_level(int half, int level, uint64_t child, const void *s
   return n ? dst : src;
 }
 
-static LazyLayer lazy_layer(const Sweep &sw, const Diag &pre, int vs) {
+static LazyLayer lazy_layer(const Sweep &sw, const Diag &pre) {
   LazyLayer ll;
   std::memset(&ll, 0, sizeof(ll));
   ll.k = (int)sw.gates.size();
@@ -768,8 +888,8 @@ static LazyLayer lazy_layer(const Sweep &sw, const Diag &pre, int vs) {
     ll.tmask |= 1u << sw.gates[t].bit;
     (sw.gates[t].kind == 1 ? ll.sxmask : ll.symask) |= 1u << sw.gates[t].bit;
   }
-  ll.pre = to_dev(pre, vs);
-  ll.post = to_dev(sw.post, vs, true);
+  ll.pre = to_dev(pre);
+  ll.post = to_dev(sw.post, true);
   return ll;
 }
 
@@ -801,18 +921,17 @@ void Engine::gather_leaf(int half, uint64_t child_last, const void *psi, const u
   HalfExec &he = half_[half];
   const int F = (int)he.prog.levels.size() - 1;
   const Level &lev = he.prog.levels[F];
-  const int vs = he.prog.vs;
   if (depth >= 1) {
     const size_t n = lev.sweeps.size();
     auto pre_of = [&](size_t s) {
       return s == 0 ? Diag::merge(he.prog.fork_diag(F, child_last), lev.sweeps[0].pre) : lev.sweeps[s].pre;
     };
-    const LazyLayer lld = lazy_layer(lev.sweeps[n - 1], pre_of(n - 1), vs);
+    const LazyLayer lld = lazy_layer(lev.sweeps[n - 1], pre_of(n - 1));
     if (depth == 1) {
       check(launch_gather_layer(psi, dS, nS, out_row, lld, c128_, stream_), "gather_layer launch");
       st_.kernel_launches++;
     } else {
-      const LazyLayer ll1 = lazy_layer(lev.sweeps[n - 2], pre_of(n - 2), vs);
+      const LazyLayer ll1 = lazy_layer(lev.sweeps[n - 2], pre_of(n - 2));
       const int64_t ncone = nS << lld.k;
       cone_idx_.reserve((size_t)ncone * 8);
       cone_val_.reserve((size_t)ncone * amp_);
@@ -828,7 +947,7 @@ void Engine::gather_leaf(int half, uint64_t child_last, const void *psi, const u
   }
   Diag pend;
   if (F >= 1 && lev.sweeps.empty()) pend = he.prog.fork_diag(F, child_last);
-  check(launch_gather(psi, dS, nS, out_row, to_dev(pend, vs), c128_, stream_), "gather launch");
+  check(launch_gather(psi, dS, nS, out_row, to_dev(pend), c128_, stream_), "gather launch");
   st_.kernel_launches++;
 }
 
@@ -988,8 +1107,8 @@ void Engine::evolve_range(uint64_t b0, uint64_t b1) {
   for (uint64_t s = b0; s < b1;) {
     uint64_t e = std::min(b1, (s / p2 + 1) * p2);
     e = std::min(e, s + chunk);
-    evolve_half(0, s, e, U_.ptr, d_Su_.as<uint64_t>(), nu);
-    evolve_half(1, s, e, L_.ptr, d_Sl_.as<uint64_t>(), nl);
+    evolve_half(0, s, e, U_.ptr, d_Sp_[0].as<uint64_t>(), nu);
+    evolve_half(1, s, e, L_.ptr, d_Sp_[1].as<uint64_t>(), nl);
     gemm(U_.ptr, L_.ptr, (int64_t)(e - s), nu, nl, A_acc_.as<double>());
     st_.branches_evolved += e - s;
     s = e;
@@ -1187,7 +1306,7 @@ void Engine::branch_state(int half, uint64_t b, void *out) {
   // gather every index of the leaf: the same executor, S = 0 .. 2^h - 1
   tmp_.reserve(n * 8);
   std::vector<uint64_t> all(n);
-  for (size_t i = 0; i < n; ++i) all[i] = i;
+  for (size_t i = 0; i < n; ++i) all[i] = he.prog.phys(i);  // canonical order out
   check(cudaMemcpyAsync(tmp_.ptr, all.data(), n * 8, cudaMemcpyHostToDevice, stream_), "upload S");
   DevBuf slice;
   slice.reserve(n * amp_);

@@ -125,6 +125,7 @@ class Engine {
   bool have_blocks_ = false;
   std::vector<uint64_t> Su_, Sl_;
   DevBuf d_Su_, d_Sl_;
+  DevBuf d_Sp_[2];  // the blocks in each half's physical bit order (gathers)
   DevBuf A_acc_;  // double2 [nu, nl]
   DevBuf A_tot_;  // reduced block (rank 0 with a communicator)
   bool reduced_ = false;
@@ -150,6 +151,7 @@ class Engine {
   void ensure_device();
   void check(cudaError_t e, const char *what);
   void compile_plans(HalfExec &he);
+  std::vector<int> choose_perm(const HalfExec &he) const;
   bool plan_fused(const HalfProgram &hp, const std::vector<Stage> &stages, const Diag &pre, TilePlan &tp);
   std::vector<TilePlan> level_launches(const HalfProgram &hp, const Level &lev, size_t n);
   std::vector<TilePlan> legacy_plans(const HalfProgram &hp, const Sweep &sw);

@@ -9,13 +9,17 @@
 namespace qsim {
 
 // Device form of a fused diagonal (program.h Diag):
-//   D(i) = scale * w^{(ph0 + popc(i&t1) + 2popc(i&t2) + 4(popc(i&zm) + popc(i&i>>1&hm)
-//          + popc(i&i>>vs&vm))) & 7} * [(i & pm) == pv]
+//   D(i) = scale * w^{(ph0 + popc(i&t1) + 2popc(i&t2) + 4(popc(i&zm)
+//          + sum_k popc(i & i>>czd[k] & czm[k]))) & 7} * [(i & pm) == pv]
+// czd / czm: the distinct CZ pair distances of the diagonal and their low-bit masks.
+constexpr int kMaxCz = 31;
 struct DiagDev {
-  uint32_t t1, t2, zm, hm, vm, pm, pv;
-  int32_t vs;
+  uint32_t t1, t2, zm, pm, pv;
   int32_t ph0;
   int32_t active;  // 0: identity, skip
+  int32_t ncz;
+  uint32_t czm[kMaxCz];
+  uint8_t czd[kMaxCz];
   double scale;
 };
 

@@ -29,14 +29,24 @@ void Diag::add_proj(int bit, int value) {
   pv = (pv & ~m) | v;
 }
 
+void Diag::add_cz(int b0, int b1) {
+  const int lo = std::min(b0, b1), d = std::abs(b0 - b1);
+  cz[d] ^= 1u << lo;  // CZ^2 = I
+}
+
+int Diag::phase(uint32_t i) const {
+  int ph = ph0 + __builtin_popcount(i & t1) + 2 * __builtin_popcount(i & t2) + 4 * __builtin_popcount(i & zm);
+  for (int d = 1; d < 32; ++d) ph += 4 * __builtin_popcount(i & (i >> d) & cz[d]);
+  return ph & 7;
+}
+
 Diag Diag::merge(const Diag &a, const Diag &b) {
   Diag d = a;
   for (int bit = 0; bit < 32; ++bit) {
     const int cb = b.count(bit);
     if (cb) d.set_count(bit, d.count(bit) + cb);
   }
-  d.hm ^= b.hm;  // CZ^2 = I
-  d.vm ^= b.vm;
+  for (int k = 0; k < 32; ++k) d.cz[k] ^= b.cz[k];  // CZ^2 = I
   const uint32_t overlap = a.pm & b.pm;
   if ((a.pv & overlap) != (b.pv & overlap)) d.allzero = true;
   d.pm = a.pm | b.pm;
@@ -186,13 +196,15 @@ struct LayerSpec {
 };
 }  // namespace
 
-HalfProgram compile_half(const Circuit &c, bool upper) {
+HalfProgram compile_half(const Circuit &c, bool upper, const std::vector<int> &perm) {
   HalfProgram hp;
   hp.upper = upper;
   hp.h = (int)(upper ? c.h_u : c.h_l);
-  hp.vs = (int)c.cols;
+  hp.perm = perm;
+  if (hp.perm.empty())
+    for (int b = 0; b < hp.h; ++b) hp.perm.push_back(b);
   const uint32_t lo = upper ? 0 : c.h_u, hi = upper ? c.h_u : c.n;
-  auto bit_of = [&](uint32_t q) { return hp.h - 1 - (int)(q - lo); };
+  auto bit_of = [&](uint32_t q) { return hp.perm[hp.h - 1 - (int)(q - lo)]; };
 
   std::vector<LayerSpec> layers(c.depth + 1);
   for (const qsim_gate &g : c.gates) {
@@ -200,12 +212,7 @@ HalfProgram compile_half(const Circuit &c, bool upper) {
     if (g.kind == QSIM_CZ) {
       const bool in0 = g.q0 >= lo && g.q0 < hi, in1 = g.q1 >= lo && g.q1 < hi;
       if (!(in0 && in1)) continue;  // cut CZ (handled as a fork) or the other half
-      const int b0 = bit_of(g.q0), b1 = bit_of(g.q1);
-      const int low = std::min(b0, b1), d = std::abs(b0 - b1);
-      if (d == 1 && (g.q0 / c.cols) == (g.q1 / c.cols))
-        L.diag.add_cz_h(low);
-      else
-        L.diag.add_cz_v(low);  // d == cols (validated grid edge)
+      L.diag.add_cz(bit_of(g.q0), bit_of(g.q1));
     } else {
       if (!(g.q0 >= lo && g.q0 < hi)) continue;
       const int b = bit_of(g.q0);

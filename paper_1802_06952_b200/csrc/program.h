@@ -20,30 +20,36 @@
 namespace qsim {
 
 // D(i) = 2^(-nhalf/2) * w^ph(i) * [(i & pm) == pv],  w = e^{i pi/4},
-// ph(i) = ph0 + popc(i&t1) + 2 popc(i&t2) + 4 (popc(i&zm) + popc(i & i>>1 & hm)
-//         + popc(i & i>>vs & vm))   (mod 8).
-// t1/t2/zm carry the per-bit T count mod 8 (T = w on |1>; Z = w^4), hm / vm
-// the horizontal / vertical CZ pairs (bit b with b+1 / b+vs; CZ = w^4 on |11>),
-// pm/pv the projector constraint (P0 / P1, Eq. 1), nhalf the 1/sqrt2 factors.
+// ph(i) = ph0 + popc(i&t1) + 2 popc(i&t2) + 4 (popc(i&zm) + sum_d popc(i & i>>d & cz[d]))  (mod 8).
+// t1/t2/zm carry the per-bit T count mod 8 (T = w on |1>; Z = w^4), cz[d] the CZ pairs
+// (bit b with bit b+d, mask bit at b; CZ = w^4 on |11>) — in the identity layout the
+// horizontal pairs sit at d = 1 and the vertical ones at d = cols, under a qubit relabelling
+// anywhere — pm/pv the projector constraint (P0 / P1, Eq. 1), nhalf the 1/sqrt2 factors.
 struct Diag {
-  uint32_t t1 = 0, t2 = 0, zm = 0, hm = 0, vm = 0, pm = 0, pv = 0;
+  uint32_t t1 = 0, t2 = 0, zm = 0, pm = 0, pv = 0;
+  uint32_t cz[32] = {};
   int ph0 = 0;
   int nhalf = 0;
   bool allzero = false;
 
+  bool has_cz() const {
+    for (uint32_t m : cz)
+      if (m) return true;
+    return false;
+  }
   bool identity() const {
-    return !allzero && !t1 && !t2 && !zm && !hm && !vm && !pm && ph0 == 0 && nhalf == 0;
+    return !allzero && !t1 && !t2 && !zm && !has_cz() && !pm && ph0 == 0 && nhalf == 0;
   }
   int count(int bit) const;          // T count (mod 8) at bit
   void set_count(int bit, int c);
   void add_T(int bit) { set_count(bit, count(bit) + 1); }
   void add_Z(int bit) { set_count(bit, count(bit) + 4); }
-  void add_cz_h(int lowbit) { hm ^= 1u << lowbit; }
-  void add_cz_v(int lowbit) { vm ^= 1u << lowbit; }
+  void add_cz(int b0, int b1);        // CZ between two distinct bits
   void add_proj(int bit, int value);  // P0 (value 0) or P1 (value 1)
   // the product of two diagonals (they commute)
   static Diag merge(const Diag &a, const Diag &b);
   double scale() const;  // 2^(-nhalf/2)
+  int phase(uint32_t i) const;  // ph(i) mod 8 (host reference of the device formula)
 };
 
 // One non-diagonal gate of a sweep after factoring out its global phase:
@@ -71,10 +77,17 @@ struct Level {
 struct HalfProgram {
   bool upper = true;
   int h = 0;
-  int vs = 0;  // vertical pair distance (= cols)
+  std::vector<int> perm;  // physical bit of canonical local bit c (h-1-k' for local qubit k')
   std::vector<Level> levels;
   // Diagonal of fork child c at level l (P_{bits} on the upper endpoints, Z^{bits} on the lower)
   Diag fork_diag(int level, uint64_t child) const;
+  // physical index of canonical half index x (bit c of x moves to bit perm[c])
+  uint64_t phys(uint64_t x) const {
+    uint64_t y = 0;
+    for (int c = 0; c < h; ++c)
+      if ((x >> c) & 1u) y |= 1ull << perm[c];
+    return y;
+  }
   size_t total_sweeps() const;
 };
 
@@ -92,6 +105,8 @@ std::string build_circuit(uint32_t rows, uint32_t cols, uint32_t depth, const qs
                           size_t n_gates, uint32_t cut_row, const uint32_t *cut_layers,
                           size_t n_cut_layers, Circuit &out);
 
-HalfProgram compile_half(const Circuit &c, bool upper);
+// perm: physical bit of each canonical local bit (identity when empty); every bit position of the
+// program (gates, diagonals, forks) is physical.
+HalfProgram compile_half(const Circuit &c, bool upper, const std::vector<int> &perm = {});
 
 }  // namespace qsim

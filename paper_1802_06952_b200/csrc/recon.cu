@@ -34,9 +34,7 @@ __global__ void gather_kernel(const typename CxT<R>::T *__restrict__ psi, const 
     C x = psi[i];
     if (d.active) {
       const uint32_t ii = (uint32_t)i;
-      const int ph = (d.ph0 + __popc(ii & d.t1) + 2 * __popc(ii & d.t2) +
-                      4 * (__popc(ii & d.zm) + __popc(ii & (ii >> 1) & d.hm) +
-                           __popc(ii & (ii >> d.vs) & d.vm))) & 7;
+      const int ph = diag_phase(ii, d, d.zm);
       const R wr = (R)(c_omega[2 * ph] * d.scale), wi = (R)(c_omega[2 * ph + 1] * d.scale);
       C y;
       y.x = x.x * wr - x.y * wi;

@@ -38,17 +38,27 @@ static __constant__ double c_omega[16] = {1.0,
                                           0.70710678118654752440,
                                           -0.70710678118654752440};
 
+// CZ pair term of the fused diagonal mod 2: parity of sum_k popc(i & i>>czd[k] & czm[k]).  The first
+// kCzFast distances use static parameter offsets (no dynamic indexing, no extra live registers).
+constexpr int kCzFast = 8;
+__device__ __forceinline__ int diag_cz(uint32_t i, const DiagDev &d) {
+  uint32_t x = 0;
+#pragma unroll
+  for (int k = 0; k < kCzFast; ++k)
+    if (k < d.ncz) x ^= i & (i >> d.czd[k]) & d.czm[k];
+  for (int k = kCzFast; k < d.ncz; ++k) x ^= i & (i >> d.czd[k]) & d.czm[k];
+  return __popc(x) & 1;
+}
+
 // full phase of the fused diagonal at index i (see DiagDev), zm passed separately
 __device__ __forceinline__ int diag_phase(uint32_t i, const DiagDev &d, uint32_t zm) {
-  const int ph = d.ph0 + __popc(i & d.t1) + 2 * __popc(i & d.t2) +
-                 4 * (__popc(i & zm) + __popc(i & (i >> 1) & d.hm) + __popc(i & (i >> d.vs) & d.vm));
+  const int ph = d.ph0 + __popc(i & d.t1) + 2 * __popc(i & d.t2) + 4 * (__popc(i & zm) + diag_cz(i, d));
   return ph & 7;
 }
 
 // the same without ph0 (the B part of the DiagSplit decomposition)
 __device__ __forceinline__ int diag_phase_b(uint32_t i, const DiagDev &d) {
-  return __popc(i & d.t1) + 2 * __popc(i & d.t2) +
-         4 * (__popc(i & d.zm) + __popc(i & (i >> 1) & d.hm) + __popc(i & (i >> d.vs) & d.vm));
+  return __popc(i & d.t1) + 2 * __popc(i & d.t2) + 4 * (__popc(i & d.zm) + diag_cz(i, d));
 }
 
 template <typename C>

@@ -55,13 +55,15 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
 // Fused diagonal through the DiagSplit decomposition (kernels.h).  The phase table
 // holds w^k * scale at byte offset 8k (float2) / 16k (double2); the cross terms of
 // register bits with their B-side CZ partners are a per-tile parity mask over the slots.
+// phB = diag_phase_b(B, d) & 7, evaluated by the caller before the tile's values are live
+// (the CZ term loops over pair distances; inside here it would spill)
 template <typename R, int NV>
-__device__ __forceinline__ void apply_split(typename Cx2<R>::T (&v)[16][NV], const uint32_t B, const DiagDev &d,
+__device__ __forceinline__ void apply_split(typename Cx2<R>::T (&v)[16][NV], const uint32_t B, const uint32_t phB,
                                             const DiagSplit &sp, const typename Cx2<R>::T *tab) {
   using C = typename Cx2<R>::T;
   constexpr int VB = NV == 2 ? 1 : 0;
   constexpr uint32_t pat[5] = {0xAAAAAAAAu, 0xCCCCCCCCu, 0xF0F0F0F0u, 0xFF00FF00u, 0xFFFF0000u};
-  const uint32_t pB8 = (uint32_t)(diag_phase_b(B, d) & 7) << 3;
+  const uint32_t pB8 = phB << 3;
   uint32_t cpm = 0;
 #pragma unroll
   for (int j = 0; j < VB + 4; ++j)
@@ -298,6 +300,19 @@ __global__ void __launch_bounds__(544, 1) tile_sweep_tma_kernel(const __grid_con
     // the group always uses stage grp (k-th use); with 3 its tiles cycle the stages
     // (2k + grp mod 3), so the k-th tile is the (k / 3)-th use of its stage
     const uint32_t use = NST == 2 ? (uint32_t)k : (uint32_t)(k / 3);
+    // B-phases of the pre (pass-0 thread base, bits 0-2) and post (last pass, bits 3-5) diagonals
+    uint32_t phB = 0;
+    {
+      uint32_t b0 = outer | ((uint32_t)lane << VB), b1 = b0;
+#pragma unroll
+      for (int j = 0; j < 3; ++j)
+        if ((wl >> j) & 1) {
+          b0 |= 1u << p.hb[p.wsel[0][j]];
+          b1 |= 1u << p.hb[p.wsel[NPASS - 1][j]];
+        }
+      if constexpr (PRE == 1) phB = (uint32_t)diag_phase_b(b0, p.pre) & 7u;
+      if (p.post.active) phB |= ((uint32_t)diag_phase_b(b1, p.post) & 7u) << 3;
+    }
     mbar_wait(&full_bar[s][grp], use & 1u);
 
     // pass 0: shared -> registers
@@ -310,7 +325,7 @@ __global__ void __launch_bounds__(544, 1) tile_sweep_tma_kernel(const __grid_con
       }
 #pragma unroll
     for (int r = 0; r < 16; ++r) unpack<R, NV>(tile[slot_smem(ts, p.gsel[0], r)], v[r]);
-    if constexpr (PRE == 1) apply_split<R, NV>(v, tg, p.pre, p.pre_s, tab_pre);
+    if constexpr (PRE == 1) apply_split<R, NV>(v, tg, phB & 7u, p.pre_s, tab_pre);
     low_gates<R, NV>(v, p, lane);
     reg_gates<R, NV>(v, p.gkind[0]);
 
@@ -336,7 +351,7 @@ __global__ void __launch_bounds__(544, 1) tile_sweep_tma_kernel(const __grid_con
     if constexpr (NPASS == 2) reg_gates<R, NV>(v, p.gkind[1]);
 
     constexpr int QL = NPASS - 1;
-    if (p.post.active) apply_split<R, NV>(v, tg, p.post, p.post_s, tab_post);
+    if (p.post.active) apply_split<R, NV>(v, tg, phB >> 3, p.post_s, tab_post);
     V *d0 = dst + (tg >> VB);
 #pragma unroll
     for (int r = 0; r < 16; ++r) {

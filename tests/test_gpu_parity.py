@@ -156,6 +156,39 @@ def test_fused_sweeps_c3_branch(prec, branch, c3_circuit):
         assert_close(got, ref, prec, f"C3 fused={fuse}")
 
 
+@pytest.fixture
+def perm_mode(request, monkeypatch):
+    """Forces the qubit-to-bit relabelling of tree halves (engine.cu choose_perm) for one test."""
+    monkeypatch.setenv("QSIM_PERM", request.param)
+    return request.param
+
+
+@pytest.mark.parametrize("prec", PRECS, ids=PNAME.get)
+@pytest.mark.parametrize("perm_mode", ["id", "rev", "rand", "auto"], indirect=True)
+def test_tree_mode_h14_relabelled(prec, perm_mode, h14_reference):
+    """Every relabelling of the half qubits to physical bits gives the same amplitudes
+    (gates, fused diagonals with CZ pairs at any distance, forks, lazy tail, gathers)."""
+    circ, Su, Sl, ref = h14_reference
+    for lazy in (0, 2):
+        assert_close(run_block(circ, Su, Sl, prec, opts={Q.QSIM_OPT_LAZY_LAST: lazy}), ref, prec,
+                     f"h14 perm={perm_mode} lazy={lazy}")
+
+
+@pytest.mark.parametrize("prec", PRECS, ids=PNAME.get)
+@pytest.mark.parametrize("perm_mode", ["rev", "rand"], indirect=True)
+def test_c3_branch_state_relabelled(prec, perm_mode, c3_circuit):
+    """qsim_branch_state returns the leaf in canonical bit order under any relabelling."""
+    circ = c3_circuit
+    for half, branch in ((0, 9000), (1, 5)):
+        ctx = Q.qsim_create(prec, 0)
+        try:
+            Q.qsim_load_circuit(ctx, 6, 7, 22, circ.gate_array())
+            got = Q.qsim_branch_state(ctx, half, branch, 21, prec)
+        finally:
+            Q.qsim_destroy(ctx)
+        assert_close(got, OP.branch_state(circ, half, branch), prec, f"C3 perm={perm_mode} half {half}")
+
+
 @pytest.mark.parametrize("prec", PRECS, ids=PNAME.get)
 def test_tree_recompute_path_and_ranges(prec, h14_reference):
     """Memory budget of 2 states forces path recomputation; split ranges accumulate."""

@@ -1,6 +1,6 @@
 """Micro-benchmark of single-layer tile sweeps by target placement (one branch, no cut).
 
-Builds an 8x7 grid circuit whose upper half (h = 28) repeats one layer of SX gates on chosen
+Run with QSIM_PERM=id so the layout is the one described.  Builds an 8x7 grid circuit whose upper half (h = 28) repeats one layer of SX gates on chosen
 qubits, evolves it with sweep timing on, and prints GB/s per case.  Local bit of qubit k is
 27 - k: qubits 27 (vector bit, c64), 26..24 (lane bits 0-2), 23, 22 (vector bits 3, 4) and
 21..0 (hi bits).
@@ -36,6 +36,10 @@ CASES = {
     "hi4hi": [3, 2, 1, 0],                   # bits 24..27, m = 3
     "hi6lo": [20, 19, 18, 17, 16, 15],       # m = 1
     "hi6hi": [5, 4, 3, 2, 1, 0],             # m = 1
+    # lane-bit (shuffle) targets on top of 4 hi targets: qubits 25, 24, 23 = bits 2, 3, 4
+    "hi4+l1": [0, 5, 10, 15, 25],
+    "hi4+l2": [0, 5, 10, 15, 25, 24],
+    "hi4+l3": [0, 5, 10, 15, 25, 24, 23],
 }
 
 
