@@ -90,8 +90,15 @@ typedef enum {
   QSIM_OPT_LAZY_LAST = 5     /* lazy tail of each leaf, evaluated only at the sampled indices during the
                                 gather instead of full 2^h passes: 0 off, 1 the last sweep, 2 (default)
                                 the last one or two by a cost model, 3 always two when possible      */,
-  QSIM_OPT_FUSE_LAYERS = 6   /* 1: consecutive layers whose high targets fit one tile share one HBM
+  QSIM_OPT_FUSE_LAYERS = 6,  /* 1: consecutive layers whose high targets fit one tile share one HBM
                                 pass (up to 3 register passes per tile); 0 (default): one layer per pass */
+  QSIM_OPT_DISTRIBUTE = 7    /* 1: distributed half (§2.3.3): every half state
+                                is sharded over the ranks of qsim_comm_init (1, 2 or 4, by its top
+                                physical bits); every rank runs every branch on its shard; a gate on a
+                                global qubit is preceded by a local/global qubit swap fused into the
+                                previous sweep (its tiles are stored straight into the peer's HBM over
+                                NVLink); sampled slices are summed over the ranks before the GEMM.
+                                Needs >= tile bits + 2 qubits per shard; lazy tail off. 0: default */
 } qsim_option;
 
 /* Create a context bound to CUDA device `device` (no device call is made until the

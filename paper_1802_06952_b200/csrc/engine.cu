@@ -131,6 +131,7 @@ Engine::~Engine() {
       cudaEventDestroy(pr.second);
     }
     for (auto e : ev_pool_) cudaEventDestroy(e);
+    for (void *p : ipc_opened_) cudaIpcCloseMemHandle(p);
     for (auto *b : states_) delete b;
     states_.clear();
     if (comm_) ncclCommDestroy(comm_);
@@ -199,6 +200,12 @@ void Engine::set_option(int key, int64_t value) {
       if (have_circuit_)
         for (int h = 0; h < 2; ++h) compile_plans(half_[h]);
       return;
+    case QSIM_OPT_DISTRIBUTE:
+      if (value < 0 || value > 1) throw Error(QSIM_EINVAL, "QSIM_OPT_DISTRIBUTE must be 0 or 1");
+      dist_ = value != 0;
+      if (have_circuit_) compile_all();
+      have_blocks_ = false;  // the sampled indices are relabelled per layout
+      return;
     case QSIM_OPT_SWEEP_KERNEL:
       if (value < 0 || value > 3) throw Error(QSIM_EINVAL, "QSIM_OPT_SWEEP_KERNEL must be 0, 1, 2 or 3");
       sweep_kernel_ = (int)value;
@@ -222,11 +229,28 @@ void Engine::load_circuit(uint32_t rows, uint32_t cols, uint32_t depth, const qs
   std::string err = build_circuit(rows, cols, depth, gates, n_gates, cut_row, cut_layers, n_cut_layers, c);
   if (!err.empty()) throw Error(QSIM_EINVAL, err);
   circ_ = std::move(c);
+  compile_all();
+  have_circuit_ = true;
+  have_blocks_ = false;
+  reduced_ = false;
+}
+
+void Engine::compile_all() {
+  if (dist_) {
+    if (world_ & (world_ - 1) || world_ > 4)
+      throw Error(QSIM_EINVAL, "distributed halves need 1, 2 or 4 ranks (qsim_comm_init)");
+    gbits_ = world_ == 4 ? 2 : world_ == 2 ? 1 : 0;
+  } else {
+    gbits_ = 0;
+  }
   for (int h = 0; h < 2; ++h) {
     half_[h].prog = compile_half(circ_, h == 0);
     half_[h].uploaded = false;
     compile_plans(half_[h]);
-    if (half_[h].tree) {  // relabel qubits to physical bits for long tile runs (choose_perm)
+    if (dist_) {
+      plan_distributed(half_[h]);
+      compile_plans(half_[h]);
+    } else if (half_[h].tree) {  // relabel qubits to physical bits for long tile runs (choose_perm)
       const std::vector<int> perm = choose_perm(half_[h]);
       bool ident = true;
       for (size_t b = 0; b < perm.size(); ++b) ident = ident && perm[b] == (int)b;
@@ -236,9 +260,6 @@ void Engine::load_circuit(uint32_t rows, uint32_t cols, uint32_t depth, const qs
       }
     }
   }
-  have_circuit_ = true;
-  have_blocks_ = false;
-  reduced_ = false;
 }
 
 void Engine::partition(uint32_t *n_cuts, uint64_t *n_branches, qsim_cut *cuts) const {
@@ -279,7 +300,7 @@ bool Engine::plan_fused(const HalfProgram &hp, const std::vector<Stage> &stages,
     for (auto &g : st.gates)
       if (g.bit >= L && std::find(hb.begin(), hb.end(), (int)g.bit) == hb.end()) hb.push_back(g.bit);
   if ((int)hb.size() > kHiBits) return false;
-  for (int b = L; (int)hb.size() < kHiBits && b < hp.h; ++b)
+  for (int b = L; (int)hb.size() < kHiBits && b < hp.hl; ++b)
     if (std::find(hb.begin(), hb.end(), b) == hb.end()) hb.push_back(b);
   std::sort(hb.begin(), hb.end());
   auto idx_of = [&](int bit) { return (int)(std::find(hb.begin(), hb.end(), bit) - hb.begin()); };
@@ -371,8 +392,8 @@ bool Engine::plan_fused(const HalfProgram &hp, const std::vector<Stage> &stages,
     f.diag[d] = to_dev(diags[d], true);
     f.diag_s[d] = make_split(diags[d], regpos(diag_pass[d]));
   }
-  outer_runs(hb, L, hp.h, f.run_start, f.run_len, &f.nruns);
-  f.log2_ntiles = hp.h - T;
+  outer_runs(hb, L, hp.hl, f.run_start, f.run_len, &f.nruns);
+  f.log2_ntiles = hp.hl - T;
   int m = 0;
   while (m < kHiBits && hb[m] == L + m) ++m;
   f.run_m = m;
@@ -406,7 +427,7 @@ std::vector<TilePlan> Engine::level_launches(const HalfProgram &hp, const Level 
       out.insert(out.end(), v.begin(), v.end());
       ++s;
     };
-    if (sweep_kernel_ == 1 || sw.gen || !fuse_layers_ || nhi(sw) > kHiBits) {
+    if (sweep_kernel_ == 1 || sw.gen || !fuse_layers_ || dist_ || nhi(sw) > kHiBits) {
       single();
       continue;
     }
@@ -440,13 +461,13 @@ std::vector<TilePlan> Engine::level_launches(const HalfProgram &hp, const Level 
 void Engine::compile_plans(HalfExec &he) {
   const HalfProgram &hp = he.prog;
   const int L = tile_low_bits(c128_), T = L + kHiBits;
-  const bool can_tree = hp.h >= T, can_small = hp.h <= small_max_h(c128_);
+  const bool can_tree = hp.hl >= T, can_small = hp.h <= small_max_h(c128_) && !dist_;
   if (mode_ == 1)
     he.tree = false;
   else if (mode_ == 2)
     he.tree = true;
   else
-    he.tree = !can_small;
+    he.tree = !can_small || dist_;
   he.plans.clear();
   if ((he.tree && !can_tree) || (!he.tree && !can_small)) return;  // reported at evolve time
   if (!he.tree) return;
@@ -570,6 +591,147 @@ std::vector<int> Engine::choose_perm(const HalfExec &he) const {
   return best;
 }
 
+// Layout schedule of a distributed half (§2.3.3).  Physical bits
+// hl .. h-1 are global (the rank); a sweep can only target local bits.  Walking the sweeps in
+// tree order (every node of a level runs the same sweeps, so the layout sequence is linear),
+// a sweep with a target on a global bit gets it swapped, at the output of the previous sweep,
+// with a local bit that is not in that sweep's tile (an outer bit of its tiles) and not a target
+// of either sweep; the evicted qubit is the one needed again the latest (Belady).  The initial
+// layout puts on the global bits qubits not targeted by the first two sweeps.  Every layer is
+// then compiled in the layout of the sweep that applies it.
+void Engine::plan_distributed(HalfExec &he) {
+  const HalfProgram id = he.prog;  // canonical layout: gate bit == canonical bit
+  const int h = id.h, g = gbits_, hl = h - g, L = tile_low_bits(c128_), T = L + kHiBits;
+  if (hl < T + 2) {
+    std::ostringstream m;
+    m << "distributed half: a " << h << "-qubit half over " << (1 << g) << " ranks leaves " << hl
+      << " local qubits; need >= " << T + 2;
+    throw Error(QSIM_EINVAL, m.str());
+  }
+  struct SQ {
+    int level, idx;
+    std::vector<int> tq;
+    bool gen;
+    int first, last;
+  };
+  std::vector<SQ> seq;
+  for (size_t l = 0; l < id.levels.size(); ++l)
+    for (size_t i = 0; i < id.levels[l].sweeps.size(); ++i) {
+      const Sweep &sw = id.levels[l].sweeps[i];
+      SQ x{(int)l, (int)i, {}, sw.gen, sw.first_layer, sw.last_layer};
+      for (auto &gt : sw.gates) x.tq.push_back(gt.bit);
+      seq.push_back(x);
+    }
+  const size_t n = seq.size();
+  auto is_target = [&](size_t s, int q) { return std::find(seq[s].tq.begin(), seq[s].tq.end(), q) != seq[s].tq.end(); };
+  auto next_use = [&](int q, size_t from) {
+    for (size_t s = from; s < n; ++s)
+      if (is_target(s, q)) return s;
+    return n + 1;
+  };
+  std::vector<int> cur(h), at(h);  // canonical bit -> position, position -> canonical bit
+  for (int b = 0; b < h; ++b) cur[b] = at[b] = b;
+  auto put = [&](int q, int pos) {  // exchange the positions of qubit q and the qubit at pos
+    const int o = at[pos], pq = cur[q];
+    cur[q] = pos;
+    at[pos] = q;
+    cur[o] = pq;
+    at[pq] = o;
+  };
+  // initial global qubits: not targeted by the first two sweeps, latest first use
+  {
+    std::vector<int> cand;
+    for (int q = 0; q < h; ++q)
+      if (!(n > 0 && is_target(0, q)) && !(n > 1 && is_target(1, q))) cand.push_back(q);
+    // QSIM_DIST_STRESS (tests): the earliest-needed qubits instead, so that swaps happen early
+    const bool stress = std::getenv("QSIM_DIST_STRESS") != nullptr;
+    std::stable_sort(cand.begin(), cand.end(), [&](int a, int b) {
+      return stress ? next_use(a, 0) < next_use(b, 0) : next_use(a, 0) > next_use(b, 0);
+    });
+    if ((int)cand.size() < g) throw Error(QSIM_EINVAL, "distributed half: no global qubit placement");
+    for (int j = 0; j < g; ++j) put(cand[j], hl + j);
+  }
+  std::vector<std::vector<int>> sperm(n);
+  std::vector<std::vector<std::pair<int, int>>> sswap(n);
+  for (size_t s = 0; s < n; ++s) {
+    std::vector<int> need;
+    for (int q : seq[s].tq)
+      if (cur[q] >= hl) need.push_back(q);
+    if (!need.empty()) {
+      if (s == 0 || seq[s - 1].gen) throw Error(QSIM_EINVAL, "distributed half: swap after the generated sweep");
+      const size_t pv = s - 1;
+      // bits of the previous sweep's tiles: its hi targets and (a superset of) their padding,
+      // the lowest free bits >= L; the swapped bit must be an outer bit of those tiles
+      std::vector<int> tile;
+      for (int q : seq[pv].tq)
+        if (cur[q] >= L) tile.push_back(cur[q]);
+      for (int pos = L, pad = 0; pos < hl && pad < kHiBits; ++pos)
+        if (std::find(tile.begin(), tile.end(), pos) == tile.end()) {
+          tile.push_back(pos);
+          ++pad;
+        }
+      std::vector<int> used;
+      for (int q : need) {
+        const int G = cur[q];
+        int best = -1;
+        size_t bu = 0;
+        for (int pos = L; pos < hl; ++pos) {
+          const int v = at[pos];
+          if (is_target(pv, v) || is_target(s, v)) continue;
+          if (std::find(tile.begin(), tile.end(), pos) != tile.end()) continue;
+          if (std::find(used.begin(), used.end(), pos) != used.end()) continue;
+          const size_t u = next_use(v, s);
+          if (best < 0 || u > bu) {
+            best = pos;
+            bu = u;
+          }
+        }
+        if (best < 0) throw Error(QSIM_EINVAL, "distributed half: no local qubit to swap out");
+        sswap[pv].push_back({best, G - hl});
+        used.push_back(best);
+        put(q, best);  // q becomes local at `best`, the evicted qubit global at G
+      }
+    }
+    sperm[s] = cur;
+  }
+  // layouts per layer: the sweep that applies the layer (pending diagonals: the level's first)
+  std::vector<std::vector<int>> layer_perm(circ_.depth + 2, sperm.empty() ? cur : sperm[0]);
+  for (size_t l = 0; l < id.levels.size(); ++l) {
+    const int first = (l == 0) ? 1 : id.levels[l].fork_layer + 1;
+    const int last = (l + 1 < id.levels.size()) ? id.levels[l + 1].fork_layer : (int)circ_.depth;
+    size_t s0 = n;
+    for (size_t s = 0; s < n; ++s)
+      if (seq[s].level == (int)l) {
+        s0 = s;
+        break;
+      }
+    for (int t = first; t <= last; ++t) {
+      size_t sw = s0;
+      for (size_t s = s0; s < n && seq[s].level == (int)l; ++s)
+        if (seq[s].first <= t && t <= seq[s].last) sw = s;
+      if (sw < n) layer_perm[t] = sperm[sw];
+    }
+    if (first <= (int)circ_.depth + 1 && s0 < n) layer_perm[first] = sperm[s0];
+  }
+  layer_perm[circ_.depth + 1] = cur;
+  HalfProgram hp = compile_half_layers(circ_, id.upper, layer_perm, cur);
+  hp.hl = hl;
+  if (std::getenv("QSIM_DEBUG_PLANS")) {
+    std::fprintf(stderr, "%s distributed h=%d hl=%d:", id.upper ? "U" : "D", h, hl);
+    for (size_t k = 0; k < n; ++k)
+      if (!sswap[k].empty()) std::fprintf(stderr, " L%d.%d x%zu", seq[k].level, seq[k].idx, sswap[k].size());
+    std::fprintf(stderr, " (%zu sweeps)\n", n);
+  }
+  size_t s = 0;
+  for (auto &lev : hp.levels)
+    for (auto &sw : lev.sweeps) {
+      sw.swaps = sswap[s++];
+      for (auto &gt : sw.gates)
+        if (gt.bit >= hl) throw Error(QSIM_EINVAL, "distributed half: a target left on a global bit");
+    }
+  he.prog = hp;
+}
+
 // Legacy per-sweep plans (register-only kernel; the generated root sweep).
 std::vector<TilePlan> Engine::legacy_plans(const HalfProgram &hp, const Sweep &sw) {
   std::vector<TilePlan> out;
@@ -587,7 +749,7 @@ std::vector<TilePlan> Engine::legacy_plans(const HalfProgram &hp, const Sweep &s
         const auto &H = chunks[ci];
         std::vector<int> hb;
         for (auto &g : H) hb.push_back(g.bit);
-        for (int b = L; (int)hb.size() < kHiBits && b < hp.h; ++b)
+        for (int b = L; (int)hb.size() < kHiBits && b < hp.hl; ++b)
           if (std::find(hb.begin(), hb.end(), b) == hb.end()) hb.push_back(b);
         std::sort(hb.begin(), hb.end());
         auto idx_of = [&](int bit) { return (int)(std::find(hb.begin(), hb.end(), bit) - hb.begin()); };
@@ -633,22 +795,23 @@ std::vector<TilePlan> Engine::legacy_plans(const HalfProgram &hp, const Sweep &s
         }
         // outer runs
         int nr = 0;
-        for (int b = L; b < hp.h;) {
+        for (int b = L; b < hp.hl;) {
           if (std::find(hb.begin(), hb.end(), b) != hb.end()) {
             ++b;
             continue;
           }
           int e = b;
-          while (e < hp.h && std::find(hb.begin(), hb.end(), e) == hb.end()) ++e;
+          while (e < hp.hl && std::find(hb.begin(), hb.end(), e) == hb.end()) ++e;
           tp.p.run_start[nr] = (uint8_t)b;
           tp.p.run_len[nr] = (uint8_t)(e - b);
           ++nr;
           b = e;
         }
         tp.p.nruns = nr;
-        tp.p.log2_ntiles = hp.h - T;
+        tp.p.log2_ntiles = hp.hl - T;
         tp.fused = false;
         tp.layers = ci == nchunks - 1 ? 1 : 0;
+        if (ci == nchunks - 1) tp.swaps = sw.swaps;
         tp.use_pre = ci == 0;
         tp.gen = sw.gen && ci == 0;
         tp.pre = sw.pre;
@@ -806,7 +969,8 @@ int Engine::tma_stages(const TilePlan &tp) const {
 }
 
 void Engine::launch_plan(const TilePlan &tp, const Diag &fork, bool first, const void *src, void *dst,
-                         int h) {
+                         const HalfProgram &hp, int out_buf) {
+  const int h = hp.hl;
   int pre_mode = 0;
   Diag pre;
   if (tp.use_pre) {
@@ -835,12 +999,25 @@ void Engine::launch_plan(const TilePlan &tp, const Diag &fork, bool first, const
     TileSweepParams p = tp.p;
     p.pre = to_dev(pre, pre_mode != 0);
     p.njobs = 1;
+    if (dist_) {
+      p.gbase = (uint32_t)rank_ << hp.hl;
+      p.rank = (uint32_t)rank_;
+      if (!tp.swaps.empty()) {  // fused local/global swap: destination buffers of the ranks
+        if (out_buf < 0 || tp.swaps.size() > 2) throw Error(QSIM_EINVAL, "distributed swap plan");
+        p.nswap = (int)tp.swaps.size();
+        for (size_t j = 0; j < tp.swaps.size(); ++j) {
+          p.swap_l[j] = (uint8_t)tp.swaps[j].first;
+          p.swap_j[j] = (uint8_t)tp.swaps[j].second;
+        }
+        for (int d = 0; d < (1 << gbits_); ++d) p.peer[d] = peer_[out_buf][rank_ ^ d];
+      }
+    }
     p.src[0] = tp.gen ? nullptr : src;
     p.dst[0] = dst;
     p.job_pv[0] = p.pre.pv;
     p.job_zm[0] = p.pre.zm;
     const uint64_t tiles = 1ull << p.log2_ntiles;
-    const bool tma = sweep_kernel_ != 1 && pre_mode != 2;
+    const bool tma = (sweep_kernel_ != 1 || p.nswap) && pre_mode != 2;
     if (tma) {
       if (pre_mode == 1) p.pre_s = make_split(pre, reg_positions(p, 0, c128_));
       const int grid = (int)std::min<uint64_t>(tiles, (uint64_t)num_sms_);
@@ -869,14 +1046,31 @@ void Engine::launch_plan(const TilePlan &tp, const Diag &fork, bool first, const
 // (the lazily evaluated tail); returns where the state ended (src when no sweep ran).
 const void *Engine::run_level(int half, int level, uint64_t child, const void *src, void *dst, int skip) {
   HalfExec &he = half_[half];
-  const Level &lev = he.prog.levels[level];
   const Diag fork = he.prog.fork_diag(level, child);
-  (void)lev;
   const auto &launches = he.plans[level][std::min<size_t>((size_t)skip, he.plans[level].size() - 1)];
   const size_t n = launches.size();
-  for (size_t i = 0; i < n; ++i)
-    launch_plan(launches[i], i == 0 ? fork : Diag(), i == 0, i == 0 ? src : dst, dst, he.prog.h);
-  return n ? dst : src;
+  if (!dist_) {
+    for (size_t i = 0; i < n; ++i)
+      launch_plan(launches[i], i == 0 ? fork : Diag(), i == 0, i == 0 ? src : dst, dst, he.prog);
+    return n ? dst : src;
+  }
+  // distributed half: level buffers 2l, 2l+1 (dst is buffer 2l).  A sweep that swaps local and
+  // global qubits stores into peers' buffers, so it runs out of place into the level's other
+  // buffer, between two barriers (no rank may still read what a peer overwrites).
+  int cur = 2 * level;
+  const void *in = src;
+  for (size_t i = 0; i < n; ++i) {
+    const TilePlan &tp = launches[i];
+    int out = (i == 0) ? 2 * level : cur;
+    if (!tp.swaps.empty() && i > 0) out = cur ^ 1;
+    if (!tp.swaps.empty()) dist_barrier();
+    launch_plan(tp, i == 0 ? fork : Diag(), i == 0, i == 0 ? in : states_[cur]->ptr, states_[out]->ptr, he.prog,
+                out);
+    if (!tp.swaps.empty()) dist_barrier();
+    cur = out;
+  }
+  (void)dst;
+  return n ? states_[cur]->ptr : src;
 }
 
 static LazyLayer lazy_layer(const Sweep &sw, const Diag &pre) {
@@ -900,7 +1094,7 @@ static LazyLayer lazy_layer(const Sweep &sw, const Diag &pre) {
 int Engine::lazy_depth(int half, int64_t nS) const {
   const HalfProgram &hp = half_[half].prog;
   const int F = (int)hp.levels.size() - 1;
-  if (full_leaf_ || F < 1 || lazy_depth_ < 1) return 0;
+  if (full_leaf_ || F < 1 || lazy_depth_ < 1 || dist_) return 0;
   const auto &sw = hp.levels[F].sweeps;
   if (sw.empty() || sw.back().gates.size() > 12) return 0;
   if (lazy_depth_ < 2 || sw.size() < 2) return 1;
@@ -947,7 +1141,9 @@ void Engine::gather_leaf(int half, uint64_t child_last, const void *psi, const u
   }
   Diag pend;
   if (F >= 1 && lev.sweeps.empty()) pend = he.prog.fork_diag(F, child_last);
-  check(launch_gather(psi, dS, nS, out_row, to_dev(pend), c128_, stream_), "gather launch");
+  const uint64_t lmask = dist_ ? (1ull << he.prog.hl) - 1ull : ~0ull;
+  const uint64_t gsel = dist_ ? (uint64_t)rank_ << he.prog.hl : 0ull;
+  check(launch_gather(psi, dS, nS, out_row, to_dev(pend), c128_, stream_, lmask, gsel), "gather launch");
   st_.kernel_launches++;
 }
 
@@ -1004,8 +1200,14 @@ void Engine::evolve_half(int half, uint64_t b0, uint64_t b1, void *slice, const 
     return;
   }
   const int T = tile_low_bits(c128_) + kHiBits;
-  if (hp.h < T) throw Error(QSIM_EINVAL, "tree mode needs h >= tile bits");
-  state_bytes_ = ((size_t)1 << hp.h) * amp_;
+  if (hp.hl < T) throw Error(QSIM_EINVAL, "tree mode needs h >= tile bits");
+  if (dist_) {
+    // shards of both halves share 2 buffers per level (sized for the larger half)
+    const int hmax = std::max(half_[0].prog.hl, half_[1].prog.hl);
+    const int nlev = (int)std::max(half_[0].prog.levels.size(), half_[1].prog.levels.size());
+    dist_buffers(((size_t)1 << hmax) * amp_, 2 * nlev);
+  }
+  state_bytes_ = ((size_t)1 << hp.hl) * amp_;
   size_t free_b = 0, total_b = 0;
   check(cudaMemGetInfo(&free_b, &total_b), "cudaMemGetInfo");
   size_t have = 0;
@@ -1013,12 +1215,12 @@ void Engine::evolve_half(int half, uint64_t b0, uint64_t b1, void *slice, const 
   const size_t margin = (size_t)512 << 20;
   const size_t avail = free_b + have > margin ? free_b + have - margin : 0;
   int nbuf = 0;
-  const int m0 = materialized_from(half, avail, &nbuf);
-  ensure_states(half, nbuf);
+  const int m0 = dist_ ? 0 : materialized_from(half, avail, &nbuf);
+  if (!dist_) ensure_states(half, nbuf);
   const int F = (int)hp.levels.size() - 1;
   std::vector<int> sbits(F + 1, 0);  // cut bits consumed up to and including level l
   for (int l = 1; l <= F; ++l) sbits[l] = sbits[l - 1] + hp.levels[l].k;
-  auto buf = [&](int l) { return states_[std::max(l, m0) - m0]->ptr; };
+  auto buf = [&](int l) { return dist_ ? states_[2 * l]->ptr : states_[std::max(l, m0) - m0]->ptr; };
   // lazy tail: the leaf level's last `lazy` sweeps are evaluated at the sampled indices
   const int lazy = lazy_depth(half, nS);
   auto skip = [&](int l) { return l == F ? lazy : 0; };
@@ -1109,6 +1311,15 @@ void Engine::evolve_range(uint64_t b0, uint64_t b1) {
     e = std::min(e, s + chunk);
     evolve_half(0, s, e, U_.ptr, d_Sp_[0].as<uint64_t>(), nu);
     evolve_half(1, s, e, L_.ptr, d_Sp_[1].as<uint64_t>(), nl);
+    if (dist_ && world_ > 1) {
+      // §2.3.3: each rank gathered the sampled entries it owns (zeros elsewhere).  The lower
+      // slices are summed on every rank; the upper ones stay partial, so the GEMM gives this
+      // rank's rows of A, and the final block reduction adds the ranks' rows.
+      ensure_comm();
+      const size_t cnt = (size_t)(e - s) * (size_t)nl * 2;
+      ncclResult_t r = ncclAllReduce(L_.ptr, L_.ptr, cnt, c128_ ? ncclDouble : ncclFloat, ncclSum, comm_, stream_);
+      if (r != ncclSuccess) throw Error(QSIM_ENCCL, std::string("ncclAllReduce: ") + ncclGetErrorString(r));
+    }
     gemm(U_.ptr, L_.ptr, (int64_t)(e - s), nu, nl, A_acc_.as<double>());
     st_.branches_evolved += e - s;
     s = e;
@@ -1318,8 +1529,72 @@ void Engine::branch_state(int half, uint64_t b, void *out) {
     throw;
   }
   full_leaf_ = false;
+  if (dist_ && world_ > 1) {  // every rank gathered its shard's entries: sum them
+    ensure_comm();
+    ncclResult_t r = ncclAllReduce(slice.ptr, slice.ptr, n * 2, c128_ ? ncclDouble : ncclFloat, ncclSum, comm_,
+                                   stream_);
+    if (r != ncclSuccess) throw Error(QSIM_ENCCL, std::string("ncclAllReduce: ") + ncclGetErrorString(r));
+  }
   check(cudaMemcpyAsync(out, slice.ptr, n * amp_, cudaMemcpyDeviceToHost, stream_), "D2H state");
   check(cudaStreamSynchronize(stream_), "branch_state");
+}
+
+// ---------------------------------------------------------------- distributed half (f3)
+// Level buffers for sharded half states, and every rank's device pointers to them (CUDA IPC
+// handles exchanged with an NCCL all-gather), for the sweeps that store into a peer's shard.
+void Engine::dist_buffers(size_t bytes, int nbuf) {
+  if (dist_bytes_ >= bytes && (int)peer_.size() >= nbuf && (int)peer_[0].size() == world_) return;
+  for (void *p : ipc_opened_) cudaIpcCloseMemHandle(p);
+  ipc_opened_.clear();
+  peer_.clear();
+  size_t free_b = 0, total_b = 0;
+  check(cudaMemGetInfo(&free_b, &total_b), "cudaMemGetInfo");
+  size_t have = 0;
+  for (auto *b : states_) have += b->bytes;
+  const size_t margin = (size_t)512 << 20;
+  if ((size_t)nbuf * bytes + margin > free_b + have) {
+    std::ostringstream m;
+    m << "distributed half: " << nbuf << " shard buffers of " << bytes << " bytes do not fit";
+    throw Error(QSIM_ENOMEM, m.str());
+  }
+  while ((int)states_.size() < nbuf) states_.push_back(new DevBuf());
+  for (int i = 0; i < nbuf; ++i) states_[i]->reserve(bytes);
+  dist_bytes_ = bytes;
+  peer_.assign(nbuf, std::vector<void *>(world_, nullptr));
+  for (int i = 0; i < nbuf; ++i) peer_[i][rank_] = states_[i]->ptr;
+  if (world_ == 1) return;
+  ensure_comm();
+  const size_t hb = sizeof(cudaIpcMemHandle_t);
+  std::vector<cudaIpcMemHandle_t> mine(nbuf), all((size_t)nbuf * world_);
+  for (int i = 0; i < nbuf; ++i) check(cudaIpcGetMemHandle(&mine[i], states_[i]->ptr), "cudaIpcGetMemHandle");
+  DevBuf dev;
+  dev.reserve(hb * nbuf * (world_ + 1));
+  char *send = dev.as<char>() + hb * nbuf * world_;
+  check(cudaMemcpyAsync(send, mine.data(), hb * nbuf, cudaMemcpyHostToDevice, stream_), "upload IPC handles");
+  ncclResult_t r = ncclAllGather(send, dev.ptr, hb * nbuf, ncclUint8, comm_, stream_);
+  if (r != ncclSuccess) throw Error(QSIM_ENCCL, std::string("ncclAllGather: ") + ncclGetErrorString(r));
+  check(cudaMemcpyAsync(all.data(), dev.ptr, hb * nbuf * world_, cudaMemcpyDeviceToHost, stream_), "IPC handles");
+  check(cudaStreamSynchronize(stream_), "IPC handles");
+  for (int q = 0; q < world_; ++q) {
+    if (q == rank_) continue;
+    for (int i = 0; i < nbuf; ++i) {
+      void *p = nullptr;
+      check(cudaIpcOpenMemHandle(&p, all[(size_t)q * nbuf + i], cudaIpcMemLazyEnablePeerAccess),
+            "cudaIpcOpenMemHandle");
+      peer_[i][q] = p;
+      ipc_opened_.push_back(p);
+    }
+  }
+}
+
+// Stream-ordered barrier: an all-reduce of one word completes on every rank only after every
+// rank's earlier work on its stream (the sweeps that read or write peer shards) has completed.
+void Engine::dist_barrier() {
+  if (world_ == 1) return;
+  ensure_comm();
+  dbar_.reserve(16);
+  ncclResult_t r = ncclAllReduce(dbar_.ptr, dbar_.ptr, 1, ncclInt32, ncclSum, comm_, stream_);
+  if (r != ncclSuccess) throw Error(QSIM_ENCCL, std::string("ncclAllReduce: ") + ncclGetErrorString(r));
 }
 
 // ---------------------------------------------------------------- multi-GPU
@@ -1335,6 +1610,10 @@ void Engine::comm_init(int rank, int world, const void *id) {
   rank_ = rank;
   world_ = world;
   reduced_ = false;
+  if (dist_ && have_circuit_) {
+    compile_all();
+    have_blocks_ = false;
+  }
 }
 
 void Engine::ensure_comm() {
@@ -1352,6 +1631,11 @@ void Engine::rank_range(uint64_t *b0, uint64_t *b1) const {
   const int c = (int)circ_.cuts.size();
   if (c > 62) throw Error(QSIM_EINVAL, "too many cuts");
   const unsigned __int128 B = (unsigned __int128)1 << c;
+  if (dist_) {  // distributed halves: every rank runs every branch on its shard
+    *b0 = 0;
+    *b1 = (uint64_t)B;
+    return;
+  }
   *b0 = (uint64_t)(B * (unsigned)rank_ / (unsigned)world_);
   *b1 = (uint64_t)(B * (unsigned)(rank_ + 1) / (unsigned)world_);
 }

@@ -39,6 +39,7 @@ struct DevBuf {
 // single-layer register sweep (TileSweepParams; the generated root sweep, or
 // QSIM_OPT_SWEEP_KERNEL 1).  A layer wider than the tile is split into several launches.
 struct TilePlan {
+  std::vector<std::pair<int, int>> swaps;  // distributed half: (local bit, global bit index) after it
   bool fused = false;
   bool multi_layer = false;  // several layers (stage lists) in this launch
   FusedSweepParams f;        // src/dst/pre filled at launch
@@ -117,6 +118,14 @@ class Engine {
   bool fuse_layers_ = false; // fuse consecutive layers into one HBM pass when they fit a tile
                              // (off by default: multi-pass tiles are not yet faster)
   bool time_sweeps_ = false;
+  // distributed half (§2.3.3): every half state is sharded over the
+  // communicator's ranks by its top gbits_ physical bits; all ranks run every branch
+  bool dist_ = false;
+  int gbits_ = 0;
+  std::vector<std::vector<void *>> peer_;  // [level buffer][rank]: device pointers (CUDA IPC)
+  std::vector<void *> ipc_opened_;
+  size_t dist_bytes_ = 0;
+  DevBuf dbar_;
 
   bool have_circuit_ = false;
   Circuit circ_;
@@ -151,6 +160,10 @@ class Engine {
   void ensure_device();
   void check(cudaError_t e, const char *what);
   void compile_plans(HalfExec &he);
+  void compile_all();                       // both halves for the current options / world
+  void plan_distributed(HalfExec &he);      // layout schedule with fused local/global swaps
+  void dist_buffers(size_t bytes, int nbuf);  // level buffers + IPC peer pointers
+  void dist_barrier();                      // stream-ordered barrier over the ranks
   std::vector<int> choose_perm(const HalfExec &he) const;
   bool plan_fused(const HalfProgram &hp, const std::vector<Stage> &stages, const Diag &pre, TilePlan &tp);
   std::vector<TilePlan> level_launches(const HalfProgram &hp, const Level &lev, size_t n);
@@ -165,7 +178,7 @@ class Engine {
   int lazy_depth(int half, int64_t nS) const;
   int tma_stages(const TilePlan &tp) const;
   void launch_plan(const TilePlan &tp, const Diag &fork, bool first_chunk_of_level, const void *src,
-                   void *dst, int h);
+                   void *dst, const HalfProgram &hp, int out_buf = -1);
   void gather_leaf(int half, uint64_t child_last, const void *psi, const uint64_t *dS, int64_t nS,
                    void *out_row, int depth);
   void gemm(const void *U, const void *L, int64_t K, int64_t M, int64_t N, double *A);

@@ -68,6 +68,16 @@ struct TileSweepParams {
   int32_t run_m;            // hb[0..run_m-1] == L..L+run_m-1: contiguous run of 2^(L+m) amps
   int32_t n_lane;           // TMA sweep: compact list of the lane-bit targets (pass 0)
   uint8_t lane_bit[5], lane_kind[5];
+  // distributed half (f3): this rank's shard holds the amplitudes whose global bits (positions
+  // h_local ..) equal `rank`; gbase = those bits, ORed into indices for the diagonals only.
+  // nswap > 0: the sweep's output exchanges local bit swap_l[j] with global bit j' = swap_j[j]:
+  // a tile whose outer bit swap_l[j] differs from the rank's bit j' goes to rank ^ (1 << j')
+  // (peer[rank delta] = that rank's destination buffer) with bit swap_l[j] set to the rank's bit.
+  uint32_t gbase;
+  uint32_t rank;
+  int32_t nswap;
+  uint8_t swap_l[2], swap_j[2];
+  void *peer[4];
 };
 
 // pre_mode: 0 none, 1 apply pre diagonal to loaded values, 2 generate (no load)
@@ -159,9 +169,10 @@ cudaError_t launch_small(const SmallParams &p, bool c128, uint64_t nb, cudaStrea
 int small_max_h(bool c128);
 
 // ---------------------------------------------------------------- gather / reconstruction
-// out[j] = psi[S[j]] * pend(S[j])
+// out[j] = pend(S[j]) psi[S[j] & lmask] if (S[j] & ~lmask) == gsel (the shard owns it), else 0
 cudaError_t launch_gather(const void *psi, const uint64_t *S, int64_t n, void *out,
-                          const DiagDev &pend, bool c128, cudaStream_t s);
+                          const DiagDev &pend, bool c128, cudaStream_t s, uint64_t lmask = ~0ull,
+                          uint64_t gsel = 0);
 
 // Lazy last layer: the leaf's final sweep evaluated only at the sampled indices,
 //   out[j] = post(x) * sum_y  prod_t M'_t[x_t, y_t] * pre(y) * psi[y],   x = S[j],

@@ -197,14 +197,22 @@ struct LayerSpec {
 }  // namespace
 
 HalfProgram compile_half(const Circuit &c, bool upper, const std::vector<int> &perm) {
+  const int h = (int)(upper ? c.h_u : c.h_l);
+  std::vector<int> p = perm;
+  if (p.empty())
+    for (int b = 0; b < h; ++b) p.push_back(b);
+  return compile_half_layers(c, upper, std::vector<std::vector<int>>(c.depth + 2, p), p);
+}
+
+HalfProgram compile_half_layers(const Circuit &c, bool upper, const std::vector<std::vector<int>> &layer_perm,
+                                const std::vector<int> &final_perm) {
   HalfProgram hp;
   hp.upper = upper;
   hp.h = (int)(upper ? c.h_u : c.h_l);
-  hp.perm = perm;
-  if (hp.perm.empty())
-    for (int b = 0; b < hp.h; ++b) hp.perm.push_back(b);
+  hp.hl = hp.h;
+  hp.perm = final_perm;
   const uint32_t lo = upper ? 0 : c.h_u, hi = upper ? c.h_u : c.n;
-  auto bit_of = [&](uint32_t q) { return hp.perm[hp.h - 1 - (int)(q - lo)]; };
+  auto bit_at = [&](uint32_t q, int layer) { return layer_perm[layer][hp.h - 1 - (int)(q - lo)]; };
 
   std::vector<LayerSpec> layers(c.depth + 1);
   for (const qsim_gate &g : c.gates) {
@@ -212,10 +220,10 @@ HalfProgram compile_half(const Circuit &c, bool upper, const std::vector<int> &p
     if (g.kind == QSIM_CZ) {
       const bool in0 = g.q0 >= lo && g.q0 < hi, in1 = g.q1 >= lo && g.q1 < hi;
       if (!(in0 && in1)) continue;  // cut CZ (handled as a fork) or the other half
-      L.diag.add_cz(bit_of(g.q0), bit_of(g.q1));
+      L.diag.add_cz(bit_at(g.q0, (int)g.layer), bit_at(g.q1, (int)g.layer));
     } else {
       if (!(g.q0 >= lo && g.q0 < hi)) continue;
-      const int b = bit_of(g.q0);
+      const int b = bit_at(g.q0, (int)g.layer);
       if (g.kind == QSIM_T) {
         L.diag.add_T(b);
       } else {
@@ -242,7 +250,8 @@ HalfProgram compile_half(const Circuit &c, bool upper, const std::vector<int> &p
       lev.g0 = g0;
       for (int j = 0; j < lev.k; ++j) {
         const qsim_cut &cut = c.cuts[g0 + j];
-        lev.cut_bits.push_back(bit_of(upper ? cut.q_upper : cut.q_lower));
+        // the fork acts on the child level's input: the layout of its first layer
+        lev.cut_bits.push_back(bit_at(upper ? cut.q_upper : cut.q_lower, lev.fork_layer + 1));
       }
       g0 += lev.k;
     }

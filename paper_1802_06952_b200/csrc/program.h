@@ -64,6 +64,9 @@ struct Sweep {
   Diag pre, post;
   bool gen = false;  // input not read: value = pre(i) (the H layer and leading diagonals)
   int first_layer = 0, last_layer = 0;
+  // distributed half: after this sweep, exchange local bit .first with global
+  // bit .second (physical positions) — fused into the sweep's stores over peer memory
+  std::vector<std::pair<int, int>> swaps;
 };
 
 struct Level {
@@ -77,7 +80,9 @@ struct Level {
 struct HalfProgram {
   bool upper = true;
   int h = 0;
-  std::vector<int> perm;  // physical bit of canonical local bit c (h-1-k' for local qubit k')
+  int hl = 0;  // qubits per shard: h, or h - log2(ranks) for a distributed half (f3)
+  std::vector<int> perm;  // physical bit of canonical local bit c (h-1-k' for local qubit k'):
+                          // the layout of the leaf (and of every sweep unless the layout changes)
   std::vector<Level> levels;
   // Diagonal of fork child c at level l (P_{bits} on the upper endpoints, Z^{bits} on the lower)
   Diag fork_diag(int level, uint64_t child) const;
@@ -108,5 +113,9 @@ std::string build_circuit(uint32_t rows, uint32_t cols, uint32_t depth, const qs
 // perm: physical bit of each canonical local bit (identity when empty); every bit position of the
 // program (gates, diagonals, forks) is physical.
 HalfProgram compile_half(const Circuit &c, bool upper, const std::vector<int> &perm = {});
+// The same with a layout per gate layer (layer_perm[t], t = 0..depth; a layer's diagonal and fork
+// bits use the layout of the sweep that applies them); perm of the result = final_perm.
+HalfProgram compile_half_layers(const Circuit &c, bool upper, const std::vector<std::vector<int>> &layer_perm,
+                                const std::vector<int> &final_perm);
 
 }  // namespace qsim

@@ -26,12 +26,17 @@ struct CxT<double> {
 // ---------------------------------------------------------------- gather
 template <typename R>
 __global__ void gather_kernel(const typename CxT<R>::T *__restrict__ psi, const uint64_t *__restrict__ S,
-                              int64_t n, typename CxT<R>::T *__restrict__ out, DiagDev d) {
+                              int64_t n, typename CxT<R>::T *__restrict__ out, DiagDev d, uint64_t lmask,
+                              uint64_t gsel) {
   using C = typename CxT<R>::T;
   for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n;
        j += (int64_t)gridDim.x * blockDim.x) {
     const uint64_t i = S[j];
-    C x = psi[i];
+    if ((i & ~lmask) != gsel) {  // another shard's amplitude (distributed half)
+      out[j].x = out[j].y = (R)0;
+      continue;
+    }
+    C x = psi[i & lmask];
     if (d.active) {
       const uint32_t ii = (uint32_t)i;
       const int ph = diag_phase(ii, d, d.zm);
@@ -47,13 +52,13 @@ __global__ void gather_kernel(const typename CxT<R>::T *__restrict__ psi, const 
 }
 
 cudaError_t launch_gather(const void *psi, const uint64_t *S, int64_t n, void *out,
-                          const DiagDev &pend, bool c128, cudaStream_t s) {
+                          const DiagDev &pend, bool c128, cudaStream_t s, uint64_t lmask, uint64_t gsel) {
   const int threads = 256;
   const int blocks = (int)std::min<int64_t>((n + threads - 1) / threads, 4096);
   if (c128)
-    gather_kernel<double><<<blocks, threads, 0, s>>>((const double2 *)psi, S, n, (double2 *)out, pend);
+    gather_kernel<double><<<blocks, threads, 0, s>>>((const double2 *)psi, S, n, (double2 *)out, pend, lmask, gsel);
   else
-    gather_kernel<float><<<blocks, threads, 0, s>>>((const float2 *)psi, S, n, (float2 *)out, pend);
+    gather_kernel<float><<<blocks, threads, 0, s>>>((const float2 *)psi, S, n, (float2 *)out, pend, lmask, gsel);
   return cudaGetLastError();
 }
 

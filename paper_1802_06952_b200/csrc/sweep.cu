@@ -70,7 +70,7 @@ __global__ void __launch_bounds__(256, 2) tile_sweep_kernel(const __grid_constan
         if constexpr (PRE == 2) {
 #pragma unroll
           for (int e = 0; e < NV; ++e) {
-            const uint32_t idx = gi + e;
+            const uint32_t idx = (gi + e) | p.gbase;  // global index (distributed half)
             C x = tab_pre[diag_phase(idx, p.pre, pre_zm)];
             if ((idx & p.pre.pm) != pre_pv) x.x = x.y = (R)0;
             v[r][e] = x;
@@ -80,7 +80,7 @@ __global__ void __launch_bounds__(256, 2) tile_sweep_kernel(const __grid_constan
           if constexpr (PRE == 1) {
 #pragma unroll
             for (int e = 0; e < NV; ++e) {
-              const uint32_t idx = gi + e;
+              const uint32_t idx = (gi + e) | p.gbase;  // global index (distributed half)
               C x = cmul(v[r][e], tab_pre[diag_phase(idx, p.pre, pre_zm)]);
               if ((idx & p.pre.pm) != pre_pv) x.x = x.y = (R)0;
               v[r][e] = x;
@@ -143,7 +143,7 @@ __global__ void __launch_bounds__(256, 2) tile_sweep_kernel(const __grid_constan
           if (p.post.active) {
 #pragma unroll
             for (int e = 0; e < NV; ++e) {
-              const uint32_t idx = gi + e;
+              const uint32_t idx = (gi + e) | p.gbase;  // global index (distributed half)
               C x = cmul(v[r][e], tab_post[diag_phase(idx, p.post, p.post.zm)]);
               if ((idx & p.post.pm) != p.post.pv) x.x = x.y = (R)0;
               v[r][e] = x;
@@ -203,7 +203,7 @@ __global__ void __launch_bounds__(256, 2) tile_sweep_kernel(const __grid_constan
         if (p.post.active) {
 #pragma unroll
           for (int e = 0; e < NV; ++e) {
-            const uint32_t idx = gi + e;
+            const uint32_t idx = (gi + e) | p.gbase;  // global index (distributed half)
             C x = cmul(v[r][e], tab_post[diag_phase(idx, p.post, p.post.zm)]);
             if ((idx & p.post.pm) != p.post.pv) x.x = x.y = (R)0;
             v[r][e] = x;

@@ -196,7 +196,8 @@ __device__ __forceinline__ uint32_t slot_smem(uint32_t base, const uint8_t *gsel
   return si;
 }
 
-template <typename R, int PRE, int NPASS, int NST>
+// SW = 1: the distributed-half variant whose stores implement a local / global bit swap (p.nswap)
+template <typename R, int PRE, int NPASS, int NST, int SW = 0>
 __global__ void __launch_bounds__(544, 1) tile_sweep_tma_kernel(const __grid_constant__ TileSweepParams p) {
   using C = typename Cx2<R>::T;
   using V = typename Cx2<R>::V;
@@ -303,7 +304,7 @@ __global__ void __launch_bounds__(544, 1) tile_sweep_tma_kernel(const __grid_con
     // B-phases of the pre (pass-0 thread base, bits 0-2) and post (last pass, bits 3-5) diagonals
     uint32_t phB = 0;
     {
-      uint32_t b0 = outer | ((uint32_t)lane << VB), b1 = b0;
+      uint32_t b0 = outer | ((uint32_t)lane << VB) | p.gbase, b1 = b0;
 #pragma unroll
       for (int j = 0; j < 3; ++j)
         if ((wl >> j) & 1) {
@@ -325,7 +326,7 @@ __global__ void __launch_bounds__(544, 1) tile_sweep_tma_kernel(const __grid_con
       }
 #pragma unroll
     for (int r = 0; r < 16; ++r) unpack<R, NV>(tile[slot_smem(ts, p.gsel[0], r)], v[r]);
-    if constexpr (PRE == 1) apply_split<R, NV>(v, tg, phB & 7u, p.pre_s, tab_pre);
+    if constexpr (PRE == 1) apply_split<R, NV>(v, tg | p.gbase, phB & 7u, p.pre_s, tab_pre);
     low_gates<R, NV>(v, p, lane);
     reg_gates<R, NV>(v, p.gkind[0]);
 
@@ -351,8 +352,20 @@ __global__ void __launch_bounds__(544, 1) tile_sweep_tma_kernel(const __grid_con
     if constexpr (NPASS == 2) reg_gates<R, NV>(v, p.gkind[1]);
 
     constexpr int QL = NPASS - 1;
-    if (p.post.active) apply_split<R, NV>(v, tg, phB >> 3, p.post_s, tab_post);
-    V *d0 = dst + (tg >> VB);
+    if (p.post.active) apply_split<R, NV>(v, tg | p.gbase, phB >> 3, p.post_s, tab_post);
+    V *dbase = dst;
+    if constexpr (SW == 1) {  // distributed half: this tile's destination rank and address (kernels.h)
+      uint32_t delta = 0;
+#pragma unroll
+      for (int j = 0; j < 2; ++j)
+        if (j < p.nswap) {
+          const uint32_t lb = (outer >> p.swap_l[j]) & 1u, rb = (p.rank >> p.swap_j[j]) & 1u;
+          delta |= (lb ^ rb) << p.swap_j[j];
+          tg = (tg & ~(1u << p.swap_l[j])) | (rb << p.swap_l[j]);
+        }
+      dbase = reinterpret_cast<V *>(p.peer[delta]);
+    }
+    V *d0 = dbase + (tg >> VB);
 #pragma unroll
     for (int r = 0; r < 16; ++r) {
       uint32_t off = 0;
@@ -364,21 +377,24 @@ __global__ void __launch_bounds__(544, 1) tile_sweep_tma_kernel(const __grid_con
   }
 }
 
-template <typename R, int PRE, int NPASS, int NST>
+template <typename R, int PRE, int NPASS, int NST, int SW = 0>
 static cudaError_t launch_tma_t(const TileSweepParams &p, int grid, cudaStream_t s) {
-  tile_sweep_tma_kernel<R, PRE, NPASS, NST><<<grid, 544, (size_t)NST * kTileBytes, s>>>(p);
+  tile_sweep_tma_kernel<R, PRE, NPASS, NST, SW><<<grid, 544, (size_t)NST * kTileBytes, s>>>(p);
   return cudaGetLastError();
 }
 
-template <typename R, int NST>
+template <typename R, int NST, int SW = 0>
 static cudaError_t launch_tma_r(const TileSweepParams &p, int pre_mode, int npass, int grid, cudaStream_t s) {
   if (npass == 1)
-    return pre_mode ? launch_tma_t<R, 1, 1, NST>(p, grid, s) : launch_tma_t<R, 0, 1, NST>(p, grid, s);
-  return pre_mode ? launch_tma_t<R, 1, 2, NST>(p, grid, s) : launch_tma_t<R, 0, 2, NST>(p, grid, s);
+    return pre_mode ? launch_tma_t<R, 1, 1, NST, SW>(p, grid, s) : launch_tma_t<R, 0, 1, NST, SW>(p, grid, s);
+  return pre_mode ? launch_tma_t<R, 1, 2, NST, SW>(p, grid, s) : launch_tma_t<R, 0, 2, NST, SW>(p, grid, s);
 }
 
 cudaError_t launch_tile_sweep_tma(const TileSweepParams &p, bool c128, int pre_mode, int npass, int grid,
                                   cudaStream_t s, int stages) {
+  if (p.nswap)  // distributed-half swap sweeps: two stages
+    return c128 ? launch_tma_r<double, 2, 1>(p, pre_mode, npass, grid, s)
+                : launch_tma_r<float, 2, 1>(p, pre_mode, npass, grid, s);
   if (stages == 3)
     return c128 ? launch_tma_r<double, 3>(p, pre_mode, npass, grid, s)
                 : launch_tma_r<float, 3>(p, pre_mode, npass, grid, s);
@@ -386,11 +402,13 @@ cudaError_t launch_tile_sweep_tma(const TileSweepParams &p, bool c128, int pre_m
               : launch_tma_r<float, 2>(p, pre_mode, npass, grid, s);
 }
 
-template <typename R, int NST>
+template <typename R, int NST, int SW = 0>
 static cudaError_t tma_setup_r() {
   const int bytes = NST * kTileBytes;
-  const void *fns[4] = {(const void *)tile_sweep_tma_kernel<R, 0, 1, NST>, (const void *)tile_sweep_tma_kernel<R, 1, 1, NST>,
-                        (const void *)tile_sweep_tma_kernel<R, 0, 2, NST>, (const void *)tile_sweep_tma_kernel<R, 1, 2, NST>};
+  const void *fns[4] = {(const void *)tile_sweep_tma_kernel<R, 0, 1, NST, SW>,
+                        (const void *)tile_sweep_tma_kernel<R, 1, 1, NST, SW>,
+                        (const void *)tile_sweep_tma_kernel<R, 0, 2, NST, SW>,
+                        (const void *)tile_sweep_tma_kernel<R, 1, 2, NST, SW>};
   for (const void *f : fns) {
     cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
     if (e != cudaSuccess) return e;
@@ -400,6 +418,8 @@ static cudaError_t tma_setup_r() {
 
 cudaError_t tile_sweep_tma_setup(bool c128) {
   cudaError_t e = c128 ? tma_setup_r<double, 2>() : tma_setup_r<float, 2>();
+  if (e != cudaSuccess) return e;
+  e = c128 ? tma_setup_r<double, 2, 1>() : tma_setup_r<float, 2, 1>();
   if (e != cudaSuccess) return e;
   return c128 ? tma_setup_r<double, 3>() : tma_setup_r<float, 3>();
 }
