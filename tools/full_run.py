@@ -36,6 +36,7 @@ def main():
     ap.add_argument("--bins", type=int, default=160)
     ap.add_argument("--hbm-gbps", type=float, default=5590.0, help="sweep bandwidth for the cost model")
     ap.add_argument("--out", default=None)
+    ap.add_argument("--grid", default=None, help="rows,cols,depth,log2_nu,log2_nl instead of --config")
     args = ap.parse_args()
 
     rank, world = int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1))
@@ -45,6 +46,9 @@ def main():
         dist.init_process_group("gloo")
     prec = Q.QSIM_C128 if args.precision == "c128" else Q.QSIM_C64
     rows, cols, depth, lu, ll = CONFIGS[args.config]
+    if args.grid:
+        rows, cols, depth, lu, ll = (int(v) for v in args.grid.split(","))
+        args.config = f"{rows}x{cols}d{depth}"
     circ = generate(rows, cols, depth, args.seed)
     Su = sample_block(circ.h_upper, 1 << (lu or circ.h_upper), args.seed + 1)
     Sl = sample_block(circ.h_lower, 1 << (ll or circ.h_lower), args.seed + 2)
