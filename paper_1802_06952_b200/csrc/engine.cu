@@ -1084,6 +1084,8 @@ static LazyLayer lazy_layer(const Sweep &sw, const Diag &pre) {
   }
   ll.pre = to_dev(pre);
   ll.post = to_dev(sw.post, true);
+  ll.lmask = ~0ull;
+  ll.gsel = 0;
   return ll;
 }
 
@@ -1094,13 +1096,15 @@ static LazyLayer lazy_layer(const Sweep &sw, const Diag &pre) {
 int Engine::lazy_depth(int half, int64_t nS) const {
   const HalfProgram &hp = half_[half].prog;
   const int F = (int)hp.levels.size() - 1;
-  if (full_leaf_ || F < 1 || lazy_depth_ < 1 || dist_) return 0;
+  if (full_leaf_ || F < 1 || lazy_depth_ < 1) return 0;
   const auto &sw = hp.levels[F].sweeps;
   if (sw.empty() || sw.back().gates.size() > 12) return 0;
   if (lazy_depth_ < 2 || sw.size() < 2) return 1;
+  // distributed half: a skipped sweep must not carry a local/global swap
+  if (dist_ && !sw[sw.size() - 2].swaps.empty()) return 1;
   const int kd = (int)sw.back().gates.size(), kd1 = (int)sw[sw.size() - 2].gates.size();
   if (kd + kd1 > 20 || ((double)nS * std::ldexp(1.0, kd)) > (double)(1 << 26)) return 1;
-  const double sweep = 2.0 * std::ldexp(1.0, hp.h) * (double)amp_;
+  const double sweep = 2.0 * std::ldexp(1.0, hp.hl) * (double)amp_;
   const double lazy1 = 96.0 * (double)nS * std::ldexp(1.0, kd);
   const double lazy2 = 96.0 * (double)nS * std::ldexp(1.0, kd + kd1) + 2.0 * lazy1;
   if (lazy_depth_ == 3) return 2;  // forced (tests)
@@ -1120,12 +1124,18 @@ void Engine::gather_leaf(int half, uint64_t child_last, const void *psi, const u
     auto pre_of = [&](size_t s) {
       return s == 0 ? Diag::merge(he.prog.fork_diag(F, child_last), lev.sweeps[0].pre) : lev.sweeps[s].pre;
     };
-    const LazyLayer lld = lazy_layer(lev.sweeps[n - 1], pre_of(n - 1));
+    LazyLayer lld = lazy_layer(lev.sweeps[n - 1], pre_of(n - 1));
+    if (dist_) {
+      lld.lmask = (1ull << he.prog.hl) - 1ull;
+      lld.gsel = (uint64_t)rank_ << he.prog.hl;
+    }
     if (depth == 1) {
       check(launch_gather_layer(psi, dS, nS, out_row, lld, c128_, stream_), "gather_layer launch");
       st_.kernel_launches++;
     } else {
-      const LazyLayer ll1 = lazy_layer(lev.sweeps[n - 2], pre_of(n - 2));
+      LazyLayer ll1 = lazy_layer(lev.sweeps[n - 2], pre_of(n - 2));
+      ll1.lmask = lld.lmask;
+      ll1.gsel = lld.gsel;
       const int64_t ncone = nS << lld.k;
       cone_idx_.reserve((size_t)ncone * 8);
       cone_val_.reserve((size_t)ncone * amp_);

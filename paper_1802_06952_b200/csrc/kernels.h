@@ -182,6 +182,9 @@ struct LazyLayer {
   uint8_t bit[24];
   uint32_t sxmask, symask, tmask;
   DiagDev pre, post;
+  // distributed half: the shard holds the indices with (i & ~lmask) == gsel, at i & lmask (the
+  // layer's targets are local, so every term of an owned index is in the shard); others give 0
+  uint64_t lmask, gsel;
 };
 cudaError_t launch_gather_layer(const void *psi, const uint64_t *S, int64_t n, void *out,
                                 const LazyLayer &ll, bool c128, cudaStream_t s);

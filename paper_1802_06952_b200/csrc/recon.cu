@@ -75,6 +75,10 @@ __global__ void __launch_bounds__(256) gather_layer_kernel(const typename CxT<R>
   const int lane = threadIdx.x & 31;
   const int64_t j = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (j >= n) return;
+  if ((S[j] & ~ll.lmask) != ll.gsel) {  // another shard's index
+    if (lane == 0) out[j].x = out[j].y = (R)0;
+    return;
+  }
   const uint32_t x = (uint32_t)S[j];
   const uint32_t base = x & ~ll.tmask;
   const uint32_t nterm = 1u << ll.k;
@@ -83,7 +87,7 @@ __global__ void __launch_bounds__(256) gather_layer_kernel(const typename CxT<R>
     uint32_t y = base;
 #pragma unroll 4
     for (int t = 0; t < ll.k; ++t) y |= ((m >> t) & 1u) << ll.bit[t];
-    C v = psi[y];
+    C v = psi[y & (uint32_t)ll.lmask];
     int ph = 6 * __popc((x ^ y) & ll.sxmask) + 4 * __popc(~x & y & ll.symask);
     if (ll.pre.active) {
       ph += diag_phase(y, ll.pre, ll.pre.zm);
@@ -152,6 +156,10 @@ __global__ void __launch_bounds__(256) gather_layer_compact_kernel(const typenam
   const int lane = threadIdx.x & 31;
   const int64_t j = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (j >= n) return;
+  if ((S[j] & ~ll.lmask) != ll.gsel) {  // another shard's index
+    if (lane == 0) out[j].x = out[j].y = (R)0;
+    return;
+  }
   const uint32_t x = (uint32_t)S[j];
   const uint32_t base = x & ~ll.tmask;
   const uint32_t nterm = 1u << ll.k;
