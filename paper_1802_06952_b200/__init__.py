@@ -10,8 +10,10 @@ import importlib
 
 
 def __getattr__(name):
-    if name == "qsim":
-        return importlib.import_module(".qsim", __name__)
+    if name in ("qsim", "build"):
+        return importlib.import_module("." + name, __name__)
+    if name.startswith("__"):
+        raise AttributeError(name)
     mod = importlib.import_module(".qsim", __name__)
     if hasattr(mod, name):
         return getattr(mod, name)
