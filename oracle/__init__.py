@@ -16,6 +16,8 @@ Modules
   statevector  full state vector, gate by gate, no fusion (Supp. A Eq. 4)
   partition    cut list, branch half-circuits, flat partitioned simulator
                (Supp. A Eqs. 7-8)
+  multipart    t-way partitions (rows in bands), A = sum_b prod_k psi^k_b[S_k]
+               (Fig. 3; DESIGN.md R-f4)
   reconstruct  A[i,j] = sum_b U_b[i] L_b[j] (Fig. 1 caption P:175)
   sampler      Philox4x32-10 + two-level inverse CDF over |a|^2
   stats        Porter-Thomas / Gumbel Eq. 7
