@@ -261,6 +261,38 @@ typedef struct {
 qsim_status qsim_cost_model(qsim_ctx *ctx, uint64_t n_upper, uint64_t n_lower, double hbm_gbps,
                             qsim_cost_t *out);
 
+/* ---------------------------------------------------------------- multi-part partitions (f4) */
+
+/* t-way partitions of the loaded circuit ("dividing the circuit into three or
+ * four parts is more effective if the circuit depth is small"; Fig. 3).  Part k is
+ * the band of rows [r_k, r_{k+1}) with r_0 = 0, r_t = rows and r_1 < ... < r_{t-1} given in
+ * `row_cuts` (t - 1 host values; cut_row of qsim_load_circuit is ignored here); its qubits are
+ * [r_k*cols, r_{k+1}*cols), its local index has qubit r_k*cols as the MSB, and the full index
+ * is the concatenation x_0 x_1 ... x_{t-1} (part 0 in the top bits).  Every CZ crossing a
+ * boundary is split by Eq. 1: P_b on its upper endpoint, I / Z on its lower endpoint;
+ * boundary j's cuts are ordered by (layer, upper qubit), first cut = MSB of beta_j.
+ *
+ * qsim_multipart_plan (host only, no device needed): part_qubits[k] (t values, nullable),
+ * boundary_cuts[j] = c_j (t - 1 values, nullable) and *log2_states = log2 of
+ * sum_k 2^(n_k + c_{k-1} + c_k), the amplitudes of all part leaves this library evolves
+ * (nullable).  ESTATE without a circuit; EINVAL if t is not in 2..8, the row cuts are not
+ * strictly increasing inside (0, rows) or a part has more than 32 qubits. */
+qsim_status qsim_multipart_plan(qsim_ctx *ctx, uint32_t n_parts, const uint32_t *row_cuts,
+                                uint32_t *part_qubits, uint32_t *boundary_cuts, double *log2_states);
+
+/* Amplitudes of the index blocks S_0 x ... x S_{t-1}:
+ *   amps[i_0, ..., i_{t-1}] = sum_b prod_k psi^k_b[S_k[i_k]]   (row-major, i_{t-1} fastest)
+ * blocks: the t blocks concatenated (host, part-local indices < 2^{n_k}, unique, any order);
+ * n_block[k]: size of block k.  amps: host, prod_k n_block[k] complex values of the ctx
+ * precision (float2 / double2).  Every part is evolved as a branch tree over the cuts of its
+ * two boundaries (2^(c_{k-1} + c_k) leaves) and the blocks are contracted as a chain of fp64
+ * GEMMs on the device.  The two-half state of qsim_evolve_range is not touched.
+ * EINVAL as qsim_multipart_plan, for a bad block, a part with more than 30 cut bits, an
+ * output above 64 GiB, or with distributed halves enabled; ENOMEM if the part states, slices
+ * or contraction operands do not fit; ECUDA without a device. */
+qsim_status qsim_multipart_amplitudes(qsim_ctx *ctx, uint32_t n_parts, const uint32_t *row_cuts,
+                                      const uint64_t *blocks, const size_t *n_block, void *amps);
+
 /* Counters (see qsim_stats_t).  Synchronises the ctx stream when sweeps are timed. */
 qsim_status qsim_stats(qsim_ctx *ctx, qsim_stats_t *out);
 qsim_status qsim_stats_reset(qsim_ctx *ctx);

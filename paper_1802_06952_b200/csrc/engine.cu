@@ -116,6 +116,8 @@ Engine::Engine(qsim_precision prec, int device) : prec_(prec), device_(device) {
   if (device < 0) throw Error(QSIM_EINVAL, "device must be >= 0");
   c128_ = prec == QSIM_C128;
   amp_ = c128_ ? 16 : 8;
+  half_.emplace_back();
+  half_.emplace_back();
 }
 
 Engine::~Engine() {
@@ -841,6 +843,7 @@ void Engine::upload_small(HalfExec &he) {
     d.first_sweep = (int)sws.size();
     d.nsweeps = (int)lev.sweeps.size();
     for (int j = 0; j < lev.k; ++j) d.cut_bits[j] = (uint8_t)lev.cut_bits[j];
+    d.pmask = lev.pmask;
     levs[l] = d;
     for (auto &sw : lev.sweeps) {
       SmallSweepDev s;
@@ -1183,7 +1186,7 @@ void Engine::ensure_states(int half, int nbuf) {
 void Engine::evolve_half(int half, uint64_t b0, uint64_t b1, void *slice, const uint64_t *dS, int64_t nS) {
   HalfExec &he = half_[half];
   const HalfProgram &hp = he.prog;
-  const int c = (int)circ_.cuts.size();
+  const int c = hp.ncuts;
   if (!he.tree) {
     if (hp.h > small_max_h(c128_))
       throw Error(QSIM_EINVAL, "flat (small-state) mode needs h <= 12");
@@ -1193,7 +1196,6 @@ void Engine::evolve_half(int half, uint64_t b0, uint64_t b1, void *slice, const 
     sp.sweeps = he.d_sweeps.as<SmallSweepDev>();
     sp.nlevels = (int)hp.levels.size();
     sp.h = hp.h;
-    sp.upper = hp.upper ? 1 : 0;
     sp.c = c;
     sp.S = dS;
     sp.nS = nS;
@@ -1718,4 +1720,191 @@ void Engine::synchronize() {
   check(cudaStreamSynchronize(stream_), "cudaStreamSynchronize");
 }
 
+// ---------------------------------------------------------------- multi-part partitions (f4)
+// SURVEY §8(f) f4; PAPER.md P:114 ("dividing the circuit into three or four parts is more
+// effective if the circuit depth is small") and Fig. 3.  Parts are bands of rows
+// [r_k, r_{k+1}); Eq. 1 is applied to every CZ crossing a boundary (upper endpoint P_b,
+// lower endpoint I / Z, as the bipartition does; DESIGN.md R-f4).  Part k depends only on the
+// bits of its two boundaries, so it is one branch tree over those cuts (prefix-shared like a
+// half), and the amplitudes of sampled blocks are the chain contraction
+//   A[i_0, .., i_{t-1}] = sum_{beta_0..beta_{t-2}} X_0[beta_0, i_0] X_1[beta_0, beta_1, i_1] ...
+//                                                    X_{t-1}[beta_{t-2}, i_{t-1}],
+// evaluated right to left as batched fp64 GEMMs (branch_gemm_kernel with a batch index).
+Engine::MultiPart Engine::multipart_layout(uint32_t t, const uint32_t *row_cuts) const {
+  if (!have_circuit_) throw Error(QSIM_ESTATE, "no circuit loaded");
+  if (t < 2 || t > 8) throw Error(QSIM_EINVAL, "n_parts must be in 2..8");
+  if (!row_cuts) throw Error(QSIM_EINVAL, "row_cuts is NULL");
+  MultiPart mp;
+  mp.bounds.push_back(0);
+  for (uint32_t j = 0; j + 1 < t; ++j) mp.bounds.push_back(row_cuts[j]);
+  mp.bounds.push_back(circ_.rows);
+  for (uint32_t k = 0; k < t; ++k) {
+    if (mp.bounds[k] >= mp.bounds[k + 1])
+      throw Error(QSIM_EINVAL, "row_cuts must be strictly increasing inside (0, rows)");
+    if ((mp.bounds[k + 1] - mp.bounds[k]) * circ_.cols > 32)
+      throw Error(QSIM_EINVAL, "each part must have at most 32 qubits");
+  }
+  auto part_of = [&](uint32_t q) {
+    const uint32_t r = q / circ_.cols;
+    uint32_t k = 0;
+    while (r >= mp.bounds[k + 1]) ++k;
+    return (int)k;
+  };
+  struct XC {
+    int layer;
+    uint32_t qu, ql;
+    int j;
+  };
+  std::vector<XC> xs;
+  for (const qsim_gate &g : circ_.gates) {
+    if (g.kind != QSIM_CZ) continue;
+    const int pa = part_of(g.q0), pb = part_of(g.q1);
+    if (pa == pb) continue;
+    xs.push_back(XC{(int)g.layer, std::min(g.q0, g.q1), std::max(g.q0, g.q1), std::min(pa, pb)});
+  }
+  std::sort(xs.begin(), xs.end(),
+            [](const XC &a, const XC &b) { return a.layer != b.layer ? a.layer < b.layer : a.qu < b.qu; });
+  mp.c.assign(t - 1, 0);
+  mp.cuts.resize(t);
+  mp.bits.resize(t);
+  for (const XC &x : xs) {
+    const int idx = mp.c[x.j]++;
+    mp.cuts[x.j].push_back(PartCut{x.layer, x.qu, true});  // part above the boundary: P_b
+    mp.bits[x.j].push_back({x.j, idx});
+    mp.cuts[x.j + 1].push_back(PartCut{x.layer, x.ql, false});  // part below: Z^b
+    mp.bits[x.j + 1].push_back({x.j, idx});
+  }
+  return mp;
+}
+
+void Engine::multipart_plan(uint32_t t, const uint32_t *row_cuts, uint32_t *part_qubits, uint32_t *boundary_cuts,
+                            double *log2_states) {
+  const MultiPart mp = multipart_layout(t, row_cuts);
+  double states = 0.0;
+  for (uint32_t k = 0; k < t; ++k) {
+    const uint32_t nq = (mp.bounds[k + 1] - mp.bounds[k]) * circ_.cols;
+    if (part_qubits) part_qubits[k] = nq;
+    states += std::ldexp(1.0, (int)nq + (int)mp.cuts[k].size());
+  }
+  for (uint32_t j = 0; j + 1 < t; ++j)
+    if (boundary_cuts) boundary_cuts[j] = (uint32_t)mp.c[j];
+  if (log2_states) *log2_states = std::log2(states);
+}
+
+void Engine::multipart_amplitudes(uint32_t t, const uint32_t *row_cuts, const uint64_t *blocks, const size_t *n_block,
+                                  void *amps) {
+  if (dist_) throw Error(QSIM_EINVAL, "multi-part partitions do not combine with distributed halves");
+  if (!blocks || !n_block) throw Error(QSIM_EINVAL, "blocks / n_block is NULL");
+  const MultiPart mp = multipart_layout(t, row_cuts);
+  std::vector<int> nq(t);
+  std::vector<int64_t> ns(t);
+  std::vector<size_t> off(t + 1, 0);
+  double total = 1.0;
+  for (uint32_t k = 0; k < t; ++k) {
+    nq[k] = (int)((mp.bounds[k + 1] - mp.bounds[k]) * circ_.cols);
+    ns[k] = (int64_t)n_block[k];
+    validate_block(blocks + off[k], n_block[k], (uint32_t)nq[k], "part");
+    off[k + 1] = off[k] + n_block[k];
+    total *= (double)ns[k];
+    if ((int)mp.cuts[k].size() > 30) throw Error(QSIM_EINVAL, "a part has more than 30 cut bits");
+  }
+  if (total * 16.0 > std::ldexp(1.0, 36)) throw Error(QSIM_EINVAL, "amplitude block larger than 64 GiB");
+  ensure_device();
+
+  // compile the part programs (branch trees over each part's cuts) into half_[2 + k]
+  while (half_.size() > 2) half_.pop_back();
+  for (uint32_t k = 0; k < t; ++k) {
+    half_.emplace_back();
+    HalfExec &he = half_.back();
+    std::vector<int> id(nq[k]);
+    for (int b = 0; b < nq[k]; ++b) id[b] = b;
+    const uint32_t lo = mp.bounds[k] * circ_.cols, hi = mp.bounds[k + 1] * circ_.cols;
+    he.prog = compile_part(circ_, lo, hi, k + 1 < t, mp.cuts[k], std::vector<std::vector<int>>(circ_.depth + 2, id), id);
+    compile_plans(he);
+    if (he.tree) {
+      const std::vector<int> perm = choose_perm(he);
+      bool ident = true;
+      for (size_t b = 0; b < perm.size(); ++b) ident = ident && perm[b] == (int)b;
+      if (!ident) {
+        he.prog = compile_part(circ_, lo, hi, k + 1 < t, mp.cuts[k],
+                               std::vector<std::vector<int>>(circ_.depth + 2, perm), perm);
+        compile_plans(he);
+      }
+    }
+  }
+
+  // evolve every part's branches; X_k[(beta_{k-1} << c_k) | beta_k, i] in fp64
+  std::vector<std::unique_ptr<DevBuf>> X(t);
+  DevBuf dS, slice, rowmap;
+  for (uint32_t k = 0; k < t; ++k) {
+    const int hidx = 2 + (int)k;
+    const HalfProgram &hp = half_[hidx].prog;
+    const int cp = hp.ncuts;
+    const int64_t nrows = (int64_t)1 << cp;
+    const int c_up = k > 0 ? mp.c[k - 1] : 0, c_dn = k + 1 < t ? mp.c[k] : 0;
+    std::vector<uint64_t> P((size_t)ns[k]);
+    for (int64_t i = 0; i < ns[k]; ++i) P[i] = hp.phys(blocks[off[k] + i]);
+    std::vector<uint32_t> rm((size_t)nrows);
+    for (int64_t r = 0; r < nrows; ++r) {
+      uint32_t up = 0, dn = 0;
+      for (int j = 0; j < cp; ++j) {
+        const uint32_t bit = (uint32_t)(r >> (cp - 1 - j)) & 1u;
+        const auto &bj = mp.bits[k][j];
+        if (bj.first + 1 == (int)k)
+          up |= bit << (c_up - 1 - bj.second);
+        else
+          dn |= bit << (c_dn - 1 - bj.second);
+      }
+      rm[r] = (up << c_dn) | dn;
+    }
+    dS.reserve((size_t)ns[k] * 8);
+    rowmap.reserve((size_t)nrows * 4);
+    slice.reserve((size_t)nrows * ns[k] * amp_);
+    check(cudaMemcpyAsync(dS.ptr, P.data(), P.size() * 8, cudaMemcpyHostToDevice, stream_), "upload part block");
+    check(cudaMemcpyAsync(rowmap.ptr, rm.data(), rm.size() * 4, cudaMemcpyHostToDevice, stream_), "upload rowmap");
+    evolve_half(hidx, 0, (uint64_t)nrows, slice.ptr, dS.as<uint64_t>(), ns[k]);
+    X[k].reset(new DevBuf());
+    X[k]->reserve((size_t)nrows * ns[k] * 16);
+    check(launch_permute_rows(slice.ptr, c128_, rowmap.as<uint32_t>(), nrows, ns[k], X[k]->as<double>(), stream_),
+          "permute rows");
+    st_.kernel_launches++;
+    st_.branches_evolved += (uint64_t)nrows;
+    check(cudaStreamSynchronize(stream_), "multi-part evolve");  // P, rm are host temporaries
+  }
+
+  // chain contraction, right to left: T_k[beta_{k-1}, (i_k, .., i_{t-1})]
+  DevBuf Tbuf[2];
+  const double *T = X[t - 1]->as<double>();
+  int64_t Nrest = ns[t - 1];
+  auto contract = [&](const double *U, int64_t K, int64_t M, int64_t batch, DevBuf &out) {
+    const size_t bytes = (size_t)batch * (size_t)M * (size_t)Nrest * 16;
+    out.reserve(bytes);
+    check(cudaMemsetAsync(out.ptr, 0, bytes, stream_), "zero contraction");
+    check(launch_branch_gemm_batched(U, T, K, M, Nrest, out.as<double>(), batch, stream_), "contraction gemm");
+    st_.kernel_launches++;
+    st_.gemm_flops += 8.0 * (double)batch * (double)M * (double)Nrest * (double)K;
+  };
+  for (int k = (int)t - 2; k >= 1; --k) {
+    DevBuf &out = Tbuf[k & 1];
+    contract(X[k]->as<double>(), (int64_t)1 << mp.c[k], ns[k], (int64_t)1 << mp.c[k - 1], out);
+    T = out.as<double>();
+    Nrest *= ns[k];
+  }
+  DevBuf Aout;
+  contract(X[0]->as<double>(), (int64_t)1 << mp.c[0], ns[0], 1, Aout);
+  const size_t n = (size_t)ns[0] * (size_t)Nrest;
+  if (amps) {
+    if (c128_) {
+      check(cudaMemcpyAsync(amps, Aout.ptr, n * 16, cudaMemcpyDeviceToHost, stream_), "D2H amplitudes");
+    } else {
+      tmp_.reserve(n * 8);
+      check(launch_cast_c128_to_c64(Aout.as<double>(), (int64_t)(2 * n), tmp_.as<float>(), stream_), "cast");
+      st_.kernel_launches++;
+      check(cudaMemcpyAsync(amps, tmp_.ptr, n * 8, cudaMemcpyDeviceToHost, stream_), "D2H amplitudes");
+    }
+  }
+  check(cudaStreamSynchronize(stream_), "multi-part amplitudes");
+}
+
 }  // namespace qsim
+

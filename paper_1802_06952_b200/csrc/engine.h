@@ -3,6 +3,8 @@
 #pragma once
 
 #include <cstdint>
+#include <deque>
+#include <memory>
 #include <stdexcept>
 #include <string>
 #include <utility>
@@ -94,6 +96,11 @@ class Engine {
   void comm_init(int rank, int world, const void *id);
   void rank_range(uint64_t *b0, uint64_t *b1) const;
   void cost_model(uint64_t nu, uint64_t nl, double hbm_gbps, qsim_cost_t *out);
+  // multi-part partitions (Fig. 3)
+  void multipart_plan(uint32_t n_parts, const uint32_t *row_cuts, uint32_t *part_qubits, uint32_t *boundary_cuts,
+                      double *log2_states);
+  void multipart_amplitudes(uint32_t n_parts, const uint32_t *row_cuts, const uint64_t *blocks,
+                            const size_t *n_block, void *amps);
   void stats(qsim_stats_t *out);
   void stats_reset();
   void synchronize();
@@ -129,7 +136,7 @@ class Engine {
 
   bool have_circuit_ = false;
   Circuit circ_;
-  HalfExec half_[2];
+  std::deque<HalfExec> half_;  // [0] upper, [1] lower half; [2 + k] part k of a multi-part partition (f4)
 
   bool have_blocks_ = false;
   std::vector<uint64_t> Su_, Sl_;
@@ -185,6 +192,14 @@ class Engine {
   double *reduced_block();
   void run_sampler(const double *p, int64_t M, int64_t N, const uint64_t *dSu, const uint64_t *dSl,
                    uint32_t hl, uint64_t seed, size_t n, uint64_t *out, double *mass);
+
+  struct MultiPart {
+    std::vector<uint32_t> bounds;                        // row bounds r_0 = 0 < ... < r_t = rows
+    std::vector<int> c;                                  // cuts per boundary j (t - 1)
+    std::vector<std::vector<PartCut>> cuts;              // per part, ordered by (layer, upper qubit)
+    std::vector<std::vector<std::pair<int, int>>> bits;  // per part: branch bit j -> (boundary, index in it)
+  };
+  MultiPart multipart_layout(uint32_t n_parts, const uint32_t *row_cuts) const;
 
   cudaEvent_t get_event();
   void resolve_events();

@@ -151,6 +151,7 @@ struct SmallLevelDev {
   int32_t k;
   int32_t first_sweep;
   int32_t nsweeps;
+  uint32_t pmask;  // bit j: cut j is P_b (upper endpoint), else Z^b
   uint8_t cut_bits[32];
 };
 struct SmallParams {
@@ -158,8 +159,7 @@ struct SmallParams {
   const SmallSweepDev *sweeps;
   int32_t nlevels;
   int32_t h;
-  int32_t upper;
-  int32_t c;                 // total cuts
+  int32_t c;                 // cut bits of the branch index (the program's ncuts)
   uint64_t b0;               // first branch of this launch (blockIdx.x = b - b0)
   const uint64_t *S;         // sampled indices of this half
   int64_t nS;
@@ -198,6 +198,13 @@ cudaError_t launch_gather_layer_compact(const void *V, const uint64_t *S, int64_
 // A[m, n] += sum_k U[k, m] * L[k, n]   (complex; U, L of the ctx precision, A double2)
 cudaError_t launch_branch_gemm(const void *U, const void *L, int64_t K, int64_t M, int64_t N,
                                double *A, bool c128, cudaStream_t s);
+// Multi-part contraction: for z in [0, batch),
+//   A_z[m, n] += sum_k U_z[k, m] * L[k, n],  U_z = U + z*K*M, A_z = A + z*M*N  (all double2)
+cudaError_t launch_branch_gemm_batched(const double *U, const double *L, int64_t K, int64_t M, int64_t N,
+                                       double *A, int64_t batch, cudaStream_t s);
+// dst[rowmap[r], :] = src[r, :] converted to double2 (src of the ctx precision)
+cudaError_t launch_permute_rows(const void *src, bool c128, const uint32_t *rowmap, int64_t nrows, int64_t ncols,
+                                double *dst, cudaStream_t s);
 // p[i] = fma(re, re, im*im)
 cudaError_t launch_abs2(const double *A, int64_t n, double *p, cudaStream_t s);
 // C[i, :] = sequential inclusive prefix of p[i, :]; r[i] = C[i, N-1]

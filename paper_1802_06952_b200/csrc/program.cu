@@ -69,7 +69,7 @@ Diag HalfProgram::fork_diag(int level, uint64_t child) const {
   const Level &L = levels[level];
   for (int j = 0; j < L.k; ++j) {
     const int bit = (int)((child >> (L.k - 1 - j)) & 1u);
-    if (upper)
+    if ((L.pmask >> j) & 1u)
       d.add_proj(L.cut_bits[j], bit);
     else if (bit)
       d.add_Z(L.cut_bits[j]);
@@ -206,12 +206,27 @@ HalfProgram compile_half(const Circuit &c, bool upper, const std::vector<int> &p
 
 HalfProgram compile_half_layers(const Circuit &c, bool upper, const std::vector<std::vector<int>> &layer_perm,
                                 const std::vector<int> &final_perm) {
+  std::vector<PartCut> cuts;
+  for (const qsim_cut &cut : c.cuts) cuts.push_back(PartCut{(int)cut.layer, upper ? cut.q_upper : cut.q_lower, upper});
+  return compile_part(c, upper ? 0 : c.h_u, upper ? c.h_u : c.n, upper, cuts, layer_perm, final_perm);
+}
+
+HalfProgram compile_part(const Circuit &c, uint32_t lo, uint32_t hi, bool upper, const std::vector<PartCut> &cuts,
+                         const std::vector<std::vector<int>> &layer_perm, const std::vector<int> &final_perm) {
   HalfProgram hp;
   hp.upper = upper;
-  hp.h = (int)(upper ? c.h_u : c.h_l);
+  hp.h = (int)(hi - lo);
   hp.hl = hp.h;
   hp.perm = final_perm;
-  const uint32_t lo = upper ? 0 : c.h_u, hi = upper ? c.h_u : c.n;
+  hp.ncuts = (int)cuts.size();
+  std::vector<int> fork_layers, fork_k;
+  for (const PartCut &cut : cuts) {
+    if (fork_layers.empty() || fork_layers.back() != cut.layer) {
+      fork_layers.push_back(cut.layer);
+      fork_k.push_back(0);
+    }
+    fork_k.back()++;
+  }
   auto bit_at = [&](uint32_t q, int layer) { return layer_perm[layer][hp.h - 1 - (int)(q - lo)]; };
 
   std::vector<LayerSpec> layers(c.depth + 1);
@@ -239,24 +254,25 @@ HalfProgram compile_half_layers(const Circuit &c, bool upper, const std::vector<
     L.diag.nhalf += (int)L.gates.size();
   }
 
-  const int F = (int)c.fork_layers.size();
+  const int F = (int)fork_layers.size();
   hp.levels.resize(F + 1);
   int g0 = 0;
   for (int l = 0; l <= F; ++l) {
     Level &lev = hp.levels[l];
     if (l > 0) {
-      lev.fork_layer = c.fork_layers[l - 1];
-      lev.k = c.fork_k[l - 1];
+      lev.fork_layer = fork_layers[l - 1];
+      lev.k = fork_k[l - 1];
       lev.g0 = g0;
       for (int j = 0; j < lev.k; ++j) {
-        const qsim_cut &cut = c.cuts[g0 + j];
+        const PartCut &cut = cuts[g0 + j];
         // the fork acts on the child level's input: the layout of its first layer
-        lev.cut_bits.push_back(bit_at(upper ? cut.q_upper : cut.q_lower, lev.fork_layer + 1));
+        lev.cut_bits.push_back(bit_at(cut.q, lev.fork_layer + 1));
+        if (cut.proj) lev.pmask |= 1u << j;
       }
       g0 += lev.k;
     }
-    const int first = (l == 0) ? 1 : c.fork_layers[l - 1] + 1;
-    const int last = (l < F) ? c.fork_layers[l] : (int)c.depth;
+    const int first = (l == 0) ? 1 : fork_layers[l - 1] + 1;
+    const int last = (l < F) ? fork_layers[l] : (int)c.depth;
     Diag pending;
     if (l == 0) pending.nhalf = hp.h;  // H^{(x)h}|0> = 2^{-h/2} everywhere (layer 0)
     for (int t = first; t <= last; ++t) {

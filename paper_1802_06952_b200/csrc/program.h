@@ -74,12 +74,14 @@ struct Level {
   int k = 0;                   // cuts at this fork (children = 2^k)
   int g0 = 0;                  // index of the first of them in the cut list
   std::vector<int> cut_bits;   // half-local bit of each cut endpoint in this half
+  uint32_t pmask = 0;          // bit j: cut j acts as P_b on this part (upper endpoint), else Z^b
   std::vector<Sweep> sweeps;
 };
 
 struct HalfProgram {
   bool upper = true;
   int h = 0;
+  int ncuts = 0;  // cut bits of this program's branch index (sum of the levels' k)
   int hl = 0;  // qubits per shard: h, or h - log2(ranks) for a distributed half (f3)
   std::vector<int> perm;  // physical bit of canonical local bit c (h-1-k' for local qubit k'):
                           // the layout of the leaf (and of every sweep unless the layout changes)
@@ -109,6 +111,20 @@ struct Circuit {
 std::string build_circuit(uint32_t rows, uint32_t cols, uint32_t depth, const qsim_gate *gates,
                           size_t n_gates, uint32_t cut_row, const uint32_t *cut_layers,
                           size_t n_cut_layers, Circuit &out);
+
+// A cut endpoint inside one part of a multi-part partition: the cut CZ of
+// `layer` acts on `q` as P_b (proj, the part above the boundary) or Z^b (the part below).
+struct PartCut {
+  int layer;
+  uint32_t q;
+  bool proj;
+};
+
+// Program of the qubit range [lo, hi) whose branch index enumerates `cuts` (ordered by
+// (layer, upper qubit); one fork level per distinct layer).  Halves are the case
+// [0, h_u) with every cut as P and [h_u, n) with every cut as Z.
+HalfProgram compile_part(const Circuit &c, uint32_t lo, uint32_t hi, bool upper, const std::vector<PartCut> &cuts,
+                         const std::vector<std::vector<int>> &layer_perm, const std::vector<int> &final_perm);
 
 // perm: physical bit of each canonical local bit (identity when empty); every bit position of the
 // program (gates, diagonals, forks) is physical.

@@ -176,6 +176,16 @@ qsim_status qsim_cost_model(qsim_ctx *ctx, uint64_t nu, uint64_t nl, double hbm_
   return guard(ctx, [&](qsim::Engine &e) { e.cost_model(nu, nl, hbm_gbps, out); });
 }
 
+qsim_status qsim_multipart_plan(qsim_ctx *ctx, uint32_t n_parts, const uint32_t *row_cuts, uint32_t *part_qubits,
+                                uint32_t *boundary_cuts, double *log2_states) {
+  return guard(ctx, [&](qsim::Engine &e) { e.multipart_plan(n_parts, row_cuts, part_qubits, boundary_cuts, log2_states); });
+}
+
+qsim_status qsim_multipart_amplitudes(qsim_ctx *ctx, uint32_t n_parts, const uint32_t *row_cuts,
+                                      const uint64_t *blocks, const size_t *n_block, void *amps) {
+  return guard(ctx, [&](qsim::Engine &e) { e.multipart_amplitudes(n_parts, row_cuts, blocks, n_block, amps); });
+}
+
 qsim_status qsim_stats(qsim_ctx *ctx, qsim_stats_t *out) {
   return guard(ctx, [&](qsim::Engine &e) {
     if (!out) throw qsim::Error(QSIM_EINVAL, "null output");

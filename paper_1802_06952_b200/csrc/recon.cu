@@ -225,8 +225,10 @@ template <typename R>
 __global__ void __launch_bounds__(256) branch_gemm_kernel(const typename CxT<R>::T *__restrict__ U,
                                                           const typename CxT<R>::T *__restrict__ L,
                                                           int64_t K, int64_t M, int64_t N,
-                                                          double *__restrict__ A) {
+                                                          double *__restrict__ A, int64_t sU, int64_t sA) {
   using C = typename CxT<R>::T;
+  U += (int64_t)blockIdx.z * sU;  // batch z: its own U and A (multi-part contraction), L shared
+  A += (int64_t)blockIdx.z * sA;
   __shared__ double sUr[GB_K][GB_M + GB_PAD], sUi[GB_K][GB_M + GB_PAD];
   __shared__ double sLr[GB_K][GB_N + GB_PAD], sLi[GB_K][GB_N + GB_PAD];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -329,9 +331,48 @@ cudaError_t launch_branch_gemm(const void *U, const void *L, int64_t K, int64_t 
   if (K <= 0 || M <= 0 || N <= 0) return cudaSuccess;
   dim3 grid((unsigned)((N + GB_N - 1) / GB_N), (unsigned)((M + GB_M - 1) / GB_M));
   if (c128)
-    branch_gemm_kernel<double><<<grid, 256, 0, s>>>((const double2 *)U, (const double2 *)L, K, M, N, A);
+    branch_gemm_kernel<double><<<grid, 256, 0, s>>>((const double2 *)U, (const double2 *)L, K, M, N, A, 0, 0);
   else
-    branch_gemm_kernel<float><<<grid, 256, 0, s>>>((const float2 *)U, (const float2 *)L, K, M, N, A);
+    branch_gemm_kernel<float><<<grid, 256, 0, s>>>((const float2 *)U, (const float2 *)L, K, M, N, A, 0, 0);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_branch_gemm_batched(const double *U, const double *L, int64_t K, int64_t M, int64_t N,
+                                       double *A, int64_t batch, cudaStream_t s) {
+  if (K <= 0 || M <= 0 || N <= 0 || batch <= 0) return cudaSuccess;
+  const int64_t sU = 2 * K * M, sA = 2 * M * N;  // in doubles
+  for (int64_t z0 = 0; z0 < batch; z0 += 65535) {
+    dim3 grid((unsigned)((N + GB_N - 1) / GB_N), (unsigned)((M + GB_M - 1) / GB_M),
+              (unsigned)std::min<int64_t>(65535, batch - z0));
+    branch_gemm_kernel<double><<<grid, 256, 0, s>>>((const double2 *)(U + z0 * sU), (const double2 *)L, K, M, N,
+                                                    A + z0 * sA, sU / 2, sA);
+  }
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------- multi-part slices
+// dst[rowmap[r], :] = src[r, :] as double2 (row r of a part's leaf slice in tree order goes to
+// its (beta_{k-1}, beta_k) row of the contraction operand)
+template <typename R>
+__global__ void permute_rows_kernel(const typename CxT<R>::T *__restrict__ src, const uint32_t *__restrict__ rowmap,
+                                    int64_t nrows, int64_t ncols, double2 *__restrict__ dst) {
+  const int64_t total = nrows * ncols;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = e / ncols, j = e - r * ncols;
+    const auto v = src[e];
+    dst[(int64_t)rowmap[r] * ncols + j] = make_double2((double)v.x, (double)v.y);
+  }
+}
+
+cudaError_t launch_permute_rows(const void *src, bool c128, const uint32_t *rowmap, int64_t nrows, int64_t ncols,
+                                double *dst, cudaStream_t s) {
+  const int64_t total = nrows * ncols;
+  if (total <= 0) return cudaSuccess;
+  const int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 16);
+  if (c128)
+    permute_rows_kernel<double><<<blocks, 256, 0, s>>>((const double2 *)src, rowmap, nrows, ncols, (double2 *)dst);
+  else
+    permute_rows_kernel<float><<<blocks, 256, 0, s>>>((const float2 *)src, rowmap, nrows, ncols, (double2 *)dst);
   return cudaGetLastError();
 }
 

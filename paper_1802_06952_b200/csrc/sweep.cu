@@ -305,7 +305,7 @@ __global__ void __launch_bounds__(256) small_kernel(const SmallParams p) {
           for (int j = 0; j < L.k; ++j) {
             const uint32_t cb = (child >> (L.k - 1 - j)) & 1u;
             const uint32_t ib = ((uint32_t)i >> L.cut_bits[j]) & 1u;
-            if (p.upper)
+            if ((L.pmask >> j) & 1u)
               zero |= (ib != cb);
             else
               neg ^= (ib & cb) != 0;
@@ -344,7 +344,7 @@ __global__ void __launch_bounds__(256) small_kernel(const SmallParams p) {
         for (int j = 0; j < L.k; ++j) {
           const uint32_t cb = (child >> (L.k - 1 - j)) & 1u;
           const uint32_t ib = ((uint32_t)i >> L.cut_bits[j]) & 1u;
-          if (p.upper)
+          if ((L.pmask >> j) & 1u)
             zero |= (ib != cb);
           else
             neg ^= (ib & cb) != 0;

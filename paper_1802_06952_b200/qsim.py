@@ -37,7 +37,7 @@ EXPORTED = ["qsim_create", "qsim_destroy", "qsim_last_error", "qsim_version", "q
             "qsim_sample", "qsim_sample_probs", "qsim_branch_sum", "qsim_branch_state",
             "qsim_nccl_unique_id", "qsim_comm_init", "qsim_rank_range", "qsim_stats",
             "qsim_stats_reset", "qsim_synchronize", "qsim_eq2_time", "qsim_cost_model",
-            "qsim_porter_thomas"]
+            "qsim_porter_thomas", "qsim_multipart_plan", "qsim_multipart_amplitudes"]
 
 
 class qsim_cut(C.Structure):
@@ -80,6 +80,8 @@ _sig = {
                                      C.POINTER(qsim_pt_t)]),
     "qsim_eq2_time": (C.c_int, [_P, C.c_size_t, C.c_double, C.c_double, C.c_double, C.POINTER(C.c_double)]),
     "qsim_cost_model": (C.c_int, [_P, C.c_uint64, C.c_uint64, C.c_double, _P]),
+    "qsim_multipart_plan": (C.c_int, [_P, C.c_uint32, _P, _P, _P, C.POINTER(C.c_double)]),
+    "qsim_multipart_amplitudes": (C.c_int, [_P, C.c_uint32, _P, _P, _P, _P]),
     "qsim_create": (C.c_int, [C.POINTER(_P), C.c_int, C.c_int]),
     "qsim_destroy": (None, [_P]),
     "qsim_last_error": (C.c_char_p, [_P]),
@@ -282,6 +284,31 @@ def qsim_cost_model(ctx, n_upper: int, n_lower: int, hbm_gbps: float) -> dict:
     c = qsim_cost_t()
     _check(ctx, _lib.qsim_cost_model(ctx, n_upper, n_lower, hbm_gbps, C.byref(c)))
     return c.as_dict()
+
+
+def qsim_multipart_plan(ctx, row_cuts) -> dict:
+    """Parts (bands of rows split at ``row_cuts``) of the loaded circuit: qubits per part, cuts per
+    boundary, log2 of the leaf amplitudes evolved (include/qsim.h)."""
+    rc = np.ascontiguousarray(np.asarray(row_cuts, dtype=np.uint32))
+    t = rc.size + 1
+    pq = np.zeros(t, dtype=np.uint32)
+    bc = np.zeros(max(t - 1, 1), dtype=np.uint32)
+    l2 = C.c_double()
+    _check(ctx, _lib.qsim_multipart_plan(ctx, t, _ptr(rc), _ptr(pq), _ptr(bc), C.byref(l2)))
+    return {"part_qubits": pq.tolist(), "boundary_cuts": bc[:t - 1].tolist(), "log2_states": l2.value}
+
+
+def qsim_multipart_amplitudes(ctx, row_cuts, blocks, prec: int) -> np.ndarray:
+    """amps[i_0, ..., i_{t-1}] = sum_b prod_k psi^k_b[S_k[i_k]] for the blocks S_k (one per part)."""
+    rc = np.ascontiguousarray(np.asarray(row_cuts, dtype=np.uint32))
+    bl = [_u64(b) for b in blocks]
+    if len(bl) != rc.size + 1:
+        raise ValueError(f"{rc.size} row cuts make {rc.size + 1} parts; got {len(bl)} blocks")
+    cat = np.ascontiguousarray(np.concatenate(bl)) if bl else np.zeros(0, dtype=np.uint64)
+    nb = np.asarray([b.size for b in bl], dtype=np.uint64)
+    out = np.zeros(tuple(b.size for b in bl), dtype=np.complex128 if prec == QSIM_C128 else np.complex64)
+    _check(ctx, _lib.qsim_multipart_amplitudes(ctx, len(bl), _ptr(rc), _ptr(cat), _ptr(nb), _ptr(out)))
+    return out
 
 
 def qsim_stats(ctx) -> dict:

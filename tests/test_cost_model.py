@@ -108,3 +108,44 @@ def test_cost_model_errors():
             Q.qsim_cost_model(ctx, 1, 1, 0.0)
     finally:
         Q.qsim_destroy(ctx)
+
+
+# ---------------------------------------------------------------- multi-part partitions (f4)
+@pytest.mark.parametrize("grid,depth,row_cuts", [
+    ((8, 8), 8, [3, 5]), ((8, 8), 8, [2, 4, 6]), ((8, 8), 22, [2, 4, 6]), ((8, 8), 22, [4]),
+    ((8, 7), 12, [1, 4]), ((6, 2), 16, [1, 3]), ((5, 3), 12, [1, 2, 4]),
+])
+def test_multipart_plan_matches_oracle(grid, depth, row_cuts):
+    """qsim_multipart_plan's parts and per-boundary cut counts are the oracle's (oracle.multipart)."""
+    from oracle import multipart as MP
+    circ = generate(*grid, depth, 0)
+    bounds = MP.full_bounds(circ, row_cuts)
+    cuts = MP.cut_list(circ, bounds)
+    ctx = Q.qsim_create(Q.QSIM_C64, 0)
+    try:
+        Q.qsim_load_circuit(ctx, *grid, depth, circ.gate_array())
+        p = Q.qsim_multipart_plan(ctx, row_cuts)
+    finally:
+        Q.qsim_destroy(ctx)
+    t = len(bounds) - 1
+    assert p["part_qubits"] == [(bounds[k + 1] - bounds[k]) * grid[1] for k in range(t)]
+    c = [sum(1 for cu in cuts if cu[3] == j) for j in range(t - 1)]
+    assert p["boundary_cuts"] == c
+    cc = [0] + c + [0]
+    states = sum(2.0 ** (p["part_qubits"][k] + cc[k] + cc[k + 1]) for k in range(t))
+    assert p["log2_states"] == pytest.approx(math.log2(states), abs=1e-12)
+
+
+def test_multipart_plan_fig3_anchor():
+    """Fig. 3 caption: the 64-qubit bipartition at depth 22 'is equivalent to a 49-qubit
+    circuit' — 2 halves x 2^16 copies x 2^32 amplitudes = 2^49 through the multi-part planner."""
+    circ = generate(8, 8, 22, 0)
+    ctx = Q.qsim_create(Q.QSIM_C64, 0)
+    try:
+        Q.qsim_load_circuit(ctx, 8, 8, 22, circ.gate_array())
+        assert Q.qsim_multipart_plan(ctx, [4])["log2_states"] == pytest.approx(49.0, abs=1e-12)
+        for bad in ([0], [8], [5, 3], [1, 2, 3, 4, 5, 6, 7, 7]):
+            with pytest.raises(Q.QsimError):
+                Q.qsim_multipart_plan(ctx, bad)
+    finally:
+        Q.qsim_destroy(ctx)
