@@ -98,7 +98,12 @@ typedef enum {
                                 global qubit is preceded by a local/global qubit swap fused into the
                                 previous sweep (its tiles are stored straight into the peer's HBM over
                                 NVLink); sampled slices are summed over the ranks before the GEMM.
-                                Needs >= tile bits + 2 qubits per shard; lazy tail off. 0: default */
+                                Needs >= tile bits + 2 qubits per shard; lazy tail off. 0: default */,
+  QSIM_OPT_BFS = 8           /* multi-part partitions (qsim_multipart_amplitudes): 1 (default) runs a
+                                part's branch tree level by level when two consecutive levels fit in
+                                device memory, each sweep as ONE node-batched launch over every state of
+                                the level (the fork's P / Z applied per node in the sweep); 0: the
+                                depth-first executor of the halves (one launch per node and sweep)   */
 } qsim_option;
 
 /* Create a context bound to CUDA device `device` (no device call is made until the

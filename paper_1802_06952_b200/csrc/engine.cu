@@ -208,6 +208,10 @@ void Engine::set_option(int key, int64_t value) {
       if (have_circuit_) compile_all();
       have_blocks_ = false;  // the sampled indices are relabelled per layout
       return;
+    case QSIM_OPT_BFS:
+      if (value < 0 || value > 1) throw Error(QSIM_EINVAL, "QSIM_OPT_BFS must be 0 or 1");
+      bfs_ = value != 0;
+      return;
     case QSIM_OPT_SWEEP_KERNEL:
       if (value < 0 || value > 3) throw Error(QSIM_EINVAL, "QSIM_OPT_SWEEP_KERNEL must be 0, 1, 2 or 3");
       sweep_kernel_ = (int)value;
@@ -1720,6 +1724,121 @@ void Engine::synchronize() {
   check(cudaStreamSynchronize(stream_), "cudaStreamSynchronize");
 }
 
+// ---------------------------------------------------------------- level-synchronous tree (BFS)
+// Node-batched launch of one planned sweep over 2^log2_nodes states (TMA kernel only).
+void Engine::launch_nodes(const TilePlan &tp, const void *src, void *dst, int log2_nodes, int shift,
+                          const ForkDev &fork, const HalfProgram &hp) {
+  if (tp.fused || tp.gen || !tp.swaps.empty()) throw Error(QSIM_EINVAL, "node-batched sweep of an unsupported plan");
+  const int h = hp.hl;
+  int pre_mode = 0;
+  Diag pre;
+  if (tp.use_pre) {
+    pre = tp.pre;
+    if (!pre.identity()) pre_mode = 1;
+  }
+  const bool timed = time_sweeps_;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (timed) {
+    e0 = get_event();
+    e1 = get_event();
+    check(cudaEventRecord(e0, stream_), "cudaEventRecord");
+  }
+  TileSweepParams p = tp.p;
+  p.pre = to_dev(pre, pre_mode != 0);
+  p.njobs = 1;
+  p.src[0] = src;
+  p.dst[0] = dst;
+  p.job_pv[0] = p.pre.pv;
+  p.job_zm[0] = p.pre.zm;
+  p.log2_nodes = log2_nodes;
+  p.node_src_shift = shift;
+  p.node_stride = (uint64_t)1 << h;
+  p.fork = fork;
+  if (pre_mode == 1) p.pre_s = make_split(pre, reg_positions(p, 0, c128_));
+  const uint64_t tiles = 1ull << (p.log2_ntiles + log2_nodes);
+  const int grid = (int)std::min<uint64_t>(tiles, (uint64_t)num_sms_);
+  const int stages = sweep_kernel_ == 2 ? 2 : sweep_kernel_ == 3 ? 3 : tma_stages(tp);
+  check(launch_tile_sweep_tma(p, c128_, pre_mode, tp.npass, grid, stream_, stages), "node-batched sweep launch");
+  if (timed) {
+    check(cudaEventRecord(e1, stream_), "cudaEventRecord");
+    ev_sweep_.emplace_back(e0, e1);
+    if (ev_sweep_.size() > 8192) resolve_events();
+  }
+  const double nodes = std::ldexp(1.0, log2_nodes);
+  st_.kernel_launches++;
+  st_.sweeps++;
+  st_.sweep_states += (uint64_t)nodes;
+  st_.layers_applied += (uint64_t)tp.layers * (uint64_t)nodes;
+  st_.sweep_bytes += 2.0 * nodes * std::ldexp(1.0, h) * (double)amp_;
+}
+
+static ForkDev fork_dev(const Level &lev) {
+  ForkDev f;
+  std::memset(&f, 0, sizeof(f));
+  f.n = lev.k;
+  f.pmask = lev.pmask;
+  for (int j = 0; j < lev.k; ++j) f.bit[j] = (uint8_t)lev.cut_bits[j];
+  return f;
+}
+
+bool Engine::bfs_fits(int half) const {
+  const HalfExec &he = half_[half];
+  const HalfProgram &hp = he.prog;
+  if (!bfs_ || dist_ || fuse_layers_ || sweep_kernel_ == 1 || !he.tree || he.plans.empty()) return false;
+  if (hp.ncuts > 40) return false;
+  const int F = (int)hp.levels.size() - 1;
+  for (int l = 1; l <= F; ++l) {
+    if (l < F && he.plans[l][0].empty()) return false;  // only the leaf level may defer its fork
+    for (const TilePlan &tp : he.plans[l][0])
+      if (tp.fused || tp.gen) return false;
+  }
+  size_t free_b = 0, total_b = 0;
+  if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) return false;
+  size_t have = bfs_buf_[0].bytes + bfs_buf_[1].bytes;
+  for (auto *b : states_) have += b->bytes;
+  const double need = 2.0 * std::ldexp(1.0, hp.ncuts + hp.h) * (double)amp_;
+  return need + (double)(1u << 30) < (double)(free_b + have);
+}
+
+// Every level l: its first sweep reads the parents (node >> k_l) and applies the fork per node,
+// the others run in place; the leaves are gathered in one launch.
+void Engine::evolve_half_bfs(int half, void *slice, const uint64_t *dS, int64_t nS) {
+  HalfExec &he = half_[half];
+  const HalfProgram &hp = he.prog;
+  const int F = (int)hp.levels.size() - 1;
+  const size_t node_bytes = ((size_t)1 << hp.h) * amp_;
+  // the two buffers alternate by level; the last level is the largest
+  for (auto *b : states_) b->release();
+  bfs_buf_[F & 1].reserve(node_bytes << hp.ncuts);
+  bfs_buf_[(F & 1) ^ 1].reserve(node_bytes << std::max(0, hp.ncuts - (F >= 1 ? hp.levels[F].k : 0)));
+  run_level(half, 0, 0, nullptr, bfs_buf_[0].ptr, 0);
+  int sb = 0;
+  for (int l = 1; l <= F; ++l) {
+    const Level &lev = hp.levels[l];
+    const auto &launches = he.plans[l][0];
+    if (launches.empty()) break;  // a fork at the last layer: applied in the gather
+    sb += lev.k;
+    const void *src = bfs_buf_[(l - 1) & 1].ptr;
+    void *dst = bfs_buf_[l & 1].ptr;
+    for (size_t i = 0; i < launches.size(); ++i) {
+      ForkDev f;
+      std::memset(&f, 0, sizeof(f));
+      if (i == 0) f = fork_dev(lev);
+      launch_nodes(launches[i], i == 0 ? src : dst, dst, sb, i == 0 ? lev.k : 0, f, hp);
+    }
+  }
+  // leaves: the last level's states, or its parents with the pending fork
+  const bool pending = F >= 1 && he.plans[F][0].empty();
+  const int lastbuf = pending ? (F - 1) & 1 : F & 1;
+  ForkDev f;
+  std::memset(&f, 0, sizeof(f));
+  if (pending) f = fork_dev(hp.levels[F]);
+  check(launch_gather_nodes(bfs_buf_[lastbuf].ptr, (uint64_t)1 << hp.h, pending ? hp.levels[F].k : 0,
+                            (int64_t)1 << hp.ncuts, dS, nS, slice, f, c128_, stream_),
+        "gather nodes launch");
+  st_.kernel_launches++;
+}
+
 // ---------------------------------------------------------------- multi-part partitions (f4)
 // SURVEY §8(f) f4; PAPER.md P:114 ("dividing the circuit into three or four parts is more
 // effective if the circuit depth is small") and Fig. 3.  Parts are bands of rows
@@ -1862,7 +1981,10 @@ void Engine::multipart_amplitudes(uint32_t t, const uint32_t *row_cuts, const ui
     slice.reserve((size_t)nrows * ns[k] * amp_);
     check(cudaMemcpyAsync(dS.ptr, P.data(), P.size() * 8, cudaMemcpyHostToDevice, stream_), "upload part block");
     check(cudaMemcpyAsync(rowmap.ptr, rm.data(), rm.size() * 4, cudaMemcpyHostToDevice, stream_), "upload rowmap");
-    evolve_half(hidx, 0, (uint64_t)nrows, slice.ptr, dS.as<uint64_t>(), ns[k]);
+    if (bfs_fits(hidx))
+      evolve_half_bfs(hidx, slice.ptr, dS.as<uint64_t>(), ns[k]);
+    else
+      evolve_half(hidx, 0, (uint64_t)nrows, slice.ptr, dS.as<uint64_t>(), ns[k]);
     X[k].reset(new DevBuf());
     X[k]->reserve((size_t)nrows * ns[k] * 16);
     check(launch_permute_rows(slice.ptr, c128_, rowmap.as<uint32_t>(), nrows, ns[k], X[k]->as<double>(), stream_),

@@ -133,6 +133,7 @@ class Engine {
   std::vector<void *> ipc_opened_;
   size_t dist_bytes_ = 0;
   DevBuf dbar_;
+  DevBuf bfs_buf_[2];
 
   bool have_circuit_ = false;
   Circuit circ_;
@@ -181,6 +182,13 @@ class Engine {
 
   // executor
   void evolve_half(int half, uint64_t b0, uint64_t b1, void *slice, const uint64_t *dS, int64_t nS);
+  // level-synchronous (BFS) variant for a whole tree whose two largest consecutive levels fit:
+  // every sweep of level l runs once over all 2^{sbits_l} node states (node-batched TMA launch)
+  bool bfs_fits(int half) const;
+  void evolve_half_bfs(int half, void *slice, const uint64_t *dS, int64_t nS);
+  void launch_nodes(const TilePlan &tp, const void *src, void *dst, int log2_nodes, int shift, const ForkDev &fork,
+                    const HalfProgram &hp);
+  bool bfs_ = true;  // QSIM_OPT_BFS (multi-part parts)
   const void *run_level(int half, int level, uint64_t child, const void *src, void *dst, int skip);
   int lazy_depth(int half, int64_t nS) const;
   int tma_stages(const TilePlan &tp) const;

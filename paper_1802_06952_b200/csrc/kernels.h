@@ -49,6 +49,15 @@ struct DiagSplit {
   int32_t has_proj;   // any projector at all (else the zeroing is skipped)
 };
 
+// Fork of a branch-tree level applied per node of a node-batched launch (multi-part BFS
+// levels): node index = (parent << n) | child; cut j (child bit n-1-j) at local bit bit[j]
+// is P_b (zero where the bit != b) when pmask bit j is set, else Z^b (negate where bit & b).
+struct ForkDev {
+  int32_t n;
+  uint32_t pmask;
+  uint8_t bit[32];
+};
+
 struct TileSweepParams {
   const void *src[kMaxJobs];
   void *dst[kMaxJobs];
@@ -78,6 +87,13 @@ struct TileSweepParams {
   int32_t nswap;
   uint8_t swap_l[2], swap_j[2];
   void *peer[4];
+  // node batching (TMA sweep only): 2^log2_nodes states of node_stride amplitudes, tile index
+  // t = (node << log2_ntiles) | tile; node reads state node >> node_src_shift of src[0] (the
+  // parent of a fork child) and writes state node of dst[0]; fork applied per node at pass 0
+  int32_t log2_nodes;
+  int32_t node_src_shift;
+  uint64_t node_stride;
+  ForkDev fork;
 };
 
 // pre_mode: 0 none, 1 apply pre diagonal to loaded values, 2 generate (no load)
@@ -174,6 +190,9 @@ cudaError_t launch_gather(const void *psi, const uint64_t *S, int64_t n, void *o
                           const DiagDev &pend, bool c128, cudaStream_t s, uint64_t lmask = ~0ull,
                           uint64_t gsel = 0);
 
+// Leaves of a node-batched level: out[node * n + j] = fork(node, S[j]) * psi[(node >> shift) * stride + S[j]]
+cudaError_t launch_gather_nodes(const void *psi, uint64_t stride, int shift, int64_t nnodes, const uint64_t *S,
+                                int64_t n, void *out, const ForkDev &fork, bool c128, cudaStream_t s);
 // Lazy last layer: the leaf's final sweep evaluated only at the sampled indices,
 //   out[j] = post(x) * sum_y  prod_t M'_t[x_t, y_t] * pre(y) * psi[y],   x = S[j],
 // y ranging over the 2^k values of the sweep's target bits (others equal to x).

@@ -62,6 +62,48 @@ cudaError_t launch_gather(const void *psi, const uint64_t *S, int64_t n, void *o
   return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------- node-batched leaves
+template <typename R>
+__global__ void gather_nodes_kernel(const typename CxT<R>::T *__restrict__ psi, uint64_t stride, int shift,
+                                    int64_t nnodes, const uint64_t *__restrict__ S, int64_t n,
+                                    typename CxT<R>::T *__restrict__ out, const __grid_constant__ ForkDev f) {
+  using C = typename CxT<R>::T;
+  const int64_t total = nnodes * n;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t node = e / n;
+    const uint64_t x = S[e - node * n];
+    C v = psi[(uint64_t)(node >> shift) * stride + x];
+    bool zero = false, neg = false;
+    for (int j = 0; j < f.n; ++j) {
+      const uint64_t cb = ((uint64_t)node >> (f.n - 1 - j)) & 1u, xb = (x >> f.bit[j]) & 1u;
+      if ((f.pmask >> j) & 1u)
+        zero |= xb != cb;
+      else
+        neg ^= (xb & cb) != 0;
+    }
+    if (zero) v.x = v.y = (R)0;
+    if (neg) {
+      v.x = -v.x;
+      v.y = -v.y;
+    }
+    out[e] = v;
+  }
+}
+
+cudaError_t launch_gather_nodes(const void *psi, uint64_t stride, int shift, int64_t nnodes, const uint64_t *S,
+                                int64_t n, void *out, const ForkDev &fork, bool c128, cudaStream_t s) {
+  const int64_t total = nnodes * n;
+  if (total <= 0) return cudaSuccess;
+  const int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 16);
+  if (c128)
+    gather_nodes_kernel<double><<<blocks, 256, 0, s>>>((const double2 *)psi, stride, shift, nnodes, S, n,
+                                                       (double2 *)out, fork);
+  else
+    gather_nodes_kernel<float><<<blocks, 256, 0, s>>>((const float2 *)psi, stride, shift, nnodes, S, n,
+                                                      (float2 *)out, fork);
+  return cudaGetLastError();
+}
+
 // ---------------------------------------------------------------- lazy last layer
 // One warp per sampled index x: lanes split the 2^k input combinations y, each term is
 // w^{ph(x,y)} pre(y) psi[y] with ph = 6 popc((x^y) & SX) + 4 popc(~x & y & SY) (the

@@ -187,6 +187,58 @@ __device__ __forceinline__ void low_gates(typename Cx2<R>::T (&v)[16][NV], const
   }
 }
 
+// per-node fork factor (node-batched launches, kernels.h ForkDev) on the pass-0 registers.
+// Element (s, e) has index tg | slot bits of s | e (c64: e = bit 0); the fork's zero / sign
+// conditions are folded into two 32-bit masks over idx = (s << VB) | e, as in apply_split.
+// fork_masks runs before the tile's values are live (register pressure), apply_fork after
+template <int NV>
+__device__ __forceinline__ void fork_masks(const uint32_t tg, const uint64_t node, const TileSweepParams &p,
+                                           uint32_t &zero, uint32_t &neg) {
+  constexpr int VB = NV == 2 ? 1 : 0;
+  constexpr uint32_t pat[5] = {0xAAAAAAAAu, 0xCCCCCCCCu, 0xF0F0F0F0u, 0xFF00FF00u, 0xFFFF0000u};
+  uint32_t fm = 0, fv = 0, zm = 0;
+  for (int j = 0; j < p.fork.n; ++j) {
+    const uint32_t cb = (uint32_t)(node >> (p.fork.n - 1 - j)) & 1u;
+    const uint32_t m = 1u << p.fork.bit[j];
+    if ((p.fork.pmask >> j) & 1u)
+      fm |= m, fv |= cb ? m : 0u;
+    else if (cb)
+      zm |= m;
+  }
+  uint32_t sb[VB + 4];  // state bit of index bit j
+  if (VB) sb[0] = 1u;
+#pragma unroll
+  for (int kk = 0; kk < 4; ++kk) sb[VB + kk] = 1u << p.hb[p.gsel[0][kk]];
+  uint32_t smask = 0;
+#pragma unroll
+  for (int j = 0; j < VB + 4; ++j) smask |= sb[j];
+  zero = (((tg & fm) ^ fv) & ~smask) ? 0xFFFFFFFFu : 0u;
+  neg = (__popc(tg & zm & ~smask) & 1) ? 0xFFFFFFFFu : 0u;
+#pragma unroll
+  for (int j = 0; j < VB + 4; ++j) {
+    if (fm & sb[j]) zero |= (fv & sb[j]) ? ~pat[j] : pat[j];
+    if (zm & sb[j]) neg ^= pat[j];
+  }
+}
+
+template <typename R, int NV>
+__device__ __forceinline__ void apply_fork(typename Cx2<R>::T (&v)[16][NV], const uint32_t zero, const uint32_t neg) {
+  constexpr int VB = NV == 2 ? 1 : 0;
+  if (!(zero | neg)) return;
+#pragma unroll
+  for (int s = 0; s < 16; ++s)
+#pragma unroll
+    for (int e = 0; e < NV; ++e) {
+      const int idx = (s << VB) | e;
+      if ((zero >> idx) & 1u) {
+        v[s][e].x = v[s][e].y = (R)0;
+      } else if ((neg >> idx) & 1u) {
+        v[s][e].x = -v[s][e].x;
+        v[s][e].y = -v[s][e].y;
+      }
+    }
+}
+
 // shared-memory slot index of register slot r for pass q (incrementally OR-ed)
 __device__ __forceinline__ uint32_t slot_smem(uint32_t base, const uint8_t *gsel, int r) {
   uint32_t si = base;
@@ -197,7 +249,8 @@ __device__ __forceinline__ uint32_t slot_smem(uint32_t base, const uint8_t *gsel
 }
 
 // SW = 1: the distributed-half variant whose stores implement a local / global bit swap (p.nswap)
-template <typename R, int PRE, int NPASS, int NST, int SW = 0>
+// NB = 1: the node-batched variant (p.log2_nodes, p.node_*, p.fork; multi-part BFS levels)
+template <typename R, int PRE, int NPASS, int NST, int SW = 0, int NB = 0>
 __global__ void __launch_bounds__(544, 1) tile_sweep_tma_kernel(const __grid_constant__ TileSweepParams p) {
   using C = typename Cx2<R>::T;
   using V = typename Cx2<R>::V;
@@ -230,9 +283,10 @@ __global__ void __launch_bounds__(544, 1) tile_sweep_tma_kernel(const __grid_con
   }
   __syncthreads();
 
-  const uint64_t ntiles = 1ull << p.log2_ntiles;
+  const uint64_t ntiles = 1ull << (p.log2_ntiles + (NB ? p.log2_nodes : 0));
+  const uint64_t tmask = (1ull << p.log2_ntiles) - 1ull;
   auto tile_outer = [&](uint64_t t64) {
-    uint32_t t = (uint32_t)t64, outer = 0;
+    uint32_t t = (uint32_t)(NB ? (t64 & tmask) : t64), outer = 0;
     for (int q = 0; q < p.nruns; ++q) {
       outer |= (t & ((1u << p.run_len[q]) - 1u)) << p.run_start[q];
       t >>= p.run_len[q];
@@ -247,7 +301,7 @@ __global__ void __launch_bounds__(544, 1) tile_sweep_tma_kernel(const __grid_con
     const int nruns = 1 << rbits;
     const uint32_t run_log2 = L + m;
     const uint32_t run_bytes = (uint32_t)sizeof(C) << run_log2;
-    const char *src = reinterpret_cast<const char *>(p.src[0]);
+    const char *srcb = reinterpret_cast<const char *>(p.src[0]);
     for (int it = 0;; ++it) {
       const uint64_t t = blockIdx.x + (uint64_t)it * gridDim.x;
       if (t >= ntiles) break;
@@ -256,6 +310,8 @@ __global__ void __launch_bounds__(544, 1) tile_sweep_tma_kernel(const __grid_con
       mbar_wait(&empty_bar[s], par ^ 1u);
       uint64_t *fb = &full_bar[s][it & 1];
       const uint32_t outer = tile_outer(t);
+      const char *src = srcb;
+      if constexpr (NB == 1) src += (size_t)(((t >> p.log2_ntiles) >> p.node_src_shift) * p.node_stride) * sizeof(C);
       char *stage = reinterpret_cast<char *>(stages + (size_t)s * NVEC);
       if (bulk) {
         if (lane == 0) mbar_arrive_expect_tx(fb, kTileBytes);
@@ -302,7 +358,7 @@ __global__ void __launch_bounds__(544, 1) tile_sweep_tma_kernel(const __grid_con
     // (2k + grp mod 3), so the k-th tile is the (k / 3)-th use of its stage
     const uint32_t use = NST == 2 ? (uint32_t)k : (uint32_t)(k / 3);
     // B-phases of the pre (pass-0 thread base, bits 0-2) and post (last pass, bits 3-5) diagonals
-    uint32_t phB = 0;
+    uint32_t phB = 0, fzero = 0, fneg = 0;
     {
       uint32_t b0 = outer | ((uint32_t)lane << VB) | p.gbase, b1 = b0;
 #pragma unroll
@@ -313,6 +369,8 @@ __global__ void __launch_bounds__(544, 1) tile_sweep_tma_kernel(const __grid_con
         }
       if constexpr (PRE == 1) phB = (uint32_t)diag_phase_b(b0, p.pre) & 7u;
       if (p.post.active) phB |= ((uint32_t)diag_phase_b(b1, p.post) & 7u) << 3;
+      if constexpr (NB == 1)
+        if (p.fork.n) fork_masks<NV>(b0 & ~p.gbase, t >> p.log2_ntiles, p, fzero, fneg);
     }
     mbar_wait(&full_bar[s][grp], use & 1u);
 
@@ -326,6 +384,8 @@ __global__ void __launch_bounds__(544, 1) tile_sweep_tma_kernel(const __grid_con
       }
 #pragma unroll
     for (int r = 0; r < 16; ++r) unpack<R, NV>(tile[slot_smem(ts, p.gsel[0], r)], v[r]);
+    if constexpr (NB == 1)
+      if (p.fork.n) apply_fork<R, NV>(v, fzero, fneg);
     if constexpr (PRE == 1) apply_split<R, NV>(v, tg | p.gbase, phB & 7u, p.pre_s, tab_pre);
     low_gates<R, NV>(v, p, lane);
     reg_gates<R, NV>(v, p.gkind[0]);
@@ -354,6 +414,7 @@ __global__ void __launch_bounds__(544, 1) tile_sweep_tma_kernel(const __grid_con
     constexpr int QL = NPASS - 1;
     if (p.post.active) apply_split<R, NV>(v, tg | p.gbase, phB >> 3, p.post_s, tab_post);
     V *dbase = dst;
+    if constexpr (NB == 1) dbase += ((t >> p.log2_ntiles) * p.node_stride) >> VB;
     if constexpr (SW == 1) {  // distributed half: this tile's destination rank and address (kernels.h)
       uint32_t delta = 0;
 #pragma unroll
@@ -377,21 +438,28 @@ __global__ void __launch_bounds__(544, 1) tile_sweep_tma_kernel(const __grid_con
   }
 }
 
-template <typename R, int PRE, int NPASS, int NST, int SW = 0>
+template <typename R, int PRE, int NPASS, int NST, int SW = 0, int NB = 0>
 static cudaError_t launch_tma_t(const TileSweepParams &p, int grid, cudaStream_t s) {
-  tile_sweep_tma_kernel<R, PRE, NPASS, NST, SW><<<grid, 544, (size_t)NST * kTileBytes, s>>>(p);
+  tile_sweep_tma_kernel<R, PRE, NPASS, NST, SW, NB><<<grid, 544, (size_t)NST * kTileBytes, s>>>(p);
   return cudaGetLastError();
 }
 
-template <typename R, int NST, int SW = 0>
+template <typename R, int NST, int SW = 0, int NB = 0>
 static cudaError_t launch_tma_r(const TileSweepParams &p, int pre_mode, int npass, int grid, cudaStream_t s) {
   if (npass == 1)
-    return pre_mode ? launch_tma_t<R, 1, 1, NST, SW>(p, grid, s) : launch_tma_t<R, 0, 1, NST, SW>(p, grid, s);
-  return pre_mode ? launch_tma_t<R, 1, 2, NST, SW>(p, grid, s) : launch_tma_t<R, 0, 2, NST, SW>(p, grid, s);
+    return pre_mode ? launch_tma_t<R, 1, 1, NST, SW, NB>(p, grid, s) : launch_tma_t<R, 0, 1, NST, SW, NB>(p, grid, s);
+  return pre_mode ? launch_tma_t<R, 1, 2, NST, SW, NB>(p, grid, s) : launch_tma_t<R, 0, 2, NST, SW, NB>(p, grid, s);
 }
 
 cudaError_t launch_tile_sweep_tma(const TileSweepParams &p, bool c128, int pre_mode, int npass, int grid,
                                   cudaStream_t s, int stages) {
+  if (p.log2_nodes > 0 || p.fork.n > 0) {  // node-batched (multi-part BFS levels)
+    if (stages == 3)
+      return c128 ? launch_tma_r<double, 3, 0, 1>(p, pre_mode, npass, grid, s)
+                  : launch_tma_r<float, 3, 0, 1>(p, pre_mode, npass, grid, s);
+    return c128 ? launch_tma_r<double, 2, 0, 1>(p, pre_mode, npass, grid, s)
+                : launch_tma_r<float, 2, 0, 1>(p, pre_mode, npass, grid, s);
+  }
   if (p.nswap)  // distributed-half swap sweeps: two stages
     return c128 ? launch_tma_r<double, 2, 1>(p, pre_mode, npass, grid, s)
                 : launch_tma_r<float, 2, 1>(p, pre_mode, npass, grid, s);
@@ -402,13 +470,13 @@ cudaError_t launch_tile_sweep_tma(const TileSweepParams &p, bool c128, int pre_m
               : launch_tma_r<float, 2>(p, pre_mode, npass, grid, s);
 }
 
-template <typename R, int NST, int SW = 0>
+template <typename R, int NST, int SW = 0, int NB = 0>
 static cudaError_t tma_setup_r() {
   const int bytes = NST * kTileBytes;
-  const void *fns[4] = {(const void *)tile_sweep_tma_kernel<R, 0, 1, NST, SW>,
-                        (const void *)tile_sweep_tma_kernel<R, 1, 1, NST, SW>,
-                        (const void *)tile_sweep_tma_kernel<R, 0, 2, NST, SW>,
-                        (const void *)tile_sweep_tma_kernel<R, 1, 2, NST, SW>};
+  const void *fns[4] = {(const void *)tile_sweep_tma_kernel<R, 0, 1, NST, SW, NB>,
+                        (const void *)tile_sweep_tma_kernel<R, 1, 1, NST, SW, NB>,
+                        (const void *)tile_sweep_tma_kernel<R, 0, 2, NST, SW, NB>,
+                        (const void *)tile_sweep_tma_kernel<R, 1, 2, NST, SW, NB>};
   for (const void *f : fns) {
     cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
     if (e != cudaSuccess) return e;
@@ -420,6 +488,10 @@ cudaError_t tile_sweep_tma_setup(bool c128) {
   cudaError_t e = c128 ? tma_setup_r<double, 2>() : tma_setup_r<float, 2>();
   if (e != cudaSuccess) return e;
   e = c128 ? tma_setup_r<double, 2, 1>() : tma_setup_r<float, 2, 1>();
+  if (e != cudaSuccess) return e;
+  e = c128 ? tma_setup_r<double, 2, 0, 1>() : tma_setup_r<float, 2, 0, 1>();
+  if (e != cudaSuccess) return e;
+  e = c128 ? tma_setup_r<double, 3, 0, 1>() : tma_setup_r<float, 3, 0, 1>();
   if (e != cudaSuccess) return e;
   return c128 ? tma_setup_r<double, 3>() : tma_setup_r<float, 3>();
 }

@@ -30,6 +30,7 @@ QSIM_NO_QUBIT = 0xFFFFFFFF
 QSIM_OPT_TIME_SWEEPS, QSIM_OPT_MODE, QSIM_OPT_MEM_BUDGET, QSIM_OPT_SWEEP_KERNEL, QSIM_OPT_LAZY_LAST = 1, 2, 3, 4, 5
 QSIM_OPT_FUSE_LAYERS = 6
 QSIM_OPT_DISTRIBUTE = 7
+QSIM_OPT_BFS = 8
 
 EXPORTED = ["qsim_create", "qsim_destroy", "qsim_last_error", "qsim_version", "qsim_set_option",
             "qsim_set_stream", "qsim_load_circuit", "qsim_partition", "qsim_set_blocks",

@@ -64,29 +64,33 @@ def test_multipart_all_amplitudes(grid, depth, row_cuts, prec):
     assert_close(A.reshape(-1), ref, prec, f"{grid} d{depth} {row_cuts}")
 
 
+@pytest.mark.parametrize("bfs", [1, 0], ids=["bfs", "dfs"])
 @pytest.mark.parametrize("prec", PRECS, ids=PNAME.get)
-def test_multipart_tree_parts_vs_oracle(prec):
-    """6x7 d5 in 3 parts of 14 qubits (tile-sweep branch trees), ragged permuted blocks vs the oracle."""
+def test_multipart_tree_parts_vs_oracle(prec, bfs):
+    """6x7 d5 in 3 parts of 14 qubits (tile-sweep branch trees, level-synchronous node-batched
+    launches or depth-first), ragged permuted blocks vs the oracle."""
     circ = generate(6, 7, 5, 1)
     rng = np.random.default_rng(3)
     blocks = [rng.permutation(sample_block(14, n, s)) for n, s in ((37, 1), (64, 2), (29, 3))]
     ref = MP.amplitudes(circ, [2, 4], blocks)
-    A = run_multipart(circ, [2, 4], blocks, prec)
+    A = run_multipart(circ, [2, 4], blocks, prec, {Q.QSIM_OPT_BFS: bfs})
     assert_close(A, ref, prec, "6x7 d5 [2,4]")
 
 
+@pytest.mark.parametrize("bfs", [1, 0], ids=["bfs", "dfs"])
 @pytest.mark.parametrize("prec", PRECS, ids=PNAME.get)
-def test_multipart_mixed_parts_vs_oracle(prec):
+def test_multipart_mixed_parts_vs_oracle(prec, bfs):
     """7x4 d6 split 8 / 16 / 4 qubits: a small-state part, a tree part, a 4-qubit part; 2^8 branches."""
     circ = generate(7, 4, 6, 2)
     blocks = [np.arange(256)[::-5], sample_block(16, 41, 4), np.arange(16)]
     ref = MP.amplitudes(circ, [2, 6], blocks)
-    A = run_multipart(circ, [2, 6], blocks, prec)
+    A = run_multipart(circ, [2, 6], blocks, prec, {Q.QSIM_OPT_BFS: bfs})
     assert_close(A, ref, prec, "7x4 d6 [2,6]")
 
 
+@pytest.mark.parametrize("bfs", [1, 0], ids=["bfs", "dfs"])
 @pytest.mark.parametrize("row_cuts", [[2, 4, 6], [3, 5], [1, 4]])
-def test_multipart_equals_bipartition_56q(row_cuts):
+def test_multipart_equals_bipartition_56q(row_cuts, bfs):
     """8x7 (56 qubits) d8: the t-part result equals the (oracle-checked) bipartition on the same block."""
     circ = generate(8, 7, 8, 0)
     prec = Q.QSIM_C128
@@ -94,7 +98,7 @@ def test_multipart_equals_bipartition_56q(row_cuts):
     nq = [(bounds[k + 1] - bounds[k]) * 7 for k in range(len(bounds) - 1)]
     sizes = {4: [11, 9, 7, 5], 3: [13, 12, 10]}[len(nq)]
     blocks = [sample_block(nq[k], sizes[k], 10 + k) for k in range(len(nq))]
-    A = run_multipart(circ, row_cuts, blocks, prec)
+    A = run_multipart(circ, row_cuts, blocks, prec, {Q.QSIM_OPT_BFS: bfs})
     # the same amplitudes through the bipartition at row 4: split the concatenated index
     full = np.array([0], dtype=object)
     for k in range(len(nq)):
@@ -124,7 +128,7 @@ def test_multipart_errors():
         Q.qsim_load_circuit(ctx, 6, 2, 8, circ.gate_array())
         for rc, bl in (([4, 2], [np.arange(4)] * 3),            # not increasing
                        ([2, 4], [np.arange(4)] * 2),            # one block missing
-                       ([2, 4], [np.arange(4), np.arange(16), np.arange(4)]),   # index >= 2^4
+                       ([2, 4], [np.arange(4), np.arange(17), np.arange(4)]),   # index >= 2^4
                        ([2, 4], [np.arange(4), np.array([1, 1]), np.arange(4)])):  # duplicate
             with pytest.raises((Q.QsimError, ValueError)):
                 Q.qsim_multipart_amplitudes(ctx, rc, bl, Q.QSIM_C64)
