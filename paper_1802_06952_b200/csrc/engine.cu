@@ -1953,8 +1953,7 @@ void Engine::multipart_amplitudes(uint32_t t, const uint32_t *row_cuts, const ui
   }
 
   // evolve every part's branches; X_k[(beta_{k-1} << c_k) | beta_k, i] in fp64
-  std::vector<std::unique_ptr<DevBuf>> X(t);
-  DevBuf dS, slice, rowmap;
+  while (mp_X_.size() < t) mp_X_.emplace_back(new DevBuf());
   for (uint32_t k = 0; k < t; ++k) {
     const int hidx = 2 + (int)k;
     const HalfProgram &hp = half_[hidx].prog;
@@ -1976,45 +1975,86 @@ void Engine::multipart_amplitudes(uint32_t t, const uint32_t *row_cuts, const ui
       }
       rm[r] = (up << c_dn) | dn;
     }
-    dS.reserve((size_t)ns[k] * 8);
-    rowmap.reserve((size_t)nrows * 4);
-    slice.reserve((size_t)nrows * ns[k] * amp_);
-    check(cudaMemcpyAsync(dS.ptr, P.data(), P.size() * 8, cudaMemcpyHostToDevice, stream_), "upload part block");
-    check(cudaMemcpyAsync(rowmap.ptr, rm.data(), rm.size() * 4, cudaMemcpyHostToDevice, stream_), "upload rowmap");
+    mp_dS_.reserve((size_t)ns[k] * 8);
+    mp_rowmap_.reserve((size_t)nrows * 4);
+    mp_slice_.reserve((size_t)nrows * ns[k] * amp_);
+    check(cudaMemcpyAsync(mp_dS_.ptr, P.data(), P.size() * 8, cudaMemcpyHostToDevice, stream_), "upload part block");
+    check(cudaMemcpyAsync(mp_rowmap_.ptr, rm.data(), rm.size() * 4, cudaMemcpyHostToDevice, stream_),
+          "upload rowmap");
     if (bfs_fits(hidx))
-      evolve_half_bfs(hidx, slice.ptr, dS.as<uint64_t>(), ns[k]);
+      evolve_half_bfs(hidx, mp_slice_.ptr, mp_dS_.as<uint64_t>(), ns[k]);
     else
-      evolve_half(hidx, 0, (uint64_t)nrows, slice.ptr, dS.as<uint64_t>(), ns[k]);
-    X[k].reset(new DevBuf());
-    X[k]->reserve((size_t)nrows * ns[k] * 16);
-    check(launch_permute_rows(slice.ptr, c128_, rowmap.as<uint32_t>(), nrows, ns[k], X[k]->as<double>(), stream_),
+      evolve_half(hidx, 0, (uint64_t)nrows, mp_slice_.ptr, mp_dS_.as<uint64_t>(), ns[k]);
+    mp_X_[k]->reserve((size_t)nrows * ns[k] * 16);
+    check(launch_permute_rows(mp_slice_.ptr, c128_, mp_rowmap_.as<uint32_t>(), nrows, ns[k], mp_X_[k]->as<double>(),
+                              stream_),
           "permute rows");
     st_.kernel_launches++;
     st_.branches_evolved += (uint64_t)nrows;
     check(cudaStreamSynchronize(stream_), "multi-part evolve");  // P, rm are host temporaries
   }
 
-  // chain contraction, right to left: T_k[beta_{k-1}, (i_k, .., i_{t-1})]
-  DevBuf Tbuf[2];
-  const double *T = X[t - 1]->as<double>();
-  int64_t Nrest = ns[t - 1];
-  auto contract = [&](const double *U, int64_t K, int64_t M, int64_t batch, DevBuf &out) {
-    const size_t bytes = (size_t)batch * (size_t)M * (size_t)Nrest * 16;
+  // chain contraction split at boundary js: left product L_js[beta_js, (i_0..i_js)] (left to right,
+  // GEMM outputs laid out [beta_k][i_0..i_{k-1}][i_k]), right product R[beta_js, (i_{js+1}..)]
+  // (right to left, batched over beta_{k-1}), then one GEMM over beta_js.  js minimises the flops.
+  auto C2 = [&](int j) { return std::ldexp(1.0, mp.c[j]); };
+  int js = 0;
+  double best = -1.0;
+  for (int j = 0; j + 1 < (int)t; ++j) {
+    double P = (double)ns[0], fl = 0.0;
+    for (int k = 1; k <= j; ++k) {
+      fl += 8.0 * P * C2(k) * (double)ns[k] * C2(k - 1);
+      P *= (double)ns[k];
+    }
+    double Qr = (double)ns[t - 1];
+    for (int k = (int)t - 2; k > j; --k) {
+      fl += 8.0 * C2(k - 1) * (double)ns[k] * Qr * C2(k);
+      Qr *= (double)ns[k];
+    }
+    fl += 8.0 * P * Qr * C2(j);
+    if (best < 0.0 || fl < best) best = fl, js = j;
+  }
+  auto gemm_timed = [&](const double *U, const double *L, int64_t K, int64_t M, int64_t N, DevBuf &out, int64_t batch,
+                        int64_t N2) {
+    const size_t bytes = (size_t)batch * (size_t)M * (size_t)N * 16;
     out.reserve(bytes);
     check(cudaMemsetAsync(out.ptr, 0, bytes, stream_), "zero contraction");
-    check(launch_branch_gemm_batched(U, T, K, M, Nrest, out.as<double>(), batch, stream_), "contraction gemm");
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (time_sweeps_) {
+      e0 = get_event();
+      e1 = get_event();
+      check(cudaEventRecord(e0, stream_), "cudaEventRecord");
+    }
+    check(launch_branch_gemm_batched(U, L, K, M, N, out.as<double>(), batch, stream_, N2), "contraction gemm");
+    if (time_sweeps_) {
+      check(cudaEventRecord(e1, stream_), "cudaEventRecord");
+      ev_gemm_.emplace_back(e0, e1);
+    }
     st_.kernel_launches++;
-    st_.gemm_flops += 8.0 * (double)batch * (double)M * (double)Nrest * (double)K;
+    st_.gemm_flops += 8.0 * (double)batch * (double)M * (double)N * (double)K;
   };
-  for (int k = (int)t - 2; k >= 1; --k) {
-    DevBuf &out = Tbuf[k & 1];
-    contract(X[k]->as<double>(), (int64_t)1 << mp.c[k], ns[k], (int64_t)1 << mp.c[k - 1], out);
+  // left: L_0 = X_0 [beta_0, i_0]
+  const double *Lp = mp_X_[0]->as<double>();
+  int64_t P = ns[0];
+  for (int k = 1; k <= js; ++k) {
+    DevBuf &out = mp_T_[k & 1];
+    gemm_timed(Lp, mp_X_[k]->as<double>(), (int64_t)1 << mp.c[k - 1], P, ((int64_t)1 << mp.c[k]) * ns[k], out, 1,
+               ns[k]);
+    Lp = out.as<double>();
+    P *= ns[k];
+  }
+  // right: R_{t-1} = X_{t-1} [beta_{t-2}, i_{t-1}]
+  const double *T = mp_X_[t - 1]->as<double>();
+  int64_t Nrest = ns[t - 1];
+  for (int k = (int)t - 2; k > js; --k) {
+    DevBuf &out = mp_T_[2 + (k & 1)];
+    gemm_timed(mp_X_[k]->as<double>(), T, (int64_t)1 << mp.c[k], ns[k], Nrest, out, (int64_t)1 << mp.c[k - 1], 0);
     T = out.as<double>();
     Nrest *= ns[k];
   }
-  DevBuf Aout;
-  contract(X[0]->as<double>(), (int64_t)1 << mp.c[0], ns[0], 1, Aout);
-  const size_t n = (size_t)ns[0] * (size_t)Nrest;
+  gemm_timed(Lp, T, (int64_t)1 << mp.c[js], P, Nrest, mp_A_, 1, 0);
+  const DevBuf &Aout = mp_A_;
+  const size_t n = (size_t)P * (size_t)Nrest;
   if (amps) {
     if (c128_) {
       check(cudaMemcpyAsync(amps, Aout.ptr, n * 16, cudaMemcpyDeviceToHost, stream_), "D2H amplitudes");

@@ -134,6 +134,8 @@ class Engine {
   size_t dist_bytes_ = 0;
   DevBuf dbar_;
   DevBuf bfs_buf_[2];
+  std::vector<std::unique_ptr<DevBuf>> mp_X_;  // multi-part contraction operands (kept between calls)
+  DevBuf mp_dS_, mp_slice_, mp_rowmap_, mp_T_[4], mp_A_;
 
   bool have_circuit_ = false;
   Circuit circ_;

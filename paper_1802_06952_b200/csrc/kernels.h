@@ -218,9 +218,10 @@ cudaError_t launch_gather_layer_compact(const void *V, const uint64_t *S, int64_
 cudaError_t launch_branch_gemm(const void *U, const void *L, int64_t K, int64_t M, int64_t N,
                                double *A, bool c128, cudaStream_t s);
 // Multi-part contraction: for z in [0, batch),
-//   A_z[m, n] += sum_k U_z[k, m] * L[k, n],  U_z = U + z*K*M, A_z = A + z*M*N  (all double2)
+//   A_z[m, n] += sum_k U_z[k, m] * L[k, n],  U_z = U + z*K*M, A_z = A + z*M*N  (all double2);
+// N2 > 0: n = n1 * N2 + n2 and A_z is laid out [n1][m][n2] (the left chain's next operand)
 cudaError_t launch_branch_gemm_batched(const double *U, const double *L, int64_t K, int64_t M, int64_t N,
-                                       double *A, int64_t batch, cudaStream_t s);
+                                       double *A, int64_t batch, cudaStream_t s, int64_t N2 = 0);
 // dst[rowmap[r], :] = src[r, :] converted to double2 (src of the ctx precision)
 cudaError_t launch_permute_rows(const void *src, bool c128, const uint32_t *rowmap, int64_t nrows, int64_t ncols,
                                 double *dst, cudaStream_t s);

@@ -267,7 +267,8 @@ template <typename R>
 __global__ void __launch_bounds__(256) branch_gemm_kernel(const typename CxT<R>::T *__restrict__ U,
                                                           const typename CxT<R>::T *__restrict__ L,
                                                           int64_t K, int64_t M, int64_t N,
-                                                          double *__restrict__ A, int64_t sU, int64_t sA) {
+                                                          double *__restrict__ A, int64_t sU, int64_t sA,
+                                                          int64_t N2) {
   using C = typename CxT<R>::T;
   U += (int64_t)blockIdx.z * sU;  // batch z: its own U and A (multi-part contraction), L shared
   A += (int64_t)blockIdx.z * sA;
@@ -361,7 +362,9 @@ __global__ void __launch_bounds__(256) branch_gemm_kernel(const typename CxT<R>:
         const int64_t m = m0 + wm * 32 + mt * 8 + (lane >> 2);
         const int64_t n = n0 + wn * 16 + nt * 8 + (lane & 3) * 2 + c;
         if (m < M && n < N) {
-          double *a = A + 2 * (m * N + n);
+          // N2 > 0: n = (n1, n2) with n2 < N2 and the output is laid out [n1][m][n2]
+          const int64_t o = N2 > 0 ? (n / N2) * (M * N2) + m * N2 + (n % N2) : m * N + n;
+          double *a = A + 2 * o;
           a[0] += accr[mt][nt][c];
           a[1] += acci[mt][nt][c];
         }
@@ -373,21 +376,21 @@ cudaError_t launch_branch_gemm(const void *U, const void *L, int64_t K, int64_t 
   if (K <= 0 || M <= 0 || N <= 0) return cudaSuccess;
   dim3 grid((unsigned)((N + GB_N - 1) / GB_N), (unsigned)((M + GB_M - 1) / GB_M));
   if (c128)
-    branch_gemm_kernel<double><<<grid, 256, 0, s>>>((const double2 *)U, (const double2 *)L, K, M, N, A, 0, 0);
+    branch_gemm_kernel<double><<<grid, 256, 0, s>>>((const double2 *)U, (const double2 *)L, K, M, N, A, 0, 0, 0);
   else
-    branch_gemm_kernel<float><<<grid, 256, 0, s>>>((const float2 *)U, (const float2 *)L, K, M, N, A, 0, 0);
+    branch_gemm_kernel<float><<<grid, 256, 0, s>>>((const float2 *)U, (const float2 *)L, K, M, N, A, 0, 0, 0);
   return cudaGetLastError();
 }
 
 cudaError_t launch_branch_gemm_batched(const double *U, const double *L, int64_t K, int64_t M, int64_t N,
-                                       double *A, int64_t batch, cudaStream_t s) {
+                                       double *A, int64_t batch, cudaStream_t s, int64_t N2) {
   if (K <= 0 || M <= 0 || N <= 0 || batch <= 0) return cudaSuccess;
   const int64_t sU = 2 * K * M, sA = 2 * M * N;  // in doubles
   for (int64_t z0 = 0; z0 < batch; z0 += 65535) {
     dim3 grid((unsigned)((N + GB_N - 1) / GB_N), (unsigned)((M + GB_M - 1) / GB_M),
               (unsigned)std::min<int64_t>(65535, batch - z0));
     branch_gemm_kernel<double><<<grid, 256, 0, s>>>((const double2 *)(U + z0 * sU), (const double2 *)L, K, M, N,
-                                                    A + z0 * sA, sU / 2, sA);
+                                                    A + z0 * sA, sU / 2, sA, N2);
   }
   return cudaGetLastError();
 }
