@@ -5,15 +5,16 @@
     python -m torch.distributed.run --nproc-per-node N --master-addr 127.0.0.1 ... bench.py --gpus N
     python bench.py --impl reference      # the CPU oracle arm
 
-Workload (N = 1 default): config C4 = 56-qubit 8x7 grid, depth 22 (the largest single-GPU
-configuration of BASELINE.json; the 64q metric config is the 8-GPU one, --config C5),
-14 cut CZs -> 2^14 branches, sampled block 2^12 x 2^12 = 2^24 amplitudes.
+Workload (default, every N): config C5 = the metric's configuration, 64-qubit 8x8 grid,
+depth 22, 16 cut CZs -> 2^16 branches, sampled block 2^14 x 2^14 = 2^28 amplitudes (it fits
+one B200: 32 GiB c64 half states).  --config C4 (56q 8x7) / C3 (42q 6x7) for the smaller
+BASELINE.json configurations.
 
-One STEP = one of the 2^7 first-period prefix groups of that job (128 branches sharing the
+One STEP = one of the 2^8 first-period prefix groups of that job (256 branches sharing the
 cuts of layers 7-8): both half-circuit branch trees (all prefix-shared sweeps from layer 1),
 leaf gathers, the GEMM accumulation A += U^T L, then |a|^2 + prefix tables + 2^20 Philox
 draws.  Every group costs the same (identical structure, other projector bits), so the
-whole-job rate is exact:  value = 2^24 * (groups done) / 128 / time.  Each rank does one
+whole-job rate is exact:  value = 2^28 * (groups done) / 256 / time.  Each rank does one
 group per step (weak scaling); partial blocks are summed with NCCL every step.
 """
 from __future__ import annotations
@@ -41,9 +42,9 @@ N_DRAWS = 1 << 20
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="C4", choices=["C3", "C4", "C5"])
+    ap.add_argument("--config", default="C5", choices=["C3", "C4", "C5"])
     ap.add_argument("--precision", default="c64", choices=["c64", "c128"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--seed", type=int, default=0)
@@ -146,16 +147,22 @@ def oracle_sample(circ, budget_s: float = 20.0, max_gates: int | None = None):
     per_branch = len(gu) + len(gl) + circ.h_upper + circ.h_lower   # + layer-0 H on each qubit
     job_gate_apps = (1 << c) * per_branch + (1 << max(c - 1, 0)) * c  # + Z gates (popcount)
     h = circ.h_upper
-    psi = np.full(1 << h, 2.0 ** (-h / 2), dtype=np.complex128)  # H^{(x)h}|0> (pinned closed form)
+    # bounded host memory: above 28 qubits the oracle runs the gates of the first 28 qubits on a
+    # 2^28 state and the time per gate is scaled by 2^(h - 28) (a gate application is one pass
+    # over the state: its cost is linear in the state size)
+    hs = min(h, 28)
+    scale = float(1 << (h - hs))
+    gs = [g for g in gu if int(g[2]) < hs and (g[1] not in (4, "CZ") or int(g[3]) < hs)]
+    psi = np.full(1 << hs, 2.0 ** (-h / 2), dtype=np.complex128)  # H^{(x)h}|0> (pinned closed form)
     t0 = time.perf_counter()
     done = 0
-    for g in gu:
-        psi = SV.run_gates(psi, h, [g])
+    for g in gs:
+        psi = SV.run_gates(psi, hs, [g])
         done += 1
         if time.perf_counter() - t0 > budget_s or (max_gates and done >= max_gates):
             break
     dt = time.perf_counter() - t0
-    return dt / done, job_gate_apps, done
+    return dt / done * scale, job_gate_apps, done
 
 
 def run_reference(args):
@@ -182,9 +189,11 @@ def run_reference(args):
         "config": {"workload": f"{args.config} (oracle, flat partitioned simulator, numpy complex128)",
                    "extrapolated_job_s": t_job, "gate_applications_per_job": job},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
-                         "sample": f"each step = 1 oracle gate application on a 2^{circ.h_upper} "
-                                   f"complex128 half state (branch 0, upper half); job = {job} "
-                                   "gate applications (flat: every branch from scratch), extrapolated"},
+                         "sample": f"each step = 1 oracle gate application on a 2^{min(circ.h_upper, 28)} "
+                                   f"complex128 state (branch 0, upper half"
+                                   + (f"; x 2^{circ.h_upper - 28} for the 2^{circ.h_upper} half" if circ.h_upper > 28 else "")
+                                   + f"); job = {job} gate applications (flat: every branch from scratch), "
+                                   "extrapolated"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -295,7 +304,7 @@ def main():
     value = (n_u * n_l) * groups_done / G / t_dev
 
     # ---------------- end-to-end through the C-ABI with host buffers
-    k_e2e = args.e2e_steps if args.e2e_steps is not None else max(1, min(args.steps, 3))
+    k_e2e = args.e2e_steps if args.e2e_steps is not None else max(1, min(args.steps, 3 if circ.n < 64 else 1))
     barrier()
     t0 = time.perf_counter()
     for s in range(k_e2e):  # 0 steps: e2e skipped (profiling runs)
@@ -332,8 +341,9 @@ def main():
             tg, job, done = oracle_sample(circ, budget_s=20.0)
             cpu = {"value": (n_u * n_l) / (tg * job), "unit": UNIT, "cores": 1, "kind": "oracle",
                    "sample": f"{done} gate applications of the oracle (numpy complex128, 1 thread) on a "
-                             f"2^{circ.h_upper}-amplitude half state of branch 0; extrapolated to the "
-                             f"flat job's {job} gate applications ({B} branches x 2 halves)"}
+                             f"2^{min(circ.h_upper, 28)}-amplitude state (branch 0, upper half"
+                             + (f"; x 2^{circ.h_upper - 28} for the 2^{circ.h_upper} half" if circ.h_upper > 28 else "")
+                             + f"); extrapolated to the flat job's {job} gate applications ({B} branches x 2 halves)"}
         except MemoryError:
             cpu = {"value": None, "unit": UNIT, "cores": 1, "kind": "oracle",
                    "sample": "host out of memory for a full half state"}

@@ -1024,9 +1024,9 @@ void Engine::launch_plan(const TilePlan &tp, const Diag &fork, bool first, const
     p.job_pv[0] = p.pre.pv;
     p.job_zm[0] = p.pre.zm;
     const uint64_t tiles = 1ull << p.log2_ntiles;
-    const bool tma = (sweep_kernel_ != 1 || p.nswap) && pre_mode != 2;
+    const bool tma = (sweep_kernel_ != 1 || p.nswap) && (pre_mode != 2 || (gen_tma_ && !dist_));
     if (tma) {
-      if (pre_mode == 1) p.pre_s = make_split(pre, reg_positions(p, 0, c128_));
+      if (pre_mode >= 1) p.pre_s = make_split(pre, reg_positions(p, 0, c128_));
       const int grid = (int)std::min<uint64_t>(tiles, (uint64_t)num_sms_);
       const int stages = sweep_kernel_ == 2 ? 2 : sweep_kernel_ == 3 ? 3 : tma_stages(tp);
       check(launch_tile_sweep_tma(p, c128_, pre_mode, tp.npass, grid, stream_, stages),

@@ -3,6 +3,7 @@
 #pragma once
 
 #include <cstdint>
+#include <cstdlib>
 #include <deque>
 #include <memory>
 #include <stdexcept>
@@ -191,6 +192,9 @@ class Engine {
   void launch_nodes(const TilePlan &tp, const void *src, void *dst, int log2_nodes, int shift, const ForkDev &fork,
                     const HalfProgram &hp);
   bool bfs_ = true;  // QSIM_OPT_BFS (multi-part parts)
+  // generated (write-only) sweeps through the TMA kernel's PRE = 2 variant (QSIM_GEN_TMA=0: the
+  // register kernel, A/B only)
+  bool gen_tma_ = !(std::getenv("QSIM_GEN_TMA") && std::getenv("QSIM_GEN_TMA")[0] == '0');
   const void *run_level(int half, int level, uint64_t child, const void *src, void *dst, int skip);
   int lazy_depth(int half, int64_t nS) const;
   int tma_stages(const TilePlan &tp) const;

@@ -295,6 +295,7 @@ __global__ void __launch_bounds__(544, 1) tile_sweep_tma_kernel(const __grid_con
   };
 
   if (warp == 16) {
+    if constexpr (PRE == 2) return;  // generated sweep: nothing to load
     // ------------------------------------------------ producer: TMA bulk copies
     const int m = p.run_m;
     const int rbits = kHiBits - m;
@@ -367,12 +368,12 @@ __global__ void __launch_bounds__(544, 1) tile_sweep_tma_kernel(const __grid_con
           b0 |= 1u << p.hb[p.wsel[0][j]];
           b1 |= 1u << p.hb[p.wsel[NPASS - 1][j]];
         }
-      if constexpr (PRE == 1) phB = (uint32_t)diag_phase_b(b0, p.pre) & 7u;
+      if constexpr (PRE >= 1) phB = (uint32_t)diag_phase_b(b0, p.pre) & 7u;
       if (p.post.active) phB |= ((uint32_t)diag_phase_b(b1, p.post) & 7u) << 3;
       if constexpr (NB == 1)
         if (p.fork.n) fork_masks<NV>(b0 & ~p.gbase, t >> p.log2_ntiles, p, fzero, fneg);
     }
-    mbar_wait(&full_bar[s][grp], use & 1u);
+    if constexpr (PRE != 2) mbar_wait(&full_bar[s][grp], use & 1u);
 
     // pass 0: shared -> registers
     uint32_t ts = (uint32_t)lane, tg = outer | ((uint32_t)lane << VB);
@@ -382,11 +383,18 @@ __global__ void __launch_bounds__(544, 1) tile_sweep_tma_kernel(const __grid_con
         ts |= 1u << (5 + p.wsel[0][s]);
         tg |= 1u << p.hb[p.wsel[0][s]];
       }
+    if constexpr (PRE == 2) {  // generated: v = pre(i) (the H layer and the leading diagonals)
 #pragma unroll
-    for (int r = 0; r < 16; ++r) unpack<R, NV>(tile[slot_smem(ts, p.gsel[0], r)], v[r]);
+      for (int r = 0; r < 16; ++r)
+#pragma unroll
+        for (int e = 0; e < NV; ++e) v[r][e].x = (R)1, v[r][e].y = (R)0;
+    } else {
+#pragma unroll
+      for (int r = 0; r < 16; ++r) unpack<R, NV>(tile[slot_smem(ts, p.gsel[0], r)], v[r]);
+    }
     if constexpr (NB == 1)
       if (p.fork.n) apply_fork<R, NV>(v, fzero, fneg);
-    if constexpr (PRE == 1) apply_split<R, NV>(v, tg | p.gbase, phB & 7u, p.pre_s, tab_pre);
+    if constexpr (PRE >= 1) apply_split<R, NV>(v, tg | p.gbase, phB & 7u, p.pre_s, tab_pre);
     low_gates<R, NV>(v, p, lane);
     reg_gates<R, NV>(v, p.gkind[0]);
 
@@ -408,7 +416,8 @@ __global__ void __launch_bounds__(544, 1) tile_sweep_tma_kernel(const __grid_con
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     }
     __syncwarp();
-    if (lane == 0) mbar_arrive(&empty_bar[s]);
+    if constexpr (PRE != 2)
+      if (lane == 0) mbar_arrive(&empty_bar[s]);
     if constexpr (NPASS == 2) reg_gates<R, NV>(v, p.gkind[1]);
 
     constexpr int QL = NPASS - 1;
@@ -453,6 +462,11 @@ static cudaError_t launch_tma_r(const TileSweepParams &p, int pre_mode, int npas
 
 cudaError_t launch_tile_sweep_tma(const TileSweepParams &p, bool c128, int pre_mode, int npass, int grid,
                                   cudaStream_t s, int stages) {
+  if (pre_mode == 2) {  // generated sweep (no loads; two stages so the ping-pong groups never share one)
+    if (c128)
+      return npass == 1 ? launch_tma_t<double, 2, 1, 2>(p, grid, s) : launch_tma_t<double, 2, 2, 2>(p, grid, s);
+    return npass == 1 ? launch_tma_t<float, 2, 1, 2>(p, grid, s) : launch_tma_t<float, 2, 2, 2>(p, grid, s);
+  }
   if (p.log2_nodes > 0 || p.fork.n > 0) {  // node-batched (multi-part BFS levels)
     if (stages == 3)
       return c128 ? launch_tma_r<double, 3, 0, 1>(p, pre_mode, npass, grid, s)
@@ -484,8 +498,20 @@ static cudaError_t tma_setup_r() {
   return cudaSuccess;
 }
 
+template <typename R>
+static cudaError_t tma_setup_gen() {
+  const int bytes = 2 * kTileBytes;
+  cudaError_t e = cudaFuncSetAttribute((const void *)tile_sweep_tma_kernel<R, 2, 1, 2>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e != cudaSuccess) return e;
+  return cudaFuncSetAttribute((const void *)tile_sweep_tma_kernel<R, 2, 2, 2>,
+                              cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+}
+
 cudaError_t tile_sweep_tma_setup(bool c128) {
   cudaError_t e = c128 ? tma_setup_r<double, 2>() : tma_setup_r<float, 2>();
+  if (e != cudaSuccess) return e;
+  e = c128 ? tma_setup_gen<double>() : tma_setup_gen<float>();
   if (e != cudaSuccess) return e;
   e = c128 ? tma_setup_r<double, 2, 1>() : tma_setup_r<float, 2, 1>();
   if (e != cudaSuccess) return e;
