@@ -99,11 +99,13 @@ typedef enum {
                                 previous sweep (its tiles are stored straight into the peer's HBM over
                                 NVLink); sampled slices are summed over the ranks before the GEMM.
                                 Needs >= tile bits + 2 qubits per shard; lazy tail off. 0: default */,
-  QSIM_OPT_BFS = 8           /* multi-part partitions (qsim_multipart_amplitudes): 1 (default) runs a
-                                part's branch tree level by level when two consecutive levels fit in
-                                device memory, each sweep as ONE node-batched launch over every state of
-                                the level (the fork's P / Z applied per node in the sweep); 0: the
-                                depth-first executor of the halves (one launch per node and sweep)   */
+  QSIM_OPT_BFS = 8           /* 1 (default): for half / part states of at most 256 MiB, the depth-first
+                                executor hands whole subtrees (the largest whose two deepest levels fit
+                                in device memory) to a level-synchronous one: each sweep of a level is
+                                ONE node-batched launch over every state of the level (the fork's P / Z
+                                applied per node inside the sweep), leaves gathered in one launch (or
+                                per leaf with the lazy tail when the subtree has <= 4096 leaves);
+                                0: one launch per node and sweep                                      */
 } qsim_option;
 
 /* Create a context bound to CUDA device `device` (no device call is made until the

@@ -1251,7 +1251,16 @@ void Engine::evolve_half(int half, uint64_t b0, uint64_t b1, void *slice, const 
     }
   };
 
+  // below level mb whole subtrees run level-synchronously (node-batched launches)
+  const int mb = bfs_level(half, m0, avail > (size_t)nbuf * state_bytes_ ? avail - (size_t)nbuf * state_bytes_ : 0);
   std::function<void(int, uint64_t, const void *)> node = [&](int l, uint64_t prefix, const void *state) {
+    if (l == mb && state) {
+      const uint64_t lo = prefix << (c - sbits[l]), hi = (prefix + 1) << (c - sbits[l]);
+      if (lo >= b0 && hi <= b1) {
+        bfs_subtree(half, l, state, (char *)slice + (lo - b0) * (uint64_t)nS * amp_, dS, nS);
+        return;
+      }
+    }
     if (l == F) {
       const uint64_t b = prefix;
       const uint64_t ch = F >= 1 ? (b & ((1ull << hp.levels[F].k) - 1ull)) : 0;
@@ -1781,44 +1790,60 @@ static ForkDev fork_dev(const Level &lev) {
   return f;
 }
 
-bool Engine::bfs_fits(int half) const {
+// Level at which the depth-first executor hands a whole subtree to the level-synchronous one
+// (-1: never).  Worth it for small states, where one launch per node and sweep is launch-bound;
+// the subtree's two largest levels must fit next to the depth-first buffers.
+int Engine::bfs_level(int half, int m0, size_t avail) const {
   const HalfExec &he = half_[half];
   const HalfProgram &hp = he.prog;
-  if (!bfs_ || dist_ || fuse_layers_ || sweep_kernel_ == 1 || !he.tree || he.plans.empty()) return false;
-  if (hp.ncuts > 40) return false;
+  if (!bfs_ || dist_ || fuse_layers_ || sweep_kernel_ == 1 || !he.tree || he.plans.empty()) return -1;
+  if (state_bytes_ > ((size_t)256 << 20)) return -1;
   const int F = (int)hp.levels.size() - 1;
+  if (F < 1) return -1;
   for (int l = 1; l <= F; ++l) {
-    if (l < F && he.plans[l][0].empty()) return false;  // only the leaf level may defer its fork
-    for (const TilePlan &tp : he.plans[l][0])
-      if (tp.fused || tp.gen) return false;
+    if (l < F && he.plans[l][0].empty()) return -1;  // only the leaf level may defer its fork
+    for (const auto &v : he.plans[l])
+      for (const TilePlan &tp : v)
+        if (tp.fused || tp.gen || !tp.swaps.empty()) return -1;
   }
-  size_t free_b = 0, total_b = 0;
-  if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) return false;
-  size_t have = bfs_buf_[0].bytes + bfs_buf_[1].bytes;
-  for (auto *b : states_) have += b->bytes;
-  const double need = 2.0 * std::ldexp(1.0, hp.ncuts + hp.h) * (double)amp_;
-  return need + (double)(1u << 30) < (double)(free_b + have);
+  std::vector<int> sbits(F + 1, 0);
+  for (int l = 1; l <= F; ++l) sbits[l] = sbits[l - 1] + hp.levels[l].k;
+  const size_t have = bfs_buf_[0].bytes + bfs_buf_[1].bytes;
+  for (int l = m0; l < F; ++l) {
+    if (sbits[F] - sbits[l] > 40) continue;
+    double need = std::ldexp((double)state_bytes_, sbits[F] - sbits[l]);
+    if (F - 1 > l) need += std::ldexp((double)state_bytes_, sbits[F - 1] - sbits[l]);
+    if (need + (double)(256u << 20) <= (double)(avail + have)) return sbits[F] > sbits[l] ? l : -1;
+  }
+  return -1;
 }
 
-// Every level l: its first sweep reads the parents (node >> k_l) and applies the fork per node,
-// the others run in place; the leaves are gathered in one launch.
-void Engine::evolve_half_bfs(int half, void *slice, const uint64_t *dS, int64_t nS) {
+// The subtree below one level-m node (its state given), level by level: the first sweep of
+// level l reads the parents (node >> k_l) and applies the fork per node, the others run in
+// place, each as ONE node-batched launch; leaf rows go to out[leaf * nS].
+void Engine::bfs_subtree(int half, int m, const void *state, void *out, const uint64_t *dS, int64_t nS) {
   HalfExec &he = half_[half];
   const HalfProgram &hp = he.prog;
   const int F = (int)hp.levels.size() - 1;
-  const size_t node_bytes = ((size_t)1 << hp.h) * amp_;
-  // the two buffers alternate by level; the last level is the largest
-  for (auto *b : states_) b->release();
-  bfs_buf_[F & 1].reserve(node_bytes << hp.ncuts);
-  bfs_buf_[(F & 1) ^ 1].reserve(node_bytes << std::max(0, hp.ncuts - (F >= 1 ? hp.levels[F].k : 0)));
-  run_level(half, 0, 0, nullptr, bfs_buf_[0].ptr, 0);
+  int rel = 0;
+  for (int l = m + 1; l <= F; ++l) rel += hp.levels[l].k;
+  const int64_t nleaves = (int64_t)1 << rel;
+  const int kF = hp.levels[F].k;
+  // lazy tails need one gather launch per leaf: only for subtrees of few leaves
+  const int lazy = nleaves <= 4096 ? lazy_depth(half, nS) : 0;
+  bfs_buf_[F & 1].reserve(state_bytes_ << rel);
+  if (F - 1 > m) bfs_buf_[(F & 1) ^ 1].reserve(state_bytes_ << (rel - kF));
+  const void *src = state;
   int sb = 0;
-  for (int l = 1; l <= F; ++l) {
+  bool pending = false;
+  for (int l = m + 1; l <= F; ++l) {
     const Level &lev = hp.levels[l];
-    const auto &launches = he.plans[l][0];
-    if (launches.empty()) break;  // a fork at the last layer: applied in the gather
+    const auto &launches = he.plans[l][l == F ? std::min<size_t>((size_t)lazy, he.plans[l].size() - 1) : 0];
+    if (launches.empty()) {  // leaf level without full passes: its fork is applied in the gather
+      pending = true;
+      break;
+    }
     sb += lev.k;
-    const void *src = bfs_buf_[(l - 1) & 1].ptr;
     void *dst = bfs_buf_[l & 1].ptr;
     for (size_t i = 0; i < launches.size(); ++i) {
       ForkDev f;
@@ -1826,17 +1851,22 @@ void Engine::evolve_half_bfs(int half, void *slice, const uint64_t *dS, int64_t 
       if (i == 0) f = fork_dev(lev);
       launch_nodes(launches[i], i == 0 ? src : dst, dst, sb, i == 0 ? lev.k : 0, f, hp);
     }
+    src = dst;
   }
-  // leaves: the last level's states, or its parents with the pending fork
-  const bool pending = F >= 1 && he.plans[F][0].empty();
-  const int lastbuf = pending ? (F - 1) & 1 : F & 1;
-  ForkDev f;
-  std::memset(&f, 0, sizeof(f));
-  if (pending) f = fork_dev(hp.levels[F]);
-  check(launch_gather_nodes(bfs_buf_[lastbuf].ptr, (uint64_t)1 << hp.h, pending ? hp.levels[F].k : 0,
-                            (int64_t)1 << hp.ncuts, dS, nS, slice, f, c128_, stream_),
-        "gather nodes launch");
-  st_.kernel_launches++;
+  if (lazy == 0) {
+    ForkDev f;
+    std::memset(&f, 0, sizeof(f));
+    if (pending) f = fork_dev(hp.levels[F]);
+    check(launch_gather_nodes(src, (uint64_t)1 << hp.hl, pending ? kF : 0, nleaves, dS, nS, out, f, c128_, stream_),
+          "gather nodes launch");
+    st_.kernel_launches++;
+    return;
+  }
+  for (int64_t leaf = 0; leaf < nleaves; ++leaf) {
+    const uint64_t child = (uint64_t)leaf & ((1ull << kF) - 1ull);
+    const char *psi = (const char *)src + (size_t)(pending ? (leaf >> kF) : leaf) * state_bytes_;
+    gather_leaf(half, child, psi, dS, nS, (char *)out + (size_t)leaf * (size_t)nS * amp_, lazy);
+  }
 }
 
 // ---------------------------------------------------------------- multi-part partitions (f4)
@@ -1981,10 +2011,7 @@ void Engine::multipart_amplitudes(uint32_t t, const uint32_t *row_cuts, const ui
     check(cudaMemcpyAsync(mp_dS_.ptr, P.data(), P.size() * 8, cudaMemcpyHostToDevice, stream_), "upload part block");
     check(cudaMemcpyAsync(mp_rowmap_.ptr, rm.data(), rm.size() * 4, cudaMemcpyHostToDevice, stream_),
           "upload rowmap");
-    if (bfs_fits(hidx))
-      evolve_half_bfs(hidx, mp_slice_.ptr, mp_dS_.as<uint64_t>(), ns[k]);
-    else
-      evolve_half(hidx, 0, (uint64_t)nrows, mp_slice_.ptr, mp_dS_.as<uint64_t>(), ns[k]);
+    evolve_half(hidx, 0, (uint64_t)nrows, mp_slice_.ptr, mp_dS_.as<uint64_t>(), ns[k]);
     mp_X_[k]->reserve((size_t)nrows * ns[k] * 16);
     check(launch_permute_rows(mp_slice_.ptr, c128_, mp_rowmap_.as<uint32_t>(), nrows, ns[k], mp_X_[k]->as<double>(),
                               stream_),

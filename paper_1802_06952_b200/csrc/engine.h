@@ -187,11 +187,11 @@ class Engine {
   void evolve_half(int half, uint64_t b0, uint64_t b1, void *slice, const uint64_t *dS, int64_t nS);
   // level-synchronous (BFS) variant for a whole tree whose two largest consecutive levels fit:
   // every sweep of level l runs once over all 2^{sbits_l} node states (node-batched TMA launch)
-  bool bfs_fits(int half) const;
-  void evolve_half_bfs(int half, void *slice, const uint64_t *dS, int64_t nS);
+  int bfs_level(int half, int m0, size_t avail) const;
+  void bfs_subtree(int half, int m, const void *state, void *out, const uint64_t *dS, int64_t nS);
   void launch_nodes(const TilePlan &tp, const void *src, void *dst, int log2_nodes, int shift, const ForkDev &fork,
                     const HalfProgram &hp);
-  bool bfs_ = true;  // QSIM_OPT_BFS (multi-part parts)
+  bool bfs_ = true;  // QSIM_OPT_BFS: level-synchronous subtrees for small states
   // generated (write-only) sweeps through the TMA kernel's PRE = 2 variant (QSIM_GEN_TMA=0: the
   // register kernel, A/B only)
   bool gen_tma_ = !(std::getenv("QSIM_GEN_TMA") && std::getenv("QSIM_GEN_TMA")[0] == '0');

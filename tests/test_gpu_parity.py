@@ -140,6 +140,15 @@ def test_tree_mode_h14_variants(prec, lazy, kernel, fuse, h14_reference):
 
 
 @pytest.mark.parametrize("prec", PRECS, ids=PNAME.get)
+@pytest.mark.parametrize("bfs,lazy", [(0, 2), (1, 0), (1, 1), (1, 3)])
+def test_tree_mode_h14_bfs(prec, bfs, lazy, h14_reference):
+    """Level-synchronous subtrees (node-batched sweeps, per-node forks) on / off, with every lazy tail."""
+    circ, Su, Sl, ref = h14_reference
+    A = run_block(circ, Su, Sl, prec, opts={Q.QSIM_OPT_BFS: bfs, Q.QSIM_OPT_LAZY_LAST: lazy})
+    assert_close(A, ref, prec, f"h14 bfs={bfs} lazy={lazy}")
+
+
+@pytest.mark.parametrize("prec", PRECS, ids=PNAME.get)
 @pytest.mark.parametrize("branch", [0, 77])
 def test_fused_sweeps_c3_branch(prec, branch, c3_circuit):
     """C3-size leaf with and without layer fusion (same kernels as the bench) vs the oracle."""
