@@ -1251,10 +1251,10 @@ void Engine::evolve_half(int half, uint64_t b0, uint64_t b1, void *slice, const 
     }
   };
 
-  // below level mb whole subtrees run level-synchronously (node-batched launches)
+  // from level mb down, a node whose whole subtree lies in [b0, b1) runs it level-synchronously
   const int mb = bfs_level(half, m0, avail > (size_t)nbuf * state_bytes_ ? avail - (size_t)nbuf * state_bytes_ : 0);
   std::function<void(int, uint64_t, const void *)> node = [&](int l, uint64_t prefix, const void *state) {
-    if (l == mb && state) {
+    if (mb >= 0 && l >= mb && l < F && state) {  // deeper levels have smaller subtrees: they fit too
       const uint64_t lo = prefix << (c - sbits[l]), hi = (prefix + 1) << (c - sbits[l]);
       if (lo >= b0 && hi <= b1) {
         bfs_subtree(half, l, state, (char *)slice + (lo - b0) * (uint64_t)nS * amp_, dS, nS);
