@@ -105,9 +105,10 @@ cudaError_t launch_gather_nodes(const void *psi, uint64_t stride, int shift, int
 }
 
 // ---------------------------------------------------------------- lazy last layer
-// One warp per sampled index x: lanes split the 2^k input combinations y, each term is
-// w^{ph(x,y)} pre(y) psi[y] with ph = 6 popc((x^y) & SX) + 4 popc(~x & y & SY) (the
-// factored matrices SX' = [[1,-i],[-i,1]], SY' = [[1,-1],[1,1]]); warp sum, then post(x).
+// 2^min(k,5) lanes per sampled index x (a warp holds 32 >> min(k,5) indices, so layers with few
+// targets do not idle most lanes): the lanes of an index split the 2^k input combinations y, each
+// term is w^{ph(x,y)} pre(y) psi[y] with ph = 6 popc((x^y) & SX) + 4 popc(~x & y & SY) (the
+// factored matrices SX' = [[1,-i],[-i,1]], SY' = [[1,-1],[1,1]]); segment sum, then post(x).
 template <typename R>
 __global__ void __launch_bounds__(256) gather_layer_kernel(const typename CxT<R>::T *__restrict__ psi,
                                                            const uint64_t *__restrict__ S, int64_t n,
@@ -115,17 +116,21 @@ __global__ void __launch_bounds__(256) gather_layer_kernel(const typename CxT<R>
                                                            const __grid_constant__ LazyLayer ll) {
   using C = typename CxT<R>::T;
   const int lane = threadIdx.x & 31;
-  const int64_t j = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  if (j >= n) return;
-  if ((S[j] & ~ll.lmask) != ll.gsel) {  // another shard's index
-    if (lane == 0) out[j].x = out[j].y = (R)0;
-    return;
+  const int sb = ll.k < 5 ? ll.k : 5;  // log2 lanes per index
+  const int sub = lane & ((1 << sb) - 1);
+  const int64_t j = ((((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) << (5 - sb)) + (lane >> sb);
+  const bool valid = j < n;
+  bool own = false;
+  uint32_t x = 0;
+  if (valid) {
+    const uint64_t xs = S[j];
+    own = (xs & ~ll.lmask) == ll.gsel;  // else another shard's index (distributed half)
+    x = (uint32_t)xs;
   }
-  const uint32_t x = (uint32_t)S[j];
   const uint32_t base = x & ~ll.tmask;
-  const uint32_t nterm = 1u << ll.k;
+  const uint32_t nterm = own ? (1u << ll.k) : 0u;
   R sr = 0, si = 0;
-  for (uint32_t m = lane; m < nterm; m += 32) {
+  for (uint32_t m = sub; m < nterm; m += (1u << sb)) {
     uint32_t y = base;
 #pragma unroll 4
     for (int t = 0; t < ll.k; ++t) y |= ((m >> t) & 1u) << ll.bit[t];
@@ -140,12 +145,15 @@ __global__ void __launch_bounds__(256) gather_layer_kernel(const typename CxT<R>
     sr += v.x * wr - v.y * wi;
     si += v.x * wi + v.y * wr;
   }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
+  for (int o = (1 << sb) >> 1; o > 0; o >>= 1) {
     sr += __shfl_xor_sync(0xffffffffu, sr, o);
     si += __shfl_xor_sync(0xffffffffu, si, o);
   }
-  if (lane == 0) {
+  if (sub == 0 && valid) {
+    if (!own) {
+      out[j].x = out[j].y = (R)0;
+      return;
+    }
     const double pre_scale = ll.pre.active ? ll.pre.scale : 1.0;
     const int ph = diag_phase(x, ll.post, ll.post.zm);
     const double sc = ll.post.scale * pre_scale;
@@ -161,7 +169,9 @@ __global__ void __launch_bounds__(256) gather_layer_kernel(const typename CxT<R>
 cudaError_t launch_gather_layer(const void *psi, const uint64_t *S, int64_t n, void *out, const LazyLayer &ll,
                                 bool c128, cudaStream_t s) {
   if (n <= 0) return cudaSuccess;
-  const int64_t blocks = (n * 32 + 255) / 256;
+  const int sb = ll.k < 5 ? ll.k : 5;
+  const int64_t warps = (n + (32 >> sb) - 1) / (32 >> sb);
+  const int64_t blocks = (warps * 32 + 255) / 256;
   if (c128)
     gather_layer_kernel<double><<<(unsigned)blocks, 256, 0, s>>>((const double2 *)psi, S, n, (double2 *)out, ll);
   else
