@@ -482,9 +482,16 @@ void Engine::compile_plans(HalfExec &he) {
   for (size_t l = 0; l <= F; ++l) {
     const Level &lev = hp.levels[l];
     const size_t nskip = l == F ? 3 : 1;
+    uint32_t forkmask = 0;
+    for (int b : lev.cut_bits) forkmask |= 1u << b;
     for (size_t skip = 0; skip < nskip; ++skip) {
       const size_t n = lev.sweeps.size() - std::min(skip, lev.sweeps.size());
       he.plans[l].push_back(level_launches(hp, lev, n));
+      uint32_t touched = 0;  // a projected fork bit stays fixed until a gate acts on it
+      for (TilePlan &tp : he.plans[l].back()) {
+        tp.zfix = forkmask & ~touched;
+        touched |= tp.targets;
+      }
       if (std::getenv("QSIM_DEBUG_PLANS")) {
         std::fprintf(stderr, "%s level %zu skip %zu: %zu sweeps ->", hp.upper ? "U" : "D", l, skip, n);
         for (auto &tp : he.plans[l].back())
@@ -816,6 +823,10 @@ std::vector<TilePlan> Engine::legacy_plans(const HalfProgram &hp, const Sweep &s
         tp.p.nruns = nr;
         tp.p.log2_ntiles = hp.hl - T;
         tp.fused = false;
+        tp.targets = 0;
+        for (auto &g : H) tp.targets |= 1u << g.bit;
+        if (ci == 0)
+          for (auto &g : low) tp.targets |= 1u << g.bit;
         tp.layers = ci == nchunks - 1 ? 1 : 0;
         if (ci == nchunks - 1) tp.swaps = sw.swaps;
         tp.use_pre = ci == 0;
@@ -976,7 +987,7 @@ int Engine::tma_stages(const TilePlan &tp) const {
 }
 
 void Engine::launch_plan(const TilePlan &tp, const Diag &fork, bool first, const void *src, void *dst,
-                         const HalfProgram &hp, int out_buf) {
+                         const HalfProgram &hp, int out_buf, const Diag *child_fork) {
   const int h = hp.hl;
   int pre_mode = 0;
   Diag pre;
@@ -1023,6 +1034,13 @@ void Engine::launch_plan(const TilePlan &tp, const Diag &fork, bool first, const
     p.dst[0] = dst;
     p.job_pv[0] = p.pre.pv;
     p.job_zm[0] = p.pre.zm;
+    if (child_fork && zero_skip_ && !dist_ && !tp.gen && child_fork->pm && !child_fork->allzero) {
+      // tiles outside the fork's projector (on qubits no gate of the level has touched) are zero
+      uint32_t outer = (h >= 32 ? ~0u : ((1u << h) - 1u)) & ~((1u << tile_low_bits(c128_)) - 1u);
+      for (int j = 0; j < kHiBits; ++j) outer &= ~(1u << p.hb[j]);
+      p.skip_pm = child_fork->pm & tp.zfix & outer;
+      p.skip_pv = child_fork->pv & p.skip_pm;
+    }
     const uint64_t tiles = 1ull << p.log2_ntiles;
     const bool tma = (sweep_kernel_ != 1 || p.nswap) && (pre_mode != 2 || (gen_tma_ && !dist_));
     if (tma) {
@@ -1058,7 +1076,7 @@ const void *Engine::run_level(int half, int level, uint64_t child, const void *s
   const size_t n = launches.size();
   if (!dist_) {
     for (size_t i = 0; i < n; ++i)
-      launch_plan(launches[i], i == 0 ? fork : Diag(), i == 0, i == 0 ? src : dst, dst, he.prog);
+      launch_plan(launches[i], i == 0 ? fork : Diag(), i == 0, i == 0 ? src : dst, dst, he.prog, -1, &fork);
     return n ? dst : src;
   }
   // distributed half: level buffers 2l, 2l+1 (dst is buffer 2l).  A sweep that swaps local and

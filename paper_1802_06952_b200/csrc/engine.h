@@ -53,6 +53,8 @@ struct TilePlan {
   bool gen = false;
   Diag pre;
   std::vector<int> pass0_regs;  // global bits of the pass-0 register slots (pre DiagSplit)
+  uint32_t targets = ~0u;  // bits this launch applies gates on (all: unknown)
+  uint32_t zfix = 0;       // fork bits of the level not targeted by an earlier launch of the level
 };
 
 // A stage of a fused sweep: some gates of one layer, then (optionally) a diagonal.
@@ -195,11 +197,13 @@ class Engine {
   // generated (write-only) sweeps through the TMA kernel's PRE = 2 variant (QSIM_GEN_TMA=0: the
   // register kernel, A/B only)
   bool gen_tma_ = !(std::getenv("QSIM_GEN_TMA") && std::getenv("QSIM_GEN_TMA")[0] == '0');
+  // known-zero tiles of projected fork children are not read (QSIM_ZERO_SKIP=0: off, A/B only)
+  bool zero_skip_ = !(std::getenv("QSIM_ZERO_SKIP") && std::getenv("QSIM_ZERO_SKIP")[0] == '0');
   const void *run_level(int half, int level, uint64_t child, const void *src, void *dst, int skip);
   int lazy_depth(int half, int64_t nS) const;
   int tma_stages(const TilePlan &tp) const;
   void launch_plan(const TilePlan &tp, const Diag &fork, bool first_chunk_of_level, const void *src,
-                   void *dst, const HalfProgram &hp, int out_buf = -1);
+                   void *dst, const HalfProgram &hp, int out_buf = -1, const Diag *child_fork = nullptr);
   void gather_leaf(int half, uint64_t child_last, const void *psi, const uint64_t *dS, int64_t nS,
                    void *out_row, int depth);
   void gemm(const void *U, const void *L, int64_t K, int64_t M, int64_t N, double *A);

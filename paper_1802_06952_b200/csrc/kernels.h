@@ -94,6 +94,10 @@ struct TileSweepParams {
   int32_t node_src_shift;
   uint64_t node_stride;
   ForkDev fork;
+  // known-zero tiles (TMA sweep, NB = 0): a tile whose outer bits satisfy (outer & skip_pm) !=
+  // skip_pv holds only zeros (a fork projector P_b on a qubit no gate of the level has touched
+  // yet); it is not loaded, and zeros are stored
+  uint32_t skip_pm, skip_pv;
 };
 
 // pre_mode: 0 none, 1 apply pre diagonal to loaded values, 2 generate (no load)

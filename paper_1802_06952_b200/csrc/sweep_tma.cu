@@ -314,6 +314,16 @@ __global__ void __launch_bounds__(544, 1) tile_sweep_tma_kernel(const __grid_con
       const char *src = srcb;
       if constexpr (NB == 1) src += (size_t)(((t >> p.log2_ntiles) >> p.node_src_shift) * p.node_stride) * sizeof(C);
       char *stage = reinterpret_cast<char *>(stages + (size_t)s * NVEC);
+      if constexpr (NB == 0) {
+        if ((outer & p.skip_pm) != p.skip_pv) {  // known-zero tile: complete the phase without loading
+          if (bulk) {
+            if (lane == 0) mbar_arrive(fb);
+          } else {
+            mbar_arrive(fb);
+          }
+          continue;
+        }
+      }
       if (bulk) {
         if (lane == 0) mbar_arrive_expect_tx(fb, kTileBytes);
         __syncwarp();
@@ -388,6 +398,11 @@ __global__ void __launch_bounds__(544, 1) tile_sweep_tma_kernel(const __grid_con
       for (int r = 0; r < 16; ++r)
 #pragma unroll
         for (int e = 0; e < NV; ++e) v[r][e].x = (R)1, v[r][e].y = (R)0;
+    } else if (NB == 0 && (outer & p.skip_pm) != p.skip_pv) {  // known-zero tile (not loaded)
+#pragma unroll
+      for (int r = 0; r < 16; ++r)
+#pragma unroll
+        for (int e = 0; e < NV; ++e) v[r][e].x = v[r][e].y = (R)0;
     } else {
 #pragma unroll
       for (int r = 0; r < 16; ++r) unpack<R, NV>(tile[slot_smem(ts, p.gsel[0], r)], v[r]);
