@@ -174,6 +174,7 @@ void Engine::ensure_device() {
 }
 
 void Engine::set_option(int key, int64_t value) {
+  ++plan_gen_;  // compiled multi-part programs depend on the options
   switch (key) {
     case QSIM_OPT_TIME_SWEEPS:
       time_sweeps_ = value != 0;
@@ -235,6 +236,7 @@ void Engine::load_circuit(uint32_t rows, uint32_t cols, uint32_t depth, const qs
   std::string err = build_circuit(rows, cols, depth, gates, n_gates, cut_row, cut_layers, n_cut_layers, c);
   if (!err.empty()) throw Error(QSIM_EINVAL, err);
   circ_ = std::move(c);
+  ++plan_gen_;
   compile_all();
   have_circuit_ = true;
   have_blocks_ = false;
@@ -1976,11 +1978,16 @@ void Engine::multipart_amplitudes(uint32_t t, const uint32_t *row_cuts, const ui
     if ((int)mp.cuts[k].size() > 30) throw Error(QSIM_EINVAL, "a part has more than 30 cut bits");
   }
   if (total * 16.0 > std::ldexp(1.0, 36)) throw Error(QSIM_EINVAL, "amplitude block larger than 64 GiB");
-  ensure_device();
 
-  // compile the part programs (branch trees over each part's cuts) into half_[2 + k]
-  while (half_.size() > 2) half_.pop_back();
-  for (uint32_t k = 0; k < t; ++k) {
+  // compile the part programs (branch trees over each part's cuts) into half_[2 + k]; reused while
+  // the circuit, the options and the row cuts are unchanged (the relabelling search is not free)
+  const bool cached = mp_gen_ == plan_gen_ && mp_key_ == mp.bounds && half_.size() == 2 + (size_t)t;
+  if (!cached) {
+    while (half_.size() > 2) half_.pop_back();
+    mp_key_ = mp.bounds;
+    mp_gen_ = plan_gen_;
+  }
+  for (uint32_t k = 0; k < t && !cached; ++k) {
     half_.emplace_back();
     HalfExec &he = half_.back();
     std::vector<int> id(nq[k]);
@@ -2000,6 +2007,7 @@ void Engine::multipart_amplitudes(uint32_t t, const uint32_t *row_cuts, const ui
     }
   }
 
+  ensure_device();
   // evolve every part's branches; X_k[(beta_{k-1} << c_k) | beta_k, i] in fp64
   while (mp_X_.size() < t) mp_X_.emplace_back(new DevBuf());
   for (uint32_t k = 0; k < t; ++k) {

@@ -139,6 +139,8 @@ class Engine {
   DevBuf bfs_buf_[2];
   std::vector<std::unique_ptr<DevBuf>> mp_X_;  // multi-part contraction operands (kept between calls)
   DevBuf mp_dS_, mp_slice_, mp_rowmap_, mp_T_[4], mp_A_;
+  std::vector<uint32_t> mp_key_;  // row bounds of the compiled parts in half_[2..]
+  uint64_t plan_gen_ = 0, mp_gen_ = ~0ull;
 
   bool have_circuit_ = false;
   Circuit circ_;

@@ -149,6 +149,16 @@ def test_tree_mode_h14_bfs(prec, bfs, lazy, h14_reference):
 
 
 @pytest.mark.parametrize("prec", PRECS, ids=PNAME.get)
+@pytest.mark.parametrize("zero_skip", ["0", "1"])
+def test_tree_mode_h14_zero_skip(prec, zero_skip, h14_reference, monkeypatch):
+    """Known-zero tiles of projected fork children skipped (default) or read (QSIM_ZERO_SKIP=0), depth-first."""
+    monkeypatch.setenv("QSIM_ZERO_SKIP", zero_skip)
+    circ, Su, Sl, ref = h14_reference
+    A = run_block(circ, Su, Sl, prec, opts={Q.QSIM_OPT_BFS: 0})
+    assert_close(A, ref, prec, f"h14 zero_skip={zero_skip}")
+
+
+@pytest.mark.parametrize("prec", PRECS, ids=PNAME.get)
 @pytest.mark.parametrize("branch", [0, 77])
 def test_fused_sweeps_c3_branch(prec, branch, c3_circuit):
     """C3-size leaf with and without layer fusion (same kernels as the bench) vs the oracle."""
