@@ -259,7 +259,7 @@ void Engine::compile_all() {
       plan_distributed(half_[h]);
       compile_plans(half_[h]);
     } else if (half_[h].tree) {  // relabel qubits to physical bits for long tile runs (choose_perm)
-      const std::vector<int> perm = choose_perm(half_[h]);
+      const std::vector<int> perm = choose_perm(half_[h], perm_ns_[h]);
       bool ident = true;
       for (size_t b = 0; b < perm.size(); ++b) ident = ident && perm[b] == (int)b;
       if (!ident) {
@@ -515,7 +515,7 @@ void Engine::compile_plans(HalfExec &he) {
 // of a permutation is the sum over the sweeps that run as full passes of (nodes executing the
 // sweep) / speed; a seeded local search over transpositions minimises it.
 // QSIM_PERM = id | rev | rand | auto (default) for tests.
-std::vector<int> Engine::choose_perm(const HalfExec &he) const {
+std::vector<int> Engine::choose_perm(const HalfExec &he, int64_t nS) const {
   const HalfProgram &hp = he.prog;
   const int h = hp.h, L = tile_low_bits(c128_);
   std::vector<int> perm(h);
@@ -560,6 +560,26 @@ std::vector<int> Engine::choose_perm(const HalfExec &he) const {
   }
   static const double speed[8] = {4940, 5310, 5680, 5930, 5990, 6020, 6040, 6050};
   const int VB = c128_ ? 0 : 1;
+  // lazy-tail gather (nS > 0: the block size is known): per leaf, nS * 2^(k_d) cone points each read
+  // the 2^(k_(d-1)) combinations of the earlier lazy layer's targets (depth 2; depth 1: nS points x
+  // 2^(k_d)); targets on the bits inside a 32-byte sector share sectors.  Cost in sweep units at ~4400
+  // GB/s of random sectors (B200, lazy gather measured in the launch lists).
+  int lz = 0;
+  std::vector<int> gbits;  // canonical target bits of the gathered layer
+  double gpoints = 0.0;
+  static const bool gather_term = !(std::getenv("QSIM_PERM_GATHER") && std::getenv("QSIM_PERM_GATHER")[0] == '0');
+  if (gather_term && nS > 0 && F >= 1) {
+    lz = lazy_depth_of(hp, nS);
+    const auto &sw = hp.levels[F].sweeps;
+    if (lz >= 1 && sw.size() >= (size_t)lz) {
+      const Sweep &g = sw[sw.size() - (size_t)lz];
+      for (auto &x : g.gates) gbits.push_back(x.bit);
+      gpoints = (double)nS * (lz == 2 ? std::ldexp(1.0, (int)sw.back().gates.size()) : 1.0) *
+                std::ldexp(1.0, sbits);
+    }
+  }
+  const int sector_bits = c128_ ? 1 : 2;
+  const double sweep_bytes = 2.0 * std::ldexp(1.0, h) * (double)amp_;
   auto cost = [&](const std::vector<int> &p) {
     double c = 0;
     for (const SW &x : sws) {
@@ -587,6 +607,12 @@ std::vector<int> Engine::choose_perm(const HalfExec &he) const {
         if (ci == 0) v *= 1.0 - (c128_ ? 0.03 : 0.02) * nlane;
         c += x.w / v;
       }
+    }
+    if (!gbits.empty()) {
+      int in_sector = 0;
+      for (int b : gbits) in_sector += p[b] < sector_bits;
+      const double sectors = gpoints * std::ldexp(1.0, (int)gbits.size() - in_sector);
+      c += sectors * 32.0 / sweep_bytes / 4400.0;
     }
     return c;
   };
@@ -909,6 +935,12 @@ void Engine::set_blocks(const uint64_t *up, size_t nu, const uint64_t *lo, size_
   if (!have_circuit_) throw Error(QSIM_ESTATE, "no circuit loaded");
   validate_block(up, nu, circ_.h_u, "upper");
   validate_block(lo, nl, circ_.h_l, "lower");
+  if (!dist_ && (perm_ns_[0] != (int64_t)nu || perm_ns_[1] != (int64_t)nl)) {
+    // the relabelling weighs the lazy-tail gathers by the block sizes: re-plan for these sizes
+    perm_ns_[0] = (int64_t)nu;
+    perm_ns_[1] = (int64_t)nl;
+    compile_all();
+  }
   ensure_device();
   Su_.assign(up, up + nu);
   Sl_.assign(lo, lo + nl);
@@ -1120,8 +1152,9 @@ static LazyLayer lazy_layer(const Sweep &sw, const Diag &pre) {
 // (0, 1 or 2; at most lazy_depth_).  Cost model in bytes: a sweep moves 2 * 2^h * amp;
 // a lazy layer costs ~96 bytes per scattered read (32-byte sector, ~3x random-access
 // inefficiency); depth 2 reads n_S * 2^(k_d + k_(d-1)) values.
-int Engine::lazy_depth(int half, int64_t nS) const {
-  const HalfProgram &hp = half_[half].prog;
+int Engine::lazy_depth(int half, int64_t nS) const { return lazy_depth_of(half_[half].prog, nS); }
+
+int Engine::lazy_depth_of(const HalfProgram &hp, int64_t nS) const {
   const int F = (int)hp.levels.size() - 1;
   if (full_leaf_ || F < 1 || lazy_depth_ < 1) return 0;
   const auto &sw = hp.levels[F].sweeps;
@@ -1996,7 +2029,7 @@ void Engine::multipart_amplitudes(uint32_t t, const uint32_t *row_cuts, const ui
     he.prog = compile_part(circ_, lo, hi, k + 1 < t, mp.cuts[k], std::vector<std::vector<int>>(circ_.depth + 2, id), id);
     compile_plans(he);
     if (he.tree) {
-      const std::vector<int> perm = choose_perm(he);
+      const std::vector<int> perm = choose_perm(he, ns[k]);
       bool ident = true;
       for (size_t b = 0; b < perm.size(); ++b) ident = ident && perm[b] == (int)b;
       if (!ident) {

@@ -179,7 +179,9 @@ class Engine {
   void plan_distributed(HalfExec &he);      // layout schedule with fused local/global swaps
   void dist_buffers(size_t bytes, int nbuf);  // level buffers + IPC peer pointers
   void dist_barrier();                      // stream-ordered barrier over the ranks
-  std::vector<int> choose_perm(const HalfExec &he) const;
+  std::vector<int> choose_perm(const HalfExec &he, int64_t nS = 0) const;
+  int lazy_depth_of(const HalfProgram &hp, int64_t nS) const;
+  int64_t perm_ns_[2] = {0, 0};  // block sizes the relabelling of each half was chosen for
   bool plan_fused(const HalfProgram &hp, const std::vector<Stage> &stages, const Diag &pre, TilePlan &tp);
   std::vector<TilePlan> level_launches(const HalfProgram &hp, const Level &lev, size_t n);
   std::vector<TilePlan> legacy_plans(const HalfProgram &hp, const Sweep &sw);
