@@ -616,19 +616,28 @@ std::vector<int> Engine::choose_perm(const HalfExec &he, int64_t nS) const {
     }
     return c;
   };
+  static const int iters = std::getenv("QSIM_PERM_ITERS") ? std::atoi(std::getenv("QSIM_PERM_ITERS")) : 6000;
+  static const int restarts = std::getenv("QSIM_PERM_RESTARTS") ? std::atoi(std::getenv("QSIM_PERM_RESTARTS")) : 1;
   std::vector<int> best = perm;
   double bc = cost(best);
-  for (int it = 0; it < 6000; ++it) {
-    std::vector<int> q = best;
-    const int i = (int)(next() % (uint64_t)h), j = (int)(next() % (uint64_t)h);
-    if (i == j) continue;
-    std::swap(q[i], q[j]);
-    const double c = cost(q);
-    if (c <= bc) {
-      best = q;
-      bc = c;
+  for (int r = 0; r < std::max(1, restarts); ++r) {
+    std::vector<int> cur = perm;
+    double cc = cost(cur);
+    for (int it = 0; it < iters; ++it) {
+      std::vector<int> q = cur;
+      const int i = (int)(next() % (uint64_t)h), j = (int)(next() % (uint64_t)h);
+      if (i == j) continue;
+      std::swap(q[i], q[j]);
+      const double c = cost(q);
+      if (c <= cc) {
+        cur = q;
+        cc = c;
+      }
     }
+    if (cc < bc) best = cur, bc = cc;
   }
+  if (std::getenv("QSIM_DEBUG_PERM"))
+    std::fprintf(stderr, "choose_perm h=%d nS=%lld cost %.6g (identity %.6g)\n", h, (long long)nS, bc, cost(perm));
   return best;
 }
 
