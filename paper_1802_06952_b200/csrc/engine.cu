@@ -1924,6 +1924,33 @@ void Engine::bfs_subtree(int half, int m, const void *state, void *out, const ui
     st_.kernel_launches++;
     return;
   }
+  const Level &levF = hp.levels[F];
+  if (!pending && levF.sweeps.size() > (size_t)lazy) {
+    // the lazy layers do not carry the fork: one node-batched launch per lazy stage for all leaves
+    const size_t n = levF.sweeps.size();
+    LazyLayer lld = lazy_layer(levF.sweeps[n - 1], levF.sweeps[n - 1].pre);
+    lld.node_stride = (uint64_t)1 << hp.hl;
+    lld.nper = nS;
+    if (lazy == 1) {
+      check(launch_gather_layer(src, dS, nS * nleaves, out, lld, c128_, stream_), "gather_layer launch");
+      st_.kernel_launches++;
+    } else {
+      LazyLayer ll1 = lazy_layer(levF.sweeps[n - 2], levF.sweeps[n - 2].pre);
+      const int64_t ncone = nS << lld.k;
+      ll1.node_stride = (uint64_t)1 << hp.hl;
+      ll1.nper = ncone;
+      cone_idx_.reserve((size_t)ncone * 8);
+      cone_val_.reserve((size_t)ncone * (size_t)nleaves * amp_);
+      check(launch_cone_indices(dS, nS, lld, cone_idx_.as<uint64_t>(), stream_), "cone launch");
+      check(launch_gather_layer(src, cone_idx_.as<uint64_t>(), ncone * nleaves, cone_val_.ptr, ll1, c128_, stream_),
+            "gather_layer launch");
+      check(launch_gather_layer_compact(cone_val_.ptr, dS, nS * nleaves, out, lld, c128_, stream_),
+            "gather_layer_compact launch");
+      st_.kernel_launches += 3;
+    }
+    st_.lazy_gathers += (uint64_t)nleaves;
+    return;
+  }
   for (int64_t leaf = 0; leaf < nleaves; ++leaf) {
     const uint64_t child = (uint64_t)leaf & ((1ull << kF) - 1ull);
     const char *psi = (const char *)src + (size_t)(pending ? (leaf >> kF) : leaf) * state_bytes_;

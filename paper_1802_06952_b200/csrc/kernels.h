@@ -208,6 +208,10 @@ struct LazyLayer {
   // distributed half: the shard holds the indices with (i & ~lmask) == gsel, at i & lmask (the
   // layer's targets are local, so every term of an owned index is in the shard); others give 0
   uint64_t lmask, gsel;
+  // node batching (level-synchronous leaves): node_stride > 0 -> output j covers node j / nper of
+  // states psi + node * node_stride at index S[j % nper]
+  uint64_t node_stride;
+  int64_t nper;
 };
 cudaError_t launch_gather_layer(const void *psi, const uint64_t *S, int64_t n, void *out,
                                 const LazyLayer &ll, bool c128, cudaStream_t s);

@@ -123,7 +123,13 @@ __global__ void __launch_bounds__(256) gather_layer_kernel(const typename CxT<R>
   bool own = false;
   uint32_t x = 0;
   if (valid) {
-    const uint64_t xs = S[j];
+    int64_t jj = j;
+    if (ll.node_stride) {  // node-batched leaves
+      const int64_t node = j / ll.nper;
+      jj = j - node * ll.nper;
+      psi += (uint64_t)node * ll.node_stride;
+    }
+    const uint64_t xs = S[jj];
     own = (xs & ~ll.lmask) == ll.gsel;  // else another shard's index (distributed half)
     x = (uint32_t)xs;
   }
@@ -208,11 +214,12 @@ __global__ void __launch_bounds__(256) gather_layer_compact_kernel(const typenam
   const int lane = threadIdx.x & 31;
   const int64_t j = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (j >= n) return;
-  if ((S[j] & ~ll.lmask) != ll.gsel) {  // another shard's index
+  const int64_t jj = ll.node_stride ? j % ll.nper : j;  // node-batched: V, out are [node][nper]
+  if ((S[jj] & ~ll.lmask) != ll.gsel) {  // another shard's index
     if (lane == 0) out[j].x = out[j].y = (R)0;
     return;
   }
-  const uint32_t x = (uint32_t)S[j];
+  const uint32_t x = (uint32_t)S[jj];
   const uint32_t base = x & ~ll.tmask;
   const uint32_t nterm = 1u << ll.k;
   const C *Vj = V + ((size_t)j << ll.k);
