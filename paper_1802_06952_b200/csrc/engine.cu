@@ -1925,7 +1925,8 @@ void Engine::bfs_subtree(int half, int m, const void *state, void *out, const ui
     return;
   }
   const Level &levF = hp.levels[F];
-  if (!pending && levF.sweeps.size() > (size_t)lazy) {
+  static const bool batch_lazy = !(std::getenv("QSIM_BATCH_LAZY") && std::getenv("QSIM_BATCH_LAZY")[0] == '0');
+  if (batch_lazy && !pending && levF.sweeps.size() > (size_t)lazy) {
     // the lazy layers do not carry the fork: one node-batched launch per lazy stage for all leaves
     const size_t n = levF.sweeps.size();
     LazyLayer lld = lazy_layer(levF.sweeps[n - 1], levF.sweeps[n - 1].pre);
