@@ -1798,7 +1798,7 @@ void Engine::synchronize() {
 // ---------------------------------------------------------------- level-synchronous tree (BFS)
 // Node-batched launch of one planned sweep over 2^log2_nodes states (TMA kernel only).
 void Engine::launch_nodes(const TilePlan &tp, const void *src, void *dst, int log2_nodes, int shift,
-                          const ForkDev &fork, const HalfProgram &hp) {
+                          const ForkDev &fork, const HalfProgram &hp, bool apply_fork, uint32_t proj_bits) {
   if (tp.fused || tp.gen || !tp.swaps.empty()) throw Error(QSIM_EINVAL, "node-batched sweep of an unsupported plan");
   const int h = hp.hl;
   int pre_mode = 0;
@@ -1825,6 +1825,12 @@ void Engine::launch_nodes(const TilePlan &tp, const void *src, void *dst, int lo
   p.node_src_shift = shift;
   p.node_stride = (uint64_t)1 << h;
   p.fork = fork;
+  p.fork_apply = apply_fork ? 1 : 0;
+  if (zero_skip_ && proj_bits) {  // projected fork bits not yet touched in the level, outside the tile
+    uint32_t outer = (h >= 32 ? ~0u : ((1u << h) - 1u)) & ~((1u << tile_low_bits(c128_)) - 1u);
+    for (int j = 0; j < kHiBits; ++j) outer &= ~(1u << p.hb[j]);
+    p.nb_skip = proj_bits & tp.zfix & outer;
+  }
   if (pre_mode == 1) p.pre_s = make_split(pre, reg_positions(p, 0, c128_));
   const uint64_t tiles = 1ull << (p.log2_ntiles + log2_nodes);
   const int grid = (int)std::min<uint64_t>(tiles, (uint64_t)num_sms_);
@@ -1907,12 +1913,12 @@ void Engine::bfs_subtree(int half, int m, const void *state, void *out, const ui
     }
     sb += lev.k;
     void *dst = bfs_buf_[l & 1].ptr;
-    for (size_t i = 0; i < launches.size(); ++i) {
-      ForkDev f;
-      std::memset(&f, 0, sizeof(f));
-      if (i == 0) f = fork_dev(lev);
-      launch_nodes(launches[i], i == 0 ? src : dst, dst, sb, i == 0 ? lev.k : 0, f, hp);
-    }
+    const ForkDev f = fork_dev(lev);
+    uint32_t proj = 0;  // P-role cut bits (a P_b child is zero off its branch bits)
+    for (int j = 0; j < lev.k; ++j)
+      if ((lev.pmask >> j) & 1u) proj |= 1u << lev.cut_bits[j];
+    for (size_t i = 0; i < launches.size(); ++i)
+      launch_nodes(launches[i], i == 0 ? src : dst, dst, sb, i == 0 ? lev.k : 0, f, hp, i == 0, proj);
     src = dst;
   }
   if (lazy == 0) {

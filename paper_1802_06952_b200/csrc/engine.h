@@ -196,7 +196,7 @@ class Engine {
   int bfs_level(int half, int m0, size_t avail) const;
   void bfs_subtree(int half, int m, const void *state, void *out, const uint64_t *dS, int64_t nS);
   void launch_nodes(const TilePlan &tp, const void *src, void *dst, int log2_nodes, int shift, const ForkDev &fork,
-                    const HalfProgram &hp);
+                    const HalfProgram &hp, bool apply_fork = true, uint32_t proj_bits = 0);
   bool bfs_ = true;  // QSIM_OPT_BFS: level-synchronous subtrees for small states
   // generated (write-only) sweeps through the TMA kernel's PRE = 2 variant (QSIM_GEN_TMA=0: the
   // register kernel, A/B only)

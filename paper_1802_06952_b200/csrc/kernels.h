@@ -98,6 +98,11 @@ struct TileSweepParams {
   // skip_pv holds only zeros (a fork projector P_b on a qubit no gate of the level has touched
   // yet); it is not loaded, and zeros are stored
   uint32_t skip_pm, skip_pv;
+  // node-batched variant: fork_apply = apply p.fork at pass 0 (the level's first launch); nb_skip =
+  // the projected fork bits (outer bits of the tile, untouched so far in the level): a tile whose
+  // bits there differ from the node's branch bits is zero (not loaded)
+  int32_t fork_apply;
+  uint32_t nb_skip;
 };
 
 // pre_mode: 0 none, 1 apply pre diagonal to loaded values, 2 generate (no load)

@@ -239,6 +239,17 @@ __device__ __forceinline__ void apply_fork(typename Cx2<R>::T (&v)[16][NV], cons
     }
 }
 
+// the node's branch bits on p.nb_skip (node-batched known-zero tiles)
+__device__ __forceinline__ uint32_t nb_skip_value(const uint64_t node, const TileSweepParams &p) {
+  uint32_t v = 0;
+  if (!p.nb_skip) return 0;
+  for (int j = 0; j < p.fork.n; ++j) {
+    const uint32_t m = 1u << p.fork.bit[j];
+    if ((p.nb_skip & m) && ((node >> (p.fork.n - 1 - j)) & 1u)) v |= m;
+  }
+  return v;
+}
+
 // shared-memory slot index of register slot r for pass q (incrementally OR-ed)
 __device__ __forceinline__ uint32_t slot_smem(uint32_t base, const uint8_t *gsel, int r) {
   uint32_t si = base;
@@ -314,8 +325,10 @@ __global__ void __launch_bounds__(544, 1) tile_sweep_tma_kernel(const __grid_con
       const char *src = srcb;
       if constexpr (NB == 1) src += (size_t)(((t >> p.log2_ntiles) >> p.node_src_shift) * p.node_stride) * sizeof(C);
       char *stage = reinterpret_cast<char *>(stages + (size_t)s * NVEC);
-      if constexpr (NB == 0) {
-        if ((outer & p.skip_pm) != p.skip_pv) {  // known-zero tile: complete the phase without loading
+      uint32_t spm = p.skip_pm, spv = p.skip_pv;
+      if constexpr (NB == 1) spv = nb_skip_value(t >> p.log2_ntiles, p), spm = p.nb_skip;
+      {
+        if ((outer & spm) != spv) {  // known-zero tile: complete the phase without loading
           if (bulk) {
             if (lane == 0) mbar_arrive(fb);
           } else {
@@ -381,7 +394,7 @@ __global__ void __launch_bounds__(544, 1) tile_sweep_tma_kernel(const __grid_con
       if constexpr (PRE >= 1) phB = (uint32_t)diag_phase_b(b0, p.pre) & 7u;
       if (p.post.active) phB |= ((uint32_t)diag_phase_b(b1, p.post) & 7u) << 3;
       if constexpr (NB == 1)
-        if (p.fork.n) fork_masks<NV>(b0 & ~p.gbase, t >> p.log2_ntiles, p, fzero, fneg);
+        if (p.fork.n && p.fork_apply) fork_masks<NV>(b0 & ~p.gbase, t >> p.log2_ntiles, p, fzero, fneg);
     }
     if constexpr (PRE != 2) mbar_wait(&full_bar[s][grp], use & 1u);
 
@@ -398,7 +411,8 @@ __global__ void __launch_bounds__(544, 1) tile_sweep_tma_kernel(const __grid_con
       for (int r = 0; r < 16; ++r)
 #pragma unroll
         for (int e = 0; e < NV; ++e) v[r][e].x = (R)1, v[r][e].y = (R)0;
-    } else if (NB == 0 && (outer & p.skip_pm) != p.skip_pv) {  // known-zero tile (not loaded)
+    } else if (NB == 0 ? ((outer & p.skip_pm) != p.skip_pv)
+                       : ((outer & p.nb_skip) != nb_skip_value(t >> p.log2_ntiles, p))) {  // known-zero tile
 #pragma unroll
       for (int r = 0; r < 16; ++r)
 #pragma unroll
@@ -408,7 +422,7 @@ __global__ void __launch_bounds__(544, 1) tile_sweep_tma_kernel(const __grid_con
       for (int r = 0; r < 16; ++r) unpack<R, NV>(tile[slot_smem(ts, p.gsel[0], r)], v[r]);
     }
     if constexpr (NB == 1)
-      if (p.fork.n) apply_fork<R, NV>(v, fzero, fneg);
+      if (p.fork.n && p.fork_apply) apply_fork<R, NV>(v, fzero, fneg);
     if constexpr (PRE >= 1) apply_split<R, NV>(v, tg | p.gbase, phB & 7u, p.pre_s, tab_pre);
     low_gates<R, NV>(v, p, lane);
     reg_gates<R, NV>(v, p.gkind[0]);
