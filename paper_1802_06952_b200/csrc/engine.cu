@@ -1315,6 +1315,9 @@ void Engine::evolve_half(int half, uint64_t b0, uint64_t b1, void *slice, const 
 
   // from level mb down, a node whose whole subtree lies in [b0, b1) runs it level-synchronously
   const int mb = bfs_level(half, m0, avail > (size_t)nbuf * state_bytes_ ? avail - (size_t)nbuf * state_bytes_ : 0);
+  if (std::getenv("QSIM_DEBUG_BFS"))
+    std::fprintf(stderr, "evolve_half %d [%llu, %llu): h=%d F=%d cuts=%d m0=%d mb=%d state=%zu avail=%zu\n", half,
+                 (unsigned long long)b0, (unsigned long long)b1, hp.hl, F, c, m0, mb, state_bytes_, avail);
   std::function<void(int, uint64_t, const void *)> node = [&](int l, uint64_t prefix, const void *state) {
     if (mb >= 0 && l >= mb && l < F && state) {  // deeper levels have smaller subtrees: they fit too
       const uint64_t lo = prefix << (c - sbits[l]), hi = (prefix + 1) << (c - sbits[l]);
@@ -1897,8 +1900,11 @@ void Engine::bfs_subtree(int half, int m, const void *state, void *out, const ui
   for (int l = m + 1; l <= F; ++l) rel += hp.levels[l].k;
   const int64_t nleaves = (int64_t)1 << rel;
   const int kF = hp.levels[F].k;
-  // lazy tails need one gather launch per leaf: only for subtrees of few leaves
-  const int lazy = nleaves <= 4096 ? lazy_depth(half, nS) : 0;
+  // lazy tails: node-batched when they do not carry the fork, else one gather per leaf (few leaves)
+  int lazy = nleaves <= 4096 ? lazy_depth(half, nS) : 0;
+  // a lazy tail that covers the leaf level's first sweep carries the per-leaf fork: it cannot be
+  // node-batched, and one launch per leaf costs more than the full batched pass it saves
+  if (lazy > 0 && hp.levels[F].sweeps.size() <= (size_t)lazy && nleaves > 16) lazy = 0;
   bfs_buf_[F & 1].reserve(state_bytes_ << rel);
   if (F - 1 > m) bfs_buf_[(F & 1) ^ 1].reserve(state_bytes_ << (rel - kF));
   const void *src = state;
