@@ -477,26 +477,35 @@ void Engine::compile_plans(HalfExec &he) {
   else
     he.tree = !can_small || dist_;
   he.plans.clear();
+  he.variants.clear();
+  he.glayers.clear();
+  he.ft.clear();
   if ((he.tree && !can_tree) || (!he.tree && !can_small)) return;  // reported at evolve time
   if (!he.tree) return;
+  plan_levels(hp, he.plans, false);
+}
+
+void Engine::plan_levels(const HalfProgram &hp, std::vector<std::vector<std::vector<TilePlan>>> &plans,
+                         bool all_skips) {
   const size_t F = hp.levels.size() - 1;
-  he.plans.resize(hp.levels.size());
+  plans.clear();
+  plans.resize(hp.levels.size());
   for (size_t l = 0; l <= F; ++l) {
     const Level &lev = hp.levels[l];
-    const size_t nskip = l == F ? 3 : 1;
+    const size_t nskip = (l == F || all_skips) ? 3 : 1;
     uint32_t forkmask = 0;
     for (int b : lev.cut_bits) forkmask |= 1u << b;
     for (size_t skip = 0; skip < nskip; ++skip) {
       const size_t n = lev.sweeps.size() - std::min(skip, lev.sweeps.size());
-      he.plans[l].push_back(level_launches(hp, lev, n));
+      plans[l].push_back(level_launches(hp, lev, n));
       uint32_t touched = 0;  // a projected fork bit stays fixed until a gate acts on it
-      for (TilePlan &tp : he.plans[l].back()) {
+      for (TilePlan &tp : plans[l].back()) {
         tp.zfix = forkmask & ~touched;
         touched |= tp.targets;
       }
       if (std::getenv("QSIM_DEBUG_PLANS")) {
         std::fprintf(stderr, "%s level %zu skip %zu: %zu sweeps ->", hp.upper ? "U" : "D", l, skip, n);
-        for (auto &tp : he.plans[l].back())
+        for (auto &tp : plans[l].back())
           std::fprintf(stderr, " [%s x%d p%d m%d]", tp.fused ? "F" : "legacy", tp.layers, tp.npass,
                        tp.fused ? tp.f.run_m : tp.p.run_m);
         std::fprintf(stderr, "\n");
@@ -1399,8 +1408,14 @@ void Engine::evolve_range(uint64_t b0, uint64_t b1) {
   for (uint64_t s = b0; s < b1;) {
     uint64_t e = std::min(b1, (s / p2 + 1) * p2);
     e = std::min(e, s + chunk);
-    evolve_half(0, s, e, U_.ptr, d_Sp_[0].as<uint64_t>(), nu);
-    evolve_half(1, s, e, L_.ptr, d_Sp_[1].as<uint64_t>(), nl);
+    for (int h = 0; h < 2; ++h) {
+      void *sl = h == 0 ? U_.ptr : L_.ptr;
+      const int64_t ns = h == 0 ? nu : nl;
+      if (deferred_ && !dist_ && half_[h].tree)
+        evolve_tree(h, s, e, sl, d_Sp_[h].as<uint64_t>(), ns);
+      else
+        evolve_half(h, s, e, sl, d_Sp_[h].as<uint64_t>(), ns);
+    }
     if (dist_ && world_ > 1) {
       // §2.3.3: each rank gathered the sampled entries it owns (zeros elsewhere).  The lower
       // slices are summed on every rank; the upper ones stay partial, so the GEMM gives this
@@ -1613,7 +1628,10 @@ void Engine::branch_state(int half, uint64_t b, void *out) {
   slice.reserve(n * amp_);
   full_leaf_ = true;
   try {
-    evolve_half(half, b, b + 1, slice.ptr, tmp_.as<uint64_t>(), (int64_t)n);
+    if (deferred_ && !dist_ && he.tree)
+      evolve_tree(half, b, b + 1, slice.ptr, tmp_.as<uint64_t>(), (int64_t)n);
+    else
+      evolve_half(half, b, b + 1, slice.ptr, tmp_.as<uint64_t>(), (int64_t)n);
   } catch (...) {
     full_leaf_ = false;
     throw;
@@ -1968,6 +1986,386 @@ void Engine::bfs_subtree(int half, int m, const void *state, void *out, const ui
     const uint64_t child = (uint64_t)leaf & ((1ull << kF) - 1ull);
     const char *psi = (const char *)src + (size_t)(pending ? (leaf >> kF) : leaf) * state_bytes_;
     gather_leaf(half, child, psi, dS, nS, (char *)out + (size_t)leaf * (size_t)nS * amp_, lazy);
+  }
+}
+
+// ---------------------------------------------------------------- deferred-fork branch trees
+// SURVEY §8(a) a4 (prefix sharing).  Eq. 1 replaces a cut CZ by P_b (upper endpoint) and
+// Z^b (lower endpoint) at the cut layer.  Both are diagonal on the cut's qubit, so they commute
+// with every later diagonal (T, CZ, other projectors) and with every gate on other qubits: the
+// fork may be applied at the input of any layer up to the first X^1/2 / Y^1/2 on that qubit
+// (HalfExec::ft), and the branches stay one shared state until then.  Cuts never targeted again
+// (or targeted only in the lazily evaluated tail) fork inside the leaf gather.  choose_tree
+// places the forks of a block of branches (a dynamic programme over the half's sweeps, bounded by
+// the state buffers that fit in HBM); the executor below runs the resulting tree depth-first.
+
+int Engine::tree_lazy(int half, int64_t nS) const {
+  const HalfProgram &hp = half_[half].prog;
+  std::vector<const Sweep *> sw;
+  for (auto &l : hp.levels)
+    for (auto &s : l.sweeps) sw.push_back(&s);
+  if (full_leaf_ || lazy_depth_ < 1 || sw.size() < 2) return 0;
+  const Sweep &d = *sw.back();
+  if (d.gen || d.gates.size() > 12) return 0;
+  if (lazy_depth_ < 2 || sw.size() < 3) return 1;
+  const Sweep &d1 = *sw[sw.size() - 2];
+  if (d1.gen) return 1;
+  const int kd = (int)d.gates.size(), kd1 = (int)d1.gates.size();
+  if (kd + kd1 > 20 || ((double)nS * std::ldexp(1.0, kd)) > (double)(1 << 26)) return 1;
+  if (lazy_depth_ == 3) return 2;  // forced (tests)
+  const double sweep = 2.0 * std::ldexp(1.0, hp.hl) * (double)amp_;
+  const double lazy1 = 96.0 * (double)nS * std::ldexp(1.0, kd);
+  const double lazy2 = 96.0 * (double)nS * std::ldexp(1.0, kd + kd1) + 2.0 * lazy1;
+  return lazy2 < sweep + lazy1 ? 2 : 1;
+}
+
+// Fork placement for the aligned block of 2^m branches whose top c - m cut bits are fixed.
+// Sweep i of the half (one per gate layer gl[i]; sweep 0 generates the state) is materialised for
+// i < Sm = S - lz.  A free cut g may fork at the input of sweep p with cut layer < gl[p] <=
+// ft_g (p >= 1), or in the gather when ft_g is a lazy layer or never comes (allow_gather).
+// With fork points p_1 < .. < p_K and every cut at the latest point <= its ft, the states between
+// p_i and p_{i+1} number 2^{#cuts with ft index < p_{i+1}}, so the cost of a segment does not
+// depend on the earlier points: a DP over (last point, points used), K <= nbuf - 1 (each
+// branching level keeps its parent state).  Pinning the j cuts that must fork first (the
+// executor enumerates them, recomputing the path above) trades recomputation for buffers.
+TreeChoice Engine::choose_tree(int half, int m, int lz, int64_t nS, int nbuf, bool allow_gather) const {
+  const HalfExec &he = half_[half];
+  const int c = (int)circ_.cuts.size();
+  const std::vector<int> &gl = he.glayers;
+  const int S = (int)gl.size(), Sm = S - lz;
+  const int Kmax = std::max(0, nbuf - 1);
+  auto W = [&](int a, int b) {  // sweep units of sweeps [a, b)
+    double w = 0;
+    for (int i = a; i < b; ++i) w += i == 0 ? 0.5 : 1.0;
+    return w;
+  };
+  auto idx_after = [&](int layer) {  // first sweep with gl > layer
+    int i = 0;
+    while (i < S && gl[i] <= layer) ++i;
+    return i;
+  };
+  // per cut: lo = earliest sweep it may fork at (a branching point is >= 1: sweep 0 generates the
+  // root), e = index of its first target (S: none); pinned cuts apply at sweep lo0
+  std::vector<int> lo(c), lo0(c), e(c);
+  for (int g = 0; g < c; ++g) {
+    lo0[g] = idx_after((int)circ_.cuts[g].layer);
+    lo[g] = std::max(1, lo0[g]);
+    int ei = S;
+    for (int i = 0; i < S; ++i)
+      if (gl[i] == he.ft[g]) ei = i;
+    e[g] = ei;
+  }
+  // one more fork value in the gather: a lazy stage (~96 bytes per scattered read) or a gather
+  const double sweep_bytes = 2.0 * std::ldexp(1.0, half_[half].prog.hl) * (double)amp_;
+  int kd = 0;
+  for (auto &l : he.prog.levels)
+    if (!l.sweeps.empty()) kd = (int)l.sweeps.back().gates.size();
+  const double gamma = lz > 0 ? 96.0 * (double)nS * std::ldexp(1.0, kd) / sweep_bytes : 32.0 * (double)nS / sweep_bytes;
+  std::vector<int> forced, freec;
+  for (int g = c - m; g < c; ++g) {
+    const bool gather = e[g] >= Sm;
+    const int ee = gather ? Sm - 1 : e[g];
+    if (gather && allow_gather) {
+      freec.push_back(g);
+      continue;
+    }
+    if (ee < 1 || lo[g] > ee)
+      forced.push_back(g);
+    else
+      freec.push_back(g);
+  }
+  auto eff = [&](int g) { return e[g] >= Sm ? (allow_gather ? S : Sm - 1) : e[g]; };
+  std::sort(freec.begin(), freec.end(), [&](int a, int b) { return eff(a) != eff(b) ? eff(a) < eff(b) : a < b; });
+  TreeChoice best;
+  best.cost = -1;
+  const int jmax = Kmax == 0 ? (int)freec.size() : std::min<int>((int)freec.size(), 16);
+  for (int j = 0; j <= jmax; ++j) {
+    std::vector<int> R, G;  // materialised forks, gather forks
+    for (size_t t = (size_t)j; t < freec.size(); ++t) (eff(freec[t]) >= S ? G : R).push_back(freec[t]);
+    const int nR = (int)R.size();
+    // dp[q][k]: cost of sweeps [0, q) with k points, the last at q (q >= 1); -1 = infeasible
+    std::vector<std::vector<double>> dp(Sm + 1, std::vector<double>(Kmax + 2, -1.0));
+    std::vector<std::vector<int>> from(Sm + 1, std::vector<int>(Kmax + 2, -1));
+    auto cnt_lt = [&](int q) {
+      int n = 0;
+      for (int g : R) n += eff(g) < q;
+      return n;
+    };
+    auto seg_ok = [&](int p, int q) {  // cuts with eff in [p, q) fork at p
+      for (int g : R)
+        if (eff(g) >= p && eff(g) < q && lo[g] > p) return false;
+      return true;
+    };
+    for (int q = 1; q < Sm && Kmax >= 1; ++q) {
+      if (cnt_lt(q) == 0) dp[q][1] = W(0, q), from[q][1] = 0;
+      for (int k = 2; k <= Kmax; ++k)
+        for (int p = 1; p < q; ++p) {
+          if (dp[p][k - 1] < 0 || !seg_ok(p, q)) continue;
+          const double v = dp[p][k - 1] + std::ldexp(W(p, q), cnt_lt(q));
+          if (dp[q][k] < 0 || v < dp[q][k]) dp[q][k] = v, from[q][k] = p;
+        }
+    }
+    double cost = -1;
+    int bq = -1, bk = 0;
+    if (nR == 0) cost = W(0, Sm);
+    for (int q = 1; q < Sm; ++q)
+      for (int k = 1; k <= Kmax; ++k) {
+        if (dp[q][k] < 0 || !seg_ok(q, Sm)) continue;
+        const double v = dp[q][k] + std::ldexp(W(q, Sm), nR);
+        if (cost < 0 || v < cost - 1e-9) cost = v, bq = q, bk = k;
+      }
+    if (cost < 0) continue;
+    cost += std::ldexp(gamma, nR + (int)G.size());
+    const double total = std::ldexp(cost, j + (int)forced.size());
+    if (best.cost >= 0 && total >= best.cost - 1e-9) continue;
+    best.cost = total;
+    best.points = bk;
+    best.qlist.assign(forced.begin(), forced.end());
+    for (int t = 0; t < j; ++t) best.qlist.push_back(freec[t]);
+    std::vector<int> pts;
+    for (int q = bq, k = bk; q > 0 && k > 0; q = from[q][k], --k) pts.push_back(q);
+    std::sort(pts.begin(), pts.end());
+    best.apply.assign(c, 0);
+    for (int g = 0; g < c; ++g) best.apply[g] = lo0[g] < S ? gl[lo0[g]] : (int)circ_.depth + 1;  // pinned
+    for (int g : G) best.apply[g] = he.ft[g];
+    for (int g : R) {
+      int p = -1;
+      for (int x : pts)
+        if (x <= eff(g)) p = x;
+      best.apply[g] = gl[p];
+    }
+  }
+  if (best.cost < 0) throw Error(QSIM_EINVAL, "no feasible fork placement");
+  return best;
+}
+
+TreeVariant &Engine::variant(int half, const std::vector<int> &apply) {
+  HalfExec &he = half_[half];
+  auto it = he.variants.find(apply);
+  if (it != he.variants.end()) return *it->second;
+  if (he.variants.size() >= 64) he.variants.clear();
+  auto v = std::make_unique<TreeVariant>();
+  const bool up = half == 0;
+  const std::vector<int> &perm = he.prog.perm;
+  v->prog = compile_part(circ_, up ? 0 : circ_.h_u, up ? circ_.h_u : circ_.n, up, half_cuts(circ_, up),
+                         std::vector<std::vector<int>>(circ_.depth + 2, perm), perm, &apply);
+  plan_levels(v->prog, v->plans, true);
+  TreeVariant &ref = *v;
+  he.variants[apply] = std::move(v);
+  return ref;
+}
+
+// [b0, b1) as aligned power-of-two blocks; slice row r = branch b0 + r
+void Engine::evolve_tree(int half, uint64_t b0, uint64_t b1, void *slice, const uint64_t *dS, int64_t nS) {
+  HalfExec &he = half_[half];
+  if (he.glayers.empty()) {
+    const bool up = half == 0;
+    he.glayers = gate_layers(circ_, up ? 0 : circ_.h_u, up ? circ_.h_u : circ_.n);
+    he.ft = first_targets(circ_, half_cuts(circ_, up));
+  }
+  const int c = (int)circ_.cuts.size();
+  for (uint64_t s = b0; s < b1;) {
+    int m = 0;
+    while (m < c && ((s >> m) & 1u) == 0 && s + (2ull << m) <= b1) ++m;
+    evolve_block(half, s, m, (char *)slice + (s - b0) * (uint64_t)nS * amp_, dS, nS);
+    s += 1ull << m;
+  }
+}
+
+void Engine::evolve_block(int half, uint64_t b0, int m, void *slice, const uint64_t *dS, int64_t nS) {
+  HalfExec &he = half_[half];
+  const int c = (int)circ_.cuts.size();
+  const int T = tile_low_bits(c128_) + kHiBits;
+  if (he.prog.hl < T) throw Error(QSIM_EINVAL, "tree mode needs h >= tile bits");
+  state_bytes_ = ((size_t)1 << he.prog.hl) * amp_;
+  size_t free_b = 0, total_b = 0;
+  check(cudaMemGetInfo(&free_b, &total_b), "cudaMemGetInfo");
+  size_t have = 0;
+  for (auto *b : states_) have += b->bytes;
+  const int lz = tree_lazy(half, nS);
+  size_t margin = (size_t)512 << 20;
+  if (lz == 2) margin += (size_t)nS * 256 * (amp_ + 8);  // cone buffers of the lazy tail
+  const size_t avail = free_b + have > margin ? free_b + have - margin : 0;
+  const size_t nfit = avail / state_bytes_;
+  if (nfit < 1) {
+    std::ostringstream msg;
+    msg << "a " << he.prog.h << "-qubit half state needs " << state_bytes_ << " bytes; only " << avail
+        << " bytes available for state buffers";
+    throw Error(QSIM_ENOMEM, msg.str());
+  }
+  int nbuf = (int)std::min<size_t>(nfit, 12);
+  if (mem_budget_ > 0) nbuf = std::max(1, std::min<int>(nbuf, (int)((size_t)mem_budget_ / state_bytes_)));
+  const TreeChoice tc = choose_tree(half, m, lz, nS, nbuf, true);
+  const TreeVariant &v = variant(half, tc.apply);
+  ensure_states(half, tc.points + 1);
+  if (std::getenv("QSIM_DEBUG_TREE")) {
+    std::fprintf(stderr, "tree half %d b0=%llu m=%d lz=%d nbuf=%d: cost %.1f sweeps, %d points, %zu pinned, levels",
+                 half, (unsigned long long)b0, m, lz, nbuf, tc.cost, tc.points, tc.qlist.size());
+    for (auto &l : v.prog.levels) std::fprintf(stderr, " [%d:k%d s%zu]", l.fork_layer + 1, l.k, l.sweeps.size());
+    std::fprintf(stderr, "\n");
+  }
+  std::vector<int> pin(c, -1);
+  for (int g = 0; g < c - m; ++g) pin[g] = (int)((b0 >> (c - 1 - g)) & 1u);
+  const size_t nq = tc.qlist.size();
+  for (uint64_t q = 0; q < (1ull << nq); ++q) {
+    for (size_t i = 0; i < nq; ++i) pin[tc.qlist[i]] = (int)((q >> i) & 1u);
+    run_tree(half, v, lz, pin, m, slice, dS, nS);
+  }
+}
+
+namespace {
+// the fork values of level `lev` consistent with the pinned cuts: child index (bit k-1-j = fork
+// bit j) and the branch bits it sets
+struct ChildSet {
+  uint64_t base = 0;
+  std::vector<int> free;  // fork bits j that are free
+};
+ChildSet child_set(const Level &lev, const std::vector<int> &pin) {
+  ChildSet cs;
+  for (int j = 0; j < lev.k; ++j) {
+    const int p = pin[lev.cut_g[j]];
+    if (p < 0)
+      cs.free.push_back(j);
+    else if (p)
+      cs.base |= 1ull << (lev.k - 1 - j);
+  }
+  return cs;
+}
+uint64_t child_of(const Level &lev, const ChildSet &cs, uint64_t f) {
+  uint64_t ch = cs.base;
+  for (size_t t = 0; t < cs.free.size(); ++t)
+    if ((f >> t) & 1u) ch |= 1ull << (lev.k - 1 - cs.free[t]);
+  return ch;
+}
+uint64_t branch_bits(const Level &lev, uint64_t ch, int c) {
+  uint64_t b = 0;
+  for (int j = 0; j < lev.k; ++j)
+    if ((ch >> (lev.k - 1 - j)) & 1u) b |= 1ull << (c - 1 - lev.cut_g[j]);
+  return b;
+}
+}  // namespace
+
+void Engine::run_tree(int half, const TreeVariant &v, int lz, const std::vector<int> &pin, int m, void *slice,
+                      const uint64_t *dS, int64_t nS) {
+  (void)half;
+  const HalfProgram &hp = v.prog;
+  const int F = (int)hp.levels.size() - 1, c = (int)circ_.cuts.size();
+  std::vector<int> start(F + 2, 0);
+  for (int l = 0; l <= F; ++l) start[l + 1] = start[l] + (int)hp.levels[l].sweeps.size();
+  const int Sm = start[F + 1] - lz;
+  int M = 0;
+  std::vector<int> skip(F + 1, 0);
+  for (int l = 0; l <= F; ++l) {
+    const int n = (int)hp.levels[l].sweeps.size();
+    const int mat = std::max(0, std::min(n, Sm - start[l]));
+    if (mat > 0) M = l;
+    skip[l] = n - mat;
+  }
+  auto run = [&](int l, const Diag &fork, const void *src, void *dst) {
+    const auto &launches = v.plans[l][std::min<size_t>((size_t)skip[l], v.plans[l].size() - 1)];
+    for (size_t i = 0; i < launches.size(); ++i)
+      launch_plan(launches[i], i == 0 ? fork : Diag(), i == 0, i == 0 ? src : dst, dst, hp, -1, &fork);
+  };
+  std::function<void(int, int, uint64_t)> node = [&](int l, int bi, uint64_t bacc) {
+    if (l == M) {
+      gather_tree(v, lz, M, pin, states_[bi]->ptr, bacc, m, slice, dS, nS);
+      return;
+    }
+    const Level &lev = hp.levels[l + 1];
+    const ChildSet cs = child_set(lev, pin);
+    const int di = cs.free.empty() ? bi : bi + 1;
+    for (uint64_t f = 0; f < (1ull << cs.free.size()); ++f) {
+      const uint64_t ch = child_of(lev, cs, f);
+      run(l + 1, hp.fork_diag(l + 1, ch), states_[bi]->ptr, states_[di]->ptr);
+      node(l + 1, di, bacc | branch_bits(lev, ch, c));
+    }
+  };
+  run(0, Diag(), nullptr, states_[0]->ptr);
+  node(0, 0, 0);
+}
+
+// The leaf of a tree path: the last lz sweeps are evaluated at the sampled indices; the forks of
+// the levels that start at a lazy sweep enter that stage's pre diagonal, those of a trailing level
+// without sweeps (cuts never targeted again) its post diagonal; one output row per fork value.
+void Engine::gather_tree(const TreeVariant &v, int lz, int M, const std::vector<int> &pin, const void *psi,
+                         uint64_t bacc, int m, void *slice, const uint64_t *dS, int64_t nS) {
+  const HalfProgram &hp = v.prog;
+  const int F = (int)hp.levels.size() - 1, c = (int)circ_.cuts.size();
+  const uint64_t rmask = m >= 64 ? ~0ull : ((1ull << m) - 1ull);
+  auto row = [&](uint64_t b) { return (char *)slice + (size_t)(b & rmask) * (size_t)nS * amp_; };
+  // lazy stages: (sweep, level whose fork enters its pre or -1)
+  std::vector<std::pair<const Sweep *, int>> st;
+  for (int l = F; l >= 0 && (int)st.size() < lz; --l) {
+    const auto &sw = hp.levels[l].sweeps;
+    for (int i = (int)sw.size() - 1; i >= 0 && (int)st.size() < lz; --i) st.push_back({&sw[i], i == 0 ? l : -1});
+  }
+  std::reverse(st.begin(), st.end());
+  const int pl = (F > M && hp.levels[F].sweeps.empty()) ? F : -1;
+  struct Combo {
+    Diag d[2];
+    uint64_t bits = 0;
+  };
+  auto combos = [&](int l0, int l1) {  // fork values of two levels (-1: none)
+    std::vector<Combo> out(1);
+    const int ls[2] = {l0, l1};
+    for (int t = 0; t < 2; ++t) {
+      if (ls[t] < 0) continue;
+      const Level &lev = hp.levels[ls[t]];
+      const ChildSet cs = child_set(lev, pin);
+      std::vector<Combo> nx;
+      for (const Combo &cb : out)
+        for (uint64_t f = 0; f < (1ull << cs.free.size()); ++f) {
+          Combo x = cb;
+          const uint64_t ch = child_of(lev, cs, f);
+          x.d[t] = hp.fork_diag(ls[t], ch);
+          x.bits |= branch_bits(lev, ch, c);
+          nx.push_back(x);
+        }
+      out.swap(nx);
+    }
+    return out;
+  };
+  auto lazy = [&](const Sweep &sw, const Diag &pre, const Diag &post) {
+    LazyLayer ll = lazy_layer(sw, pre);
+    ll.post = to_dev(post, true);
+    return ll;
+  };
+  if (lz == 0) {
+    for (const Combo &cb : combos(pl, -1)) {
+      check(launch_gather(psi, dS, nS, row(bacc | cb.bits), to_dev(cb.d[0]), c128_, stream_), "gather launch");
+      st_.kernel_launches++;
+    }
+    return;
+  }
+  if (lz == 1) {
+    const Sweep &sw = *st[0].first;
+    for (const Combo &cb : combos(st[0].second, pl)) {
+      const LazyLayer ll = lazy(sw, Diag::merge(sw.pre, cb.d[0]), Diag::merge(sw.post, cb.d[1]));
+      check(launch_gather_layer(psi, dS, nS, row(bacc | cb.bits), ll, c128_, stream_), "gather_layer launch");
+      st_.kernel_launches++;
+      st_.lazy_gathers++;
+    }
+    return;
+  }
+  const Sweep &s1 = *st[0].first, &s2 = *st[1].first;
+  const LazyLayer shape = lazy_layer(s2, s2.pre);
+  const int64_t ncone = nS << shape.k;
+  cone_idx_.reserve((size_t)ncone * 8);
+  cone_val_.reserve((size_t)ncone * amp_);
+  check(launch_cone_indices(dS, nS, shape, cone_idx_.as<uint64_t>(), stream_), "cone launch");
+  st_.kernel_launches++;
+  for (const Combo &ca : combos(st[0].second, -1)) {
+    const LazyLayer l1 = lazy(s1, Diag::merge(s1.pre, ca.d[0]), s1.post);
+    check(launch_gather_layer(psi, cone_idx_.as<uint64_t>(), ncone, cone_val_.ptr, l1, c128_, stream_),
+          "gather_layer launch");
+    st_.kernel_launches++;
+    for (const Combo &cb : combos(st[1].second, pl)) {
+      const LazyLayer l2 = lazy(s2, Diag::merge(s2.pre, cb.d[0]), Diag::merge(s2.post, cb.d[1]));
+      check(launch_gather_layer_compact(cone_val_.ptr, dS, nS, row(bacc | ca.bits | cb.bits), l2, c128_, stream_),
+            "gather_layer_compact launch");
+      st_.kernel_launches++;
+      st_.lazy_gathers++;
+    }
   }
 }
 

@@ -5,6 +5,7 @@
 #include <cstdint>
 #include <cstdlib>
 #include <deque>
+#include <map>
 #include <memory>
 #include <stdexcept>
 #include <string>
@@ -63,8 +64,29 @@ struct Stage {
   Diag diag;
 };
 
+// The branch tree of one half for one placement of its forks (Engine::choose_tree): the
+// program (levels = the distinct fork-apply layers) and its tile plans [level][lazy skip 0..2].
+struct TreeVariant {
+  HalfProgram prog;
+  std::vector<std::vector<std::vector<TilePlan>>> plans;
+};
+
+// Fork placement chosen for one aligned block of branches: apply[g] = layer at whose input cut
+// g's P_b / Z^b is applied; qmask = cuts pinned in addition to the block's fixed top bits (the
+// executor loops over their values); cost in full-sweep units; points = branching levels.
+struct TreeChoice {
+  std::vector<int> apply;
+  std::vector<int> qlist;
+  double cost = 0;
+  int points = 0;
+};
+
 struct HalfExec {
   HalfProgram prog;
+  // deferred-fork trees (non-distributed tree halves): gate layers of the half, first target
+  // layer of every cut, compiled variants by apply vector
+  std::vector<int> glayers, ft;
+  std::map<std::vector<int>, std::unique_ptr<TreeVariant>> variants;
   bool tree = false;                                // tile sweeps (true) or the small kernel
   std::vector<std::vector<std::vector<TilePlan>>> plans;  // [level][lazy skip] -> launches
   // small kernel program on the device
@@ -188,6 +210,19 @@ class Engine {
   void upload_small(HalfExec &he);
   void ensure_states(int half, int nbuf);
   int materialized_from(int half, size_t free_bytes, int *nbuf);
+
+  // deferred-fork tree executor (non-distributed tree halves)
+  void plan_levels(const HalfProgram &hp, std::vector<std::vector<std::vector<TilePlan>>> &plans, bool all_skips);
+  int tree_lazy(int half, int64_t nS) const;
+  TreeChoice choose_tree(int half, int m, int lz, int64_t nS, int nbuf, bool allow_gather) const;
+  TreeVariant &variant(int half, const std::vector<int> &apply);
+  void evolve_tree(int half, uint64_t b0, uint64_t b1, void *slice, const uint64_t *dS, int64_t nS);
+  void evolve_block(int half, uint64_t b0, int m, void *slice, const uint64_t *dS, int64_t nS);
+  void run_tree(int half, const TreeVariant &v, int lz, const std::vector<int> &pin, int m, void *slice,
+                const uint64_t *dS, int64_t nS);
+  void gather_tree(const TreeVariant &v, int lz, int M, const std::vector<int> &pin, const void *psi,
+                   uint64_t bacc, int m, void *slice, const uint64_t *dS, int64_t nS);
+  bool deferred_ = !(std::getenv("QSIM_DEFER") && std::getenv("QSIM_DEFER")[0] == '0');
 
   // executor
   void evolve_half(int half, uint64_t b0, uint64_t b1, void *slice, const uint64_t *dS, int64_t nS);

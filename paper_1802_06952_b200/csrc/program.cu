@@ -204,25 +204,58 @@ HalfProgram compile_half(const Circuit &c, bool upper, const std::vector<int> &p
   return compile_half_layers(c, upper, std::vector<std::vector<int>>(c.depth + 2, p), p);
 }
 
-HalfProgram compile_half_layers(const Circuit &c, bool upper, const std::vector<std::vector<int>> &layer_perm,
-                                const std::vector<int> &final_perm) {
+std::vector<PartCut> half_cuts(const Circuit &c, bool upper) {
   std::vector<PartCut> cuts;
   for (const qsim_cut &cut : c.cuts) cuts.push_back(PartCut{(int)cut.layer, upper ? cut.q_upper : cut.q_lower, upper});
-  return compile_part(c, upper ? 0 : c.h_u, upper ? c.h_u : c.n, upper, cuts, layer_perm, final_perm);
+  return cuts;
+}
+
+HalfProgram compile_half_layers(const Circuit &c, bool upper, const std::vector<std::vector<int>> &layer_perm,
+                                const std::vector<int> &final_perm) {
+  return compile_part(c, upper ? 0 : c.h_u, upper ? c.h_u : c.n, upper, half_cuts(c, upper), layer_perm, final_perm);
+}
+
+std::vector<int> first_targets(const Circuit &c, const std::vector<PartCut> &cuts) {
+  std::vector<int> ft;
+  for (const PartCut &cut : cuts) {
+    int t = (int)c.depth + 1;
+    for (const qsim_gate &g : c.gates)
+      if ((g.kind == QSIM_SX || g.kind == QSIM_SY) && g.q0 == cut.q && (int)g.layer > cut.layer)
+        t = std::min(t, (int)g.layer);
+    ft.push_back(t);
+  }
+  return ft;
+}
+
+std::vector<int> gate_layers(const Circuit &c, uint32_t lo, uint32_t hi) {
+  std::set<int> s;
+  for (const qsim_gate &g : c.gates)
+    if ((g.kind == QSIM_SX || g.kind == QSIM_SY) && g.q0 >= lo && g.q0 < hi) s.insert((int)g.layer);
+  return std::vector<int>(s.begin(), s.end());
 }
 
 HalfProgram compile_part(const Circuit &c, uint32_t lo, uint32_t hi, bool upper, const std::vector<PartCut> &cuts,
-                         const std::vector<std::vector<int>> &layer_perm, const std::vector<int> &final_perm) {
+                         const std::vector<std::vector<int>> &layer_perm, const std::vector<int> &final_perm,
+                         const std::vector<int> *apply) {
   HalfProgram hp;
   hp.upper = upper;
   hp.h = (int)(hi - lo);
   hp.hl = hp.h;
   hp.perm = final_perm;
   hp.ncuts = (int)cuts.size();
-  std::vector<int> fork_layers, fork_k;
-  for (const PartCut &cut : cuts) {
-    if (fork_layers.empty() || fork_layers.back() != cut.layer) {
-      fork_layers.push_back(cut.layer);
+  // forks: the cuts grouped by the layer at whose input they apply (in cut order inside a group)
+  std::vector<int> app(cuts.size());
+  for (size_t i = 0; i < cuts.size(); ++i) {
+    app[i] = apply ? (*apply)[i] : cuts[i].layer + 1;
+    if (app[i] <= cuts[i].layer || app[i] > (int)c.depth + 1) throw std::invalid_argument("fork apply layer");
+  }
+  std::vector<int> order(cuts.size());
+  for (size_t i = 0; i < order.size(); ++i) order[i] = (int)i;
+  std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return app[a] < app[b]; });
+  std::vector<int> fork_layers, fork_k;  // fork_layers: apply layer - 1
+  for (int i : order) {
+    if (fork_layers.empty() || fork_layers.back() != app[i] - 1) {
+      fork_layers.push_back(app[i] - 1);
       fork_k.push_back(0);
     }
     fork_k.back()++;
@@ -262,11 +295,12 @@ HalfProgram compile_part(const Circuit &c, uint32_t lo, uint32_t hi, bool upper,
     if (l > 0) {
       lev.fork_layer = fork_layers[l - 1];
       lev.k = fork_k[l - 1];
-      lev.g0 = g0;
+      lev.g0 = order[g0];
       for (int j = 0; j < lev.k; ++j) {
-        const PartCut &cut = cuts[g0 + j];
+        const PartCut &cut = cuts[order[g0 + j]];
+        lev.cut_g.push_back(order[g0 + j]);
         // the fork acts on the child level's input: the layout of its first layer
-        lev.cut_bits.push_back(bit_at(cut.q, lev.fork_layer + 1));
+        lev.cut_bits.push_back(bit_at(cut.q, std::min(lev.fork_layer + 1, (int)c.depth + 1)));
         if (cut.proj) lev.pmask |= 1u << j;
       }
       g0 += lev.k;

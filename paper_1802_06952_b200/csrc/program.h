@@ -70,9 +70,10 @@ struct Sweep {
 };
 
 struct Level {
-  int fork_layer = 0;          // 0 for the root
+  int fork_layer = 0;          // 0 for the root; the fork applies at the input of layer fork_layer + 1
   int k = 0;                   // cuts at this fork (children = 2^k)
   int g0 = 0;                  // index of the first of them in the cut list
+  std::vector<int> cut_g;      // index in the cut list (= branch bit c-1-g) of fork bit j, ascending
   std::vector<int> cut_bits;   // half-local bit of each cut endpoint in this half
   uint32_t pmask = 0;          // bit j: cut j acts as P_b on this part (upper endpoint), else Z^b
   std::vector<Sweep> sweeps;
@@ -123,8 +124,22 @@ struct PartCut {
 // Program of the qubit range [lo, hi) whose branch index enumerates `cuts` (ordered by
 // (layer, upper qubit); one fork level per distinct layer).  Halves are the case
 // [0, h_u) with every cut as P and [h_u, n) with every cut as Z.
+// apply (optional, one entry per cut): the layer at whose input the cut's P_b / Z^b is applied,
+// in (cut layer, depth + 1] (depth + 1: after the last layer, at the leaf).  Default: the layer
+// after the cut CZ.  A later layer is exact as long as no X^1/2 / Y^1/2 acts on the cut's qubit
+// in between (P_b and Z^b commute with every diagonal and with gates on other qubits): the
+// deferred forks of the tree executor (Engine::choose_tree).
 HalfProgram compile_part(const Circuit &c, uint32_t lo, uint32_t hi, bool upper, const std::vector<PartCut> &cuts,
-                         const std::vector<std::vector<int>> &layer_perm, const std::vector<int> &final_perm);
+                         const std::vector<std::vector<int>> &layer_perm, const std::vector<int> &final_perm,
+                         const std::vector<int> *apply = nullptr);
+
+// Layer of the first X^1/2 / Y^1/2 gate on the cut's qubit after the cut layer (depth + 1: none):
+// the latest layer at whose input the cut's fork may be applied.
+std::vector<int> first_targets(const Circuit &c, const std::vector<PartCut> &cuts);
+// The cut list of a half as PartCuts (P on the upper endpoint, Z on the lower one).
+std::vector<PartCut> half_cuts(const Circuit &c, bool upper);
+// Layers in [1, depth] holding at least one X^1/2 / Y^1/2 gate on a qubit in [lo, hi).
+std::vector<int> gate_layers(const Circuit &c, uint32_t lo, uint32_t hi);
 
 // perm: physical bit of each canonical local bit (identity when empty); every bit position of the
 // program (gates, diagonals, forks) is physical.
