@@ -1819,15 +1819,15 @@ void Engine::synchronize() {
 // ---------------------------------------------------------------- level-synchronous tree (BFS)
 // Node-batched launch of one planned sweep over 2^log2_nodes states (TMA kernel only).
 void Engine::launch_nodes(const TilePlan &tp, const void *src, void *dst, int log2_nodes, int shift,
-                          const ForkDev &fork, const HalfProgram &hp, bool apply_fork, uint32_t proj_bits) {
+                          const ForkDev &fork, const HalfProgram &hp, bool apply_fork, uint32_t proj_bits,
+                          const Diag *extra_pre) {
   if (tp.fused || tp.gen || !tp.swaps.empty()) throw Error(QSIM_EINVAL, "node-batched sweep of an unsupported plan");
   const int h = hp.hl;
   int pre_mode = 0;
   Diag pre;
-  if (tp.use_pre) {
-    pre = tp.pre;
-    if (!pre.identity()) pre_mode = 1;
-  }
+  if (tp.use_pre) pre = tp.pre;
+  if (extra_pre && apply_fork) pre = Diag::merge(pre, *extra_pre);
+  if (!pre.identity()) pre_mode = 1;
   const bool timed = time_sweeps_;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (timed) {
@@ -2178,9 +2178,15 @@ void Engine::evolve_block(int half, uint64_t b0, int m, void *slice, const uint6
   const int T = tile_low_bits(c128_) + kHiBits;
   if (he.prog.hl < T) throw Error(QSIM_EINVAL, "tree mode needs h >= tile bits");
   state_bytes_ = ((size_t)1 << he.prog.hl) * amp_;
+  // level-synchronous subtrees for small states (launch-bound otherwise): gather forks pinned
+  const bool bfs = bfs_ && !fuse_layers_ && sweep_kernel_ != 1 && state_bytes_ <= ((size_t)256 << 20);
+  if (!bfs) {  // their buffers are state memory now
+    bfs_buf_[0].release();
+    bfs_buf_[1].release();
+  }
   size_t free_b = 0, total_b = 0;
   check(cudaMemGetInfo(&free_b, &total_b), "cudaMemGetInfo");
-  size_t have = 0;
+  size_t have = bfs_buf_[0].bytes + bfs_buf_[1].bytes;
   for (auto *b : states_) have += b->bytes;
   const int lz = tree_lazy(half, nS);
   size_t margin = (size_t)512 << 20;
@@ -2195,9 +2201,15 @@ void Engine::evolve_block(int half, uint64_t b0, int m, void *slice, const uint6
   }
   int nbuf = (int)std::min<size_t>(nfit, 12);
   if (mem_budget_ > 0) nbuf = std::max(1, std::min<int>(nbuf, (int)((size_t)mem_budget_ / state_bytes_)));
-  const TreeChoice tc = choose_tree(half, m, lz, nS, nbuf, true);
+  const TreeChoice tc = choose_tree(half, m, lz, nS, nbuf, !bfs);
   const TreeVariant &v = variant(half, tc.apply);
   ensure_states(half, tc.points + 1);
+  size_t bfs_avail = 0;  // memory the level-synchronous buffers may take (0: none)
+  if (bfs) {
+    size_t used = 0;
+    for (auto *b : states_) used += b->bytes;
+    bfs_avail = avail > used ? avail - used : 1;
+  }
   if (std::getenv("QSIM_DEBUG_TREE")) {
     std::fprintf(stderr, "tree half %d b0=%llu m=%d lz=%d nbuf=%d: cost %.1f sweeps, %d points, %zu pinned, levels",
                  half, (unsigned long long)b0, m, lz, nbuf, tc.cost, tc.points, tc.qlist.size());
@@ -2209,7 +2221,7 @@ void Engine::evolve_block(int half, uint64_t b0, int m, void *slice, const uint6
   const size_t nq = tc.qlist.size();
   for (uint64_t q = 0; q < (1ull << nq); ++q) {
     for (size_t i = 0; i < nq; ++i) pin[tc.qlist[i]] = (int)((q >> i) & 1u);
-    run_tree(half, v, lz, pin, m, slice, dS, nS);
+    run_tree(half, v, lz, pin, m, slice, dS, nS, bfs_avail);
   }
 }
 
@@ -2245,8 +2257,172 @@ uint64_t branch_bits(const Level &lev, uint64_t ch, int c) {
 }
 }  // namespace
 
+namespace {
+// diagonal of the pinned fork bits of a level (free bits left out)
+Diag pinned_diag(const Level &lev, const std::vector<int> &pin) {
+  Diag d;
+  for (int j = 0; j < lev.k; ++j) {
+    const int p = pin[lev.cut_g[j]];
+    if (p < 0) continue;
+    if ((lev.pmask >> j) & 1u)
+      d.add_proj(lev.cut_bits[j], p);
+    else if (p)
+      d.add_Z(lev.cut_bits[j]);
+  }
+  return d;
+}
+// lazy stages of a tree path: (sweep, level whose fork enters its pre or -1), the last lz sweeps
+std::vector<std::pair<const Sweep *, int>> lazy_stages(const HalfProgram &hp, int lz) {
+  std::vector<std::pair<const Sweep *, int>> st;
+  for (int l = (int)hp.levels.size() - 1; l >= 0 && (int)st.size() < lz; --l) {
+    const auto &sw = hp.levels[l].sweeps;
+    for (int i = (int)sw.size() - 1; i >= 0 && (int)st.size() < lz; --i) st.push_back({&sw[i], i == 0 ? l : -1});
+  }
+  std::reverse(st.begin(), st.end());
+  return st;
+}
+}  // namespace
+
+// The subtree below a level-l node, level by level (SURVEY §8(a) a4 for small states, where one
+// launch per node and sweep is launch-bound): the sweeps of level q run as ONE node-batched launch
+// over its 2^{free bits of levels l+1..q} states (node = (parent << n) | child; the first launch
+// reads the parent and applies the fork per node, the pinned bits' diagonal merged into its pre);
+// the leaves are gathered by batched launches whose output rows follow the branch order.  Needs
+// the gather forks pinned (choose_tree with allow_gather = false).  false: does not fit.
+bool Engine::bfs_tree(const TreeVariant &v, int lz, int M, const std::vector<int> &skip, const std::vector<int> &pin,
+                      int l, const void *state, uint64_t bacc, int m, void *slice, const uint64_t *dS, int64_t nS,
+                      size_t avail) {
+  const HalfProgram &hp = v.prog;
+  const int F = (int)hp.levels.size() - 1, c = (int)circ_.cuts.size();
+  std::vector<ChildSet> cs(M + 1);
+  std::vector<int> sb(M + 1, 0);
+  for (int q = l + 1; q <= M; ++q) {
+    cs[q] = child_set(hp.levels[q], pin);
+    sb[q] = sb[q - 1] + (int)cs[q].free.size();
+  }
+  const int nb = sb[M];
+  if (nb < 1 || nb > 30) return false;
+  for (int q = M + 1; q <= F; ++q)
+    if (!child_set(hp.levels[q], pin).free.empty()) return false;
+  for (int q = l + 1; q <= M; ++q) {
+    const auto &launches = v.plans[q][std::min<size_t>((size_t)skip[q], v.plans[q].size() - 1)];
+    if (launches.empty()) return false;
+    for (const TilePlan &tp : launches)
+      if (tp.fused || tp.gen || !tp.swaps.empty()) return false;
+  }
+  size_t need[2] = {0, 0};
+  for (int q = l + 1; q <= M; ++q) need[q & 1] = std::max(need[q & 1], state_bytes_ << sb[q]);
+  const size_t extra = ((size_t)256 << 20) + (lz == 2 ? ((size_t)1 << 30) : 0);  // + the lazy cone chunk
+  if (need[0] + need[1] + extra > avail) return false;
+  // avail counts the buffers already held as reclaimable: drop them when growing in place would not fit
+  if (std::max(bfs_buf_[0].bytes, need[0]) + std::max(bfs_buf_[1].bytes, need[1]) + extra > avail) {
+    bfs_buf_[0].release();
+    bfs_buf_[1].release();
+  }
+  bfs_buf_[0].reserve(need[0]);
+  bfs_buf_[1].reserve(need[1]);
+  const void *src = state;
+  for (int q = l + 1; q <= M; ++q) {
+    const Level &lev = hp.levels[q];
+    const auto &launches = v.plans[q][std::min<size_t>((size_t)skip[q], v.plans[q].size() - 1)];
+    void *dst = bfs_buf_[q & 1].ptr;
+    ForkDev f;
+    std::memset(&f, 0, sizeof(f));
+    f.n = (int)cs[q].free.size();
+    uint32_t proj = 0;
+    for (int t = 0; t < f.n; ++t) {
+      const int j = cs[q].free[t];
+      f.bit[t] = (uint8_t)lev.cut_bits[j];
+      if ((lev.pmask >> j) & 1u) {
+        f.pmask |= 1u << t;
+        proj |= 1u << lev.cut_bits[j];
+      }
+    }
+    const Diag pinned = pinned_diag(lev, pin);
+    for (size_t i = 0; i < launches.size(); ++i)
+      launch_nodes(launches[i], i == 0 ? src : dst, dst, sb[q], i == 0 ? f.n : 0, f, hp, i == 0, proj,
+                   i == 0 ? &pinned : nullptr);
+    src = dst;
+  }
+  // leaf node N (bits of level q's fork entry t at N's bit (sb[M] - sb[q]) + (n_q - 1 - t)) -> row
+  RowMapDev rm;
+  std::memset(&rm, 0, sizeof(rm));
+  rm.nbits = nb;
+  uint64_t fixed = bacc;
+  for (int q = l + 1; q <= F; ++q) fixed |= branch_bits(hp.levels[q], child_set(hp.levels[q], pin).base, c);
+  const uint64_t rmask = m >= 64 ? ~0ull : ((1ull << m) - 1ull);
+  rm.base = (uint32_t)(fixed & rmask);
+  for (int q = l + 1; q <= M; ++q) {
+    const int n = (int)cs[q].free.size();
+    for (int t = 0; t < n; ++t) {
+      const int nbit = (sb[M] - sb[q]) + (n - 1 - t);
+      rm.pos[nbit] = (uint8_t)(c - 1 - hp.levels[q].cut_g[cs[q].free[t]]);
+    }
+  }
+  const int64_t nleaves = (int64_t)1 << nb;
+  rowmap_.reserve((size_t)nleaves * 4);
+  check(launch_rowmap(rowmap_.as<uint32_t>(), nleaves, rm, stream_), "rowmap launch");
+  st_.kernel_launches++;
+  // gather: forks of the gather levels are pinned (constant diagonals)
+  const auto st = lazy_stages(hp, lz);
+  const int pl = (F > M && hp.levels[F].sweeps.empty()) ? F : -1;
+  auto fork_of = [&](int q) { return q < 0 ? Diag() : pinned_diag(hp.levels[q], pin); };
+  const uint64_t stride = (uint64_t)1 << hp.hl;
+  if (lz == 0) {
+    ForkDev f0;
+    std::memset(&f0, 0, sizeof(f0));
+    const DiagDev pend = to_dev(fork_of(pl));
+    check(launch_gather_nodes(src, stride, 0, nleaves, dS, nS, slice, f0, c128_, stream_, &pend, rowmap_.as<uint32_t>()),
+          "gather nodes launch");
+    st_.kernel_launches++;
+    return true;
+  }
+  auto lazy = [&](const Sweep &sw, const Diag &pre, const Diag &post) {
+    LazyLayer ll = lazy_layer(sw, pre);
+    ll.post = to_dev(post, true);
+    ll.node_stride = stride;
+    return ll;
+  };
+  if (lz == 1) {
+    const Sweep &sw = *st[0].first;
+    LazyLayer ll = lazy(sw, Diag::merge(sw.pre, fork_of(st[0].second)), Diag::merge(sw.post, fork_of(pl)));
+    ll.nper = nS;
+    ll.rowmap = rowmap_.as<uint32_t>();
+    check(launch_gather_layer(src, dS, nS * nleaves, slice, ll, c128_, stream_), "gather_layer launch");
+    st_.kernel_launches++;
+    st_.lazy_gathers += (uint64_t)nleaves;
+    return true;
+  }
+  const Sweep &s1 = *st[0].first, &s2 = *st[1].first;
+  LazyLayer l1 = lazy(s1, Diag::merge(s1.pre, fork_of(st[0].second)), s1.post);
+  LazyLayer l2 = lazy(s2, Diag::merge(s2.pre, fork_of(st[1].second)), Diag::merge(s2.post, fork_of(pl)));
+  const int64_t ncone = nS << l2.k;
+  cone_idx_.reserve((size_t)ncone * 8);
+  check(launch_cone_indices(dS, nS, l2, cone_idx_.as<uint64_t>(), stream_), "cone launch");
+  st_.kernel_launches++;
+  // leaves in chunks whose cone values fit in 1 GiB
+  const int64_t per = std::max<int64_t>(1, ((int64_t)1 << 30) / (ncone * (int64_t)amp_));
+  int64_t chunk = 1;
+  while (chunk * 2 <= per && chunk < nleaves) chunk *= 2;
+  cone_val_.reserve((size_t)(ncone * std::min(chunk, nleaves)) * amp_);
+  for (int64_t a = 0; a < nleaves; a += chunk) {
+    const int64_t cl = std::min(chunk, nleaves - a);
+    l1.nper = ncone;
+    check(launch_gather_layer((const char *)src + (size_t)a * stride * amp_, cone_idx_.as<uint64_t>(), ncone * cl,
+                              cone_val_.ptr, l1, c128_, stream_),
+          "gather_layer launch");
+    l2.nper = nS;
+    l2.rowmap = rowmap_.as<uint32_t>() + a;
+    check(launch_gather_layer_compact(cone_val_.ptr, dS, nS * cl, slice, l2, c128_, stream_),
+          "gather_layer_compact launch");
+    st_.kernel_launches += 2;
+  }
+  st_.lazy_gathers += (uint64_t)nleaves;
+  return true;
+}
+
 void Engine::run_tree(int half, const TreeVariant &v, int lz, const std::vector<int> &pin, int m, void *slice,
-                      const uint64_t *dS, int64_t nS) {
+                      const uint64_t *dS, int64_t nS, size_t bfs_avail) {
   (void)half;
   const HalfProgram &hp = v.prog;
   const int F = (int)hp.levels.size() - 1, c = (int)circ_.cuts.size();
@@ -2271,6 +2447,7 @@ void Engine::run_tree(int half, const TreeVariant &v, int lz, const std::vector<
       gather_tree(v, lz, M, pin, states_[bi]->ptr, bacc, m, slice, dS, nS);
       return;
     }
+    if (bfs_avail && bfs_tree(v, lz, M, skip, pin, l, states_[bi]->ptr, bacc, m, slice, dS, nS, bfs_avail)) return;
     const Level &lev = hp.levels[l + 1];
     const ChildSet cs = child_set(lev, pin);
     const int di = cs.free.empty() ? bi : bi + 1;
@@ -2293,13 +2470,7 @@ void Engine::gather_tree(const TreeVariant &v, int lz, int M, const std::vector<
   const int F = (int)hp.levels.size() - 1, c = (int)circ_.cuts.size();
   const uint64_t rmask = m >= 64 ? ~0ull : ((1ull << m) - 1ull);
   auto row = [&](uint64_t b) { return (char *)slice + (size_t)(b & rmask) * (size_t)nS * amp_; };
-  // lazy stages: (sweep, level whose fork enters its pre or -1)
-  std::vector<std::pair<const Sweep *, int>> st;
-  for (int l = F; l >= 0 && (int)st.size() < lz; --l) {
-    const auto &sw = hp.levels[l].sweeps;
-    for (int i = (int)sw.size() - 1; i >= 0 && (int)st.size() < lz; --i) st.push_back({&sw[i], i == 0 ? l : -1});
-  }
-  std::reverse(st.begin(), st.end());
+  const auto st = lazy_stages(hp, lz);
   const int pl = (F > M && hp.levels[F].sweeps.empty()) ? F : -1;
   struct Combo {
     Diag d[2];

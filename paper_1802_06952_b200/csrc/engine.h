@@ -219,9 +219,14 @@ class Engine {
   void evolve_tree(int half, uint64_t b0, uint64_t b1, void *slice, const uint64_t *dS, int64_t nS);
   void evolve_block(int half, uint64_t b0, int m, void *slice, const uint64_t *dS, int64_t nS);
   void run_tree(int half, const TreeVariant &v, int lz, const std::vector<int> &pin, int m, void *slice,
-                const uint64_t *dS, int64_t nS);
+                const uint64_t *dS, int64_t nS, size_t bfs_avail);
   void gather_tree(const TreeVariant &v, int lz, int M, const std::vector<int> &pin, const void *psi,
                    uint64_t bacc, int m, void *slice, const uint64_t *dS, int64_t nS);
+  // level-synchronous subtree of a tree path below level l (node-batched sweeps; small states)
+  bool bfs_tree(const TreeVariant &v, int lz, int M, const std::vector<int> &skip, const std::vector<int> &pin,
+                int l, const void *state, uint64_t bacc, int m, void *slice, const uint64_t *dS, int64_t nS,
+                size_t avail);
+  DevBuf rowmap_;
   bool deferred_ = !(std::getenv("QSIM_DEFER") && std::getenv("QSIM_DEFER")[0] == '0');
 
   // executor
@@ -231,7 +236,8 @@ class Engine {
   int bfs_level(int half, int m0, size_t avail) const;
   void bfs_subtree(int half, int m, const void *state, void *out, const uint64_t *dS, int64_t nS);
   void launch_nodes(const TilePlan &tp, const void *src, void *dst, int log2_nodes, int shift, const ForkDev &fork,
-                    const HalfProgram &hp, bool apply_fork = true, uint32_t proj_bits = 0);
+                    const HalfProgram &hp, bool apply_fork = true, uint32_t proj_bits = 0,
+                    const Diag *extra_pre = nullptr);
   bool bfs_ = true;  // QSIM_OPT_BFS: level-synchronous subtrees for small states
   // generated (write-only) sweeps through the TMA kernel's PRE = 2 variant (QSIM_GEN_TMA=0: the
   // register kernel, A/B only)

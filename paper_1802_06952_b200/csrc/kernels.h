@@ -199,9 +199,18 @@ cudaError_t launch_gather(const void *psi, const uint64_t *S, int64_t n, void *o
                           const DiagDev &pend, bool c128, cudaStream_t s, uint64_t lmask = ~0ull,
                           uint64_t gsel = 0);
 
-// Leaves of a node-batched level: out[node * n + j] = fork(node, S[j]) * psi[(node >> shift) * stride + S[j]]
+// Leaves of a node-batched level: out[row(node) * n + j] = pend(S[j]) fork(node, S[j]) *
+// psi[(node >> shift) * stride + S[j]], row(node) = rowmap ? rowmap[node] : node
 cudaError_t launch_gather_nodes(const void *psi, uint64_t stride, int shift, int64_t nnodes, const uint64_t *S,
-                                int64_t n, void *out, const ForkDev &fork, bool c128, cudaStream_t s);
+                                int64_t n, void *out, const ForkDev &fork, bool c128, cudaStream_t s,
+                                const DiagDev *pend = nullptr, const uint32_t *rowmap = nullptr);
+// Output rows of node-batched leaves: out[N] = base | sum_t ((N >> t) & 1) << pos[t]
+struct RowMapDev {
+  int32_t nbits;
+  uint32_t base;
+  uint8_t pos[32];
+};
+cudaError_t launch_rowmap(uint32_t *out, int64_t n, const RowMapDev &rm, cudaStream_t s);
 // Lazy last layer: the leaf's final sweep evaluated only at the sampled indices,
 //   out[j] = post(x) * sum_y  prod_t M'_t[x_t, y_t] * pre(y) * psi[y],   x = S[j],
 // y ranging over the 2^k values of the sweep's target bits (others equal to x).
@@ -214,9 +223,10 @@ struct LazyLayer {
   // layer's targets are local, so every term of an owned index is in the shard); others give 0
   uint64_t lmask, gsel;
   // node batching (level-synchronous leaves): node_stride > 0 -> output j covers node j / nper of
-  // states psi + node * node_stride at index S[j % nper]
+  // states psi + node * node_stride at index S[j % nper]; its output row is rowmap[node] (when set)
   uint64_t node_stride;
   int64_t nper;
+  const uint32_t *rowmap;
 };
 cudaError_t launch_gather_layer(const void *psi, const uint64_t *S, int64_t n, void *out,
                                 const LazyLayer &ll, bool c128, cudaStream_t s);

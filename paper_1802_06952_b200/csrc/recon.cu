@@ -6,6 +6,7 @@
 // blocks this is the complex contraction over the branch index b,
 //     A[i, j] = sum_b U[b, i] * L[b, j].
 #include <algorithm>
+#include <cstring>
 
 #include "sweep_common.cuh"
 
@@ -66,13 +67,25 @@ cudaError_t launch_gather(const void *psi, const uint64_t *S, int64_t n, void *o
 template <typename R>
 __global__ void gather_nodes_kernel(const typename CxT<R>::T *__restrict__ psi, uint64_t stride, int shift,
                                     int64_t nnodes, const uint64_t *__restrict__ S, int64_t n,
-                                    typename CxT<R>::T *__restrict__ out, const __grid_constant__ ForkDev f) {
+                                    typename CxT<R>::T *__restrict__ out, const __grid_constant__ ForkDev f,
+                                    const DiagDev d, const uint32_t *__restrict__ rowmap) {
   using C = typename CxT<R>::T;
   const int64_t total = nnodes * n;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t node = e / n;
-    const uint64_t x = S[e - node * n];
+    const int64_t jj = e - node * n;
+    const uint64_t x = S[jj];
     C v = psi[(uint64_t)(node >> shift) * stride + x];
+    if (d.active) {
+      const uint32_t ii = (uint32_t)x;
+      const int ph = diag_phase(ii, d, d.zm);
+      const R wr = (R)(c_omega[2 * ph] * d.scale), wi = (R)(c_omega[2 * ph + 1] * d.scale);
+      C y;
+      y.x = v.x * wr - v.y * wi;
+      y.y = v.x * wi + v.y * wr;
+      if ((ii & d.pm) != d.pv) y.x = y.y = (R)0;
+      v = y;
+    }
     bool zero = false, neg = false;
     for (int j = 0; j < f.n; ++j) {
       const uint64_t cb = ((uint64_t)node >> (f.n - 1 - j)) & 1u, xb = (x >> f.bit[j]) & 1u;
@@ -86,21 +99,40 @@ __global__ void gather_nodes_kernel(const typename CxT<R>::T *__restrict__ psi, 
       v.x = -v.x;
       v.y = -v.y;
     }
-    out[e] = v;
+    out[(rowmap ? (int64_t)rowmap[node] : node) * n + jj] = v;
   }
 }
 
 cudaError_t launch_gather_nodes(const void *psi, uint64_t stride, int shift, int64_t nnodes, const uint64_t *S,
-                                int64_t n, void *out, const ForkDev &fork, bool c128, cudaStream_t s) {
+                                int64_t n, void *out, const ForkDev &fork, bool c128, cudaStream_t s,
+                                const DiagDev *pend, const uint32_t *rowmap) {
   const int64_t total = nnodes * n;
   if (total <= 0) return cudaSuccess;
   const int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 16);
+  DiagDev d;
+  std::memset(&d, 0, sizeof(d));
+  if (pend) d = *pend;
   if (c128)
     gather_nodes_kernel<double><<<blocks, 256, 0, s>>>((const double2 *)psi, stride, shift, nnodes, S, n,
-                                                       (double2 *)out, fork);
+                                                       (double2 *)out, fork, d, rowmap);
   else
     gather_nodes_kernel<float><<<blocks, 256, 0, s>>>((const float2 *)psi, stride, shift, nnodes, S, n,
-                                                      (float2 *)out, fork);
+                                                      (float2 *)out, fork, d, rowmap);
+  return cudaGetLastError();
+}
+
+__global__ void rowmap_kernel(uint32_t *__restrict__ out, int64_t n, const __grid_constant__ RowMapDev rm) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t r = rm.base;
+    for (int t = 0; t < rm.nbits; ++t) r |= (uint32_t)((e >> t) & 1) << rm.pos[t];
+    out[e] = r;
+  }
+}
+
+cudaError_t launch_rowmap(uint32_t *out, int64_t n, const RowMapDev &rm, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  const int blocks = (int)std::min<int64_t>((n + 255) / 256, 148 * 8);
+  rowmap_kernel<<<blocks, 256, 0, s>>>(out, n, rm);
   return cudaGetLastError();
 }
 
@@ -122,12 +154,14 @@ __global__ void __launch_bounds__(256) gather_layer_kernel(const typename CxT<R>
   const bool valid = j < n;
   bool own = false;
   uint32_t x = 0;
+  int64_t jo = j;  // output index
   if (valid) {
     int64_t jj = j;
     if (ll.node_stride) {  // node-batched leaves
       const int64_t node = j / ll.nper;
       jj = j - node * ll.nper;
       psi += (uint64_t)node * ll.node_stride;
+      if (ll.rowmap) jo = (int64_t)ll.rowmap[node] * ll.nper + jj;
     }
     const uint64_t xs = S[jj];
     own = (xs & ~ll.lmask) == ll.gsel;  // else another shard's index (distributed half)
@@ -157,7 +191,7 @@ __global__ void __launch_bounds__(256) gather_layer_kernel(const typename CxT<R>
   }
   if (sub == 0 && valid) {
     if (!own) {
-      out[j].x = out[j].y = (R)0;
+      out[jo].x = out[jo].y = (R)0;
       return;
     }
     const double pre_scale = ll.pre.active ? ll.pre.scale : 1.0;
@@ -168,7 +202,7 @@ __global__ void __launch_bounds__(256) gather_layer_kernel(const typename CxT<R>
     o.x = sr * wr - si * wi;
     o.y = sr * wi + si * wr;
     if ((x & ll.post.pm) != ll.post.pv) o.x = o.y = (R)0;
-    out[j] = o;
+    out[jo] = o;
   }
 }
 
@@ -215,8 +249,9 @@ __global__ void __launch_bounds__(256) gather_layer_compact_kernel(const typenam
   const int64_t j = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (j >= n) return;
   const int64_t jj = ll.node_stride ? j % ll.nper : j;  // node-batched: V, out are [node][nper]
+  const int64_t jo = (ll.node_stride && ll.rowmap) ? (int64_t)ll.rowmap[j / ll.nper] * ll.nper + jj : j;
   if ((S[jj] & ~ll.lmask) != ll.gsel) {  // another shard's index
-    if (lane == 0) out[j].x = out[j].y = (R)0;
+    if (lane == 0) out[jo].x = out[jo].y = (R)0;
     return;
   }
   const uint32_t x = (uint32_t)S[jj];
@@ -252,7 +287,7 @@ __global__ void __launch_bounds__(256) gather_layer_compact_kernel(const typenam
     o.x = sr * wr - si * wi;
     o.y = sr * wi + si * wr;
     if ((x & ll.post.pm) != ll.post.pv) o.x = o.y = (R)0;
-    out[j] = o;
+    out[jo] = o;
   }
 }
 
