@@ -105,7 +105,13 @@ typedef enum {
                                 ONE node-batched launch over every state of the level (the fork's P / Z
                                 applied per node inside the sweep), leaves gathered in one launch (or
                                 per leaf with the lazy tail when the subtree has <= 4096 leaves);
-                                0: one launch per node and sweep                                      */
+                                0: one launch per node and sweep                                      */,
+  QSIM_OPT_MAX_CTAS = 9,     /* test only: cap on the persistent grid of the TMA sweeps (0 = one CTA per
+                                SM, the default), so that small states run many tiles per CTA (mbarrier
+                                phase wrap, stage rotation) in the parity tests                       */
+  QSIM_OPT_DEFER = 10        /* 1 (default): deferred forks — each cut's P_b / Z^b is applied at the first
+                                layer that targets its qubit (branches share their state until then,
+                                DESIGN.md §5); 0: at the layer after the cut (A/B and tests)          */
 } qsim_option;
 
 /* Create a context bound to CUDA device `device` (no device call is made until the
@@ -228,6 +234,24 @@ qsim_status qsim_branch_sum(qsim_ctx *ctx, const void *U, const void *L, size_t 
  *  half: 0 = upper, 1 = lower; out: host, 2^h complex of the ctx precision.
  *  For spot checks at full size.  ESTATE without circuit. */
 qsim_status qsim_branch_state(qsim_ctx *ctx, int half, uint64_t branch, void *out);
+
+/* qsim_branch_values — U_b[idx[j]] (half 0) or L_b[idx[j]] (half 1) for one branch b, computed by
+ * the production path of qsim_evolve_range (deferred forks, lazy tail, gathers) with idx as the
+ * sampled block: the a3-a5 half of one row of the reconstruction.
+ *  idx: host, n canonical half indices (< 2^h, any order, repeats allowed); out: host, n complex
+ *  of the ctx precision.  For full-size spot checks (h = 24-32) where the complete leaf of
+ *  qsim_branch_state does not fit.  EINVAL on a bad half / branch / index, ESTATE without circuit. */
+qsim_status qsim_branch_values(qsim_ctx *ctx, int half, uint64_t branch, const uint64_t *idx, size_t n, void *out);
+
+/* qsim_info — what the context holds, so that callers can size and check their buffers. */
+typedef struct {
+  uint32_t precision;     /* qsim_precision: amplitudes are complex64 (0) or complex128 (1)     */
+  uint32_t have_circuit;  /* 1 after a successful qsim_load_circuit                             */
+  uint32_t h_upper, h_lower, n_cuts;
+  uint64_t n_upper, n_lower; /* sizes of the current blocks (0: none set)                        */
+  int32_t device;
+} qsim_info_t;
+qsim_status qsim_info(qsim_ctx *ctx, qsim_info_t *out);
 
 /* Multi-GPU (one process per GPU).  qsim_nccl_unique_id writes 128 bytes
  * (ncclUniqueId) on rank 0; every rank passes the same bytes to qsim_comm_init, which records

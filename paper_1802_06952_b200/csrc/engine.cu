@@ -213,6 +213,14 @@ void Engine::set_option(int key, int64_t value) {
       if (value < 0 || value > 1) throw Error(QSIM_EINVAL, "QSIM_OPT_BFS must be 0 or 1");
       bfs_ = value != 0;
       return;
+    case QSIM_OPT_MAX_CTAS:
+      if (value < 0 || value > 100000) throw Error(QSIM_EINVAL, "QSIM_OPT_MAX_CTAS must be >= 0");
+      max_ctas_ = (int)value;
+      return;
+    case QSIM_OPT_DEFER:
+      if (value < 0 || value > 1) throw Error(QSIM_EINVAL, "QSIM_OPT_DEFER must be 0 or 1");
+      deferred_ = value != 0;
+      return;
     case QSIM_OPT_SWEEP_KERNEL:
       if (value < 0 || value > 3) throw Error(QSIM_EINVAL, "QSIM_OPT_SWEEP_KERNEL must be 0, 1, 2 or 3");
       sweep_kernel_ = (int)value;
@@ -1063,7 +1071,7 @@ void Engine::launch_plan(const TilePlan &tp, const Diag &fork, bool first, const
     if (pre_mode == 1) f.pre_s = make_split(pre, tp.pass0_regs);
     f.src = src;
     f.dst = dst;
-    const int grid = (int)std::min<uint64_t>(1ull << f.log2_ntiles, (uint64_t)num_sms_);
+    const int grid = (int)std::min<uint64_t>(1ull << f.log2_ntiles, (uint64_t)grid_ctas());
     check(launch_fused_sweep(f, c128_, pre_mode, grid, stream_, tp.multi_layer), "fused sweep launch");
   } else {
     TileSweepParams p = tp.p;
@@ -1097,7 +1105,7 @@ void Engine::launch_plan(const TilePlan &tp, const Diag &fork, bool first, const
     const bool tma = (sweep_kernel_ != 1 || p.nswap) && (pre_mode != 2 || (gen_tma_ && !dist_));
     if (tma) {
       if (pre_mode >= 1) p.pre_s = make_split(pre, reg_positions(p, 0, c128_));
-      const int grid = (int)std::min<uint64_t>(tiles, (uint64_t)num_sms_);
+      const int grid = (int)std::min<uint64_t>(tiles, (uint64_t)grid_ctas());
       const int stages = sweep_kernel_ == 2 ? 2 : sweep_kernel_ == 3 ? 3 : tma_stages(tp);
       check(launch_tile_sweep_tma(p, c128_, pre_mode, tp.npass, grid, stream_, stages),
             "tma sweep launch");
@@ -1647,6 +1655,54 @@ void Engine::branch_state(int half, uint64_t b, void *out) {
   check(cudaStreamSynchronize(stream_), "branch_state");
 }
 
+void Engine::branch_values(int half, uint64_t b, const uint64_t *idx, size_t n, void *out) {
+  if (!have_circuit_) throw Error(QSIM_ESTATE, "no circuit loaded");
+  if (half != 0 && half != 1) throw Error(QSIM_EINVAL, "half must be 0 (upper) or 1 (lower)");
+  const int c = (int)circ_.cuts.size();
+  if (c > 62 || b >= (1ull << c)) throw Error(QSIM_EINVAL, "branch out of range");
+  if (!out || !idx || n == 0) throw Error(QSIM_EINVAL, "empty index list");
+  HalfExec &he = half_[half];
+  const int h = he.prog.h;
+  std::vector<uint64_t> P(n);
+  for (size_t i = 0; i < n; ++i) {
+    if (idx[i] >> h) throw Error(QSIM_EINVAL, "index >= 2^h");
+    P[i] = he.prog.phys(idx[i]);
+  }
+  ensure_device();
+  DevBuf dS, slice;
+  dS.reserve(n * 8);
+  slice.reserve(n * amp_);
+  check(cudaMemcpyAsync(dS.ptr, P.data(), n * 8, cudaMemcpyHostToDevice, stream_), "upload idx");
+  if (deferred_ && !dist_ && he.tree)
+    evolve_tree(half, b, b + 1, slice.ptr, dS.as<uint64_t>(), (int64_t)n);
+  else
+    evolve_half(half, b, b + 1, slice.ptr, dS.as<uint64_t>(), (int64_t)n);
+  if (dist_ && world_ > 1) {
+    ensure_comm();
+    ncclResult_t r = ncclAllReduce(slice.ptr, slice.ptr, n * 2, c128_ ? ncclDouble : ncclFloat, ncclSum, comm_,
+                                   stream_);
+    if (r != ncclSuccess) throw Error(QSIM_ENCCL, std::string("ncclAllReduce: ") + ncclGetErrorString(r));
+  }
+  check(cudaMemcpyAsync(out, slice.ptr, n * amp_, cudaMemcpyDeviceToHost, stream_), "D2H values");
+  check(cudaStreamSynchronize(stream_), "branch_values");
+}
+
+void Engine::info(qsim_info_t *out) const {
+  std::memset(out, 0, sizeof(*out));
+  out->precision = (uint32_t)prec_;
+  out->have_circuit = have_circuit_ ? 1u : 0u;
+  if (have_circuit_) {
+    out->h_upper = circ_.h_u;
+    out->h_lower = circ_.h_l;
+    out->n_cuts = (uint32_t)circ_.cuts.size();
+  }
+  if (have_blocks_) {
+    out->n_upper = Su_.size();
+    out->n_lower = Sl_.size();
+  }
+  out->device = device_;
+}
+
 // ---------------------------------------------------------------- distributed half (f3)
 // Level buffers for sharded half states, and every rank's device pointers to them (CUDA IPC
 // handles exchanged with an NCCL all-gather), for the sweeps that store into a peer's shard.
@@ -1854,7 +1910,7 @@ void Engine::launch_nodes(const TilePlan &tp, const void *src, void *dst, int lo
   }
   if (pre_mode == 1) p.pre_s = make_split(pre, reg_positions(p, 0, c128_));
   const uint64_t tiles = 1ull << (p.log2_ntiles + log2_nodes);
-  const int grid = (int)std::min<uint64_t>(tiles, (uint64_t)num_sms_);
+  const int grid = (int)std::min<uint64_t>(tiles, (uint64_t)grid_ctas());
   const int stages = sweep_kernel_ == 2 ? 2 : sweep_kernel_ == 3 ? 3 : tma_stages(tp);
   check(launch_tile_sweep_tma(p, c128_, pre_mode, tp.npass, grid, stream_, stages), "node-batched sweep launch");
   if (timed) {

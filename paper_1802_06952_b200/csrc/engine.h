@@ -2,6 +2,7 @@
 // sampling, NCCL reduction of partial amplitude blocks.
 #pragma once
 
+#include <algorithm>
 #include <cstdint>
 #include <cstdlib>
 #include <deque>
@@ -118,6 +119,8 @@ class Engine {
                      uint64_t *hist, double *expected, qsim_pt_t *out);
   void branch_sum(const void *U, const void *L, size_t nb, size_t nu, size_t nl, void *A);
   void branch_state(int half, uint64_t b, void *out);
+  void branch_values(int half, uint64_t b, const uint64_t *idx, size_t n, void *out);
+  void info(qsim_info_t *out) const;
   void comm_init(int rank, int world, const void *id);
   void rank_range(uint64_t *b0, uint64_t *b1) const;
   void cost_model(uint64_t nu, uint64_t nl, double hbm_gbps, qsim_cost_t *out);
@@ -228,6 +231,8 @@ class Engine {
                 size_t avail);
   DevBuf rowmap_;
   bool deferred_ = !(std::getenv("QSIM_DEFER") && std::getenv("QSIM_DEFER")[0] == '0');
+  int max_ctas_ = 0;  // QSIM_OPT_MAX_CTAS (tests)
+  int grid_ctas() const { return max_ctas_ > 0 ? std::min(max_ctas_, num_sms_) : num_sms_; }
 
   // executor
   void evolve_half(int half, uint64_t b0, uint64_t b1, void *slice, const uint64_t *dS, int64_t nS);

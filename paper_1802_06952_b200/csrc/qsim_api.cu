@@ -144,6 +144,17 @@ qsim_status qsim_branch_state(qsim_ctx *ctx, int half, uint64_t b, void *out) {
   return guard(ctx, [&](qsim::Engine &e) { e.branch_state(half, b, out); });
 }
 
+qsim_status qsim_branch_values(qsim_ctx *ctx, int half, uint64_t b, const uint64_t *idx, size_t n, void *out) {
+  return guard(ctx, [&](qsim::Engine &e) { e.branch_values(half, b, idx, n, out); });
+}
+
+qsim_status qsim_info(qsim_ctx *ctx, qsim_info_t *out) {
+  return guard(ctx, [&](qsim::Engine &e) {
+    if (!out) throw qsim::Error(QSIM_EINVAL, "null output");
+    e.info(out);
+  });
+}
+
 qsim_status qsim_nccl_unique_id(void *out128) {
   if (!out128) return QSIM_EINVAL;
   ncclUniqueId id;

@@ -31,6 +31,8 @@ QSIM_OPT_TIME_SWEEPS, QSIM_OPT_MODE, QSIM_OPT_MEM_BUDGET, QSIM_OPT_SWEEP_KERNEL,
 QSIM_OPT_FUSE_LAYERS = 6
 QSIM_OPT_DISTRIBUTE = 7
 QSIM_OPT_BFS = 8
+QSIM_OPT_MAX_CTAS = 9
+QSIM_OPT_DEFER = 10
 
 EXPORTED = ["qsim_create", "qsim_destroy", "qsim_last_error", "qsim_version", "qsim_set_option",
             "qsim_set_stream", "qsim_load_circuit", "qsim_partition", "qsim_set_blocks",
@@ -43,6 +45,12 @@ EXPORTED = ["qsim_create", "qsim_destroy", "qsim_last_error", "qsim_version", "q
 
 class qsim_cut(C.Structure):
     _fields_ = [("layer", C.c_uint32), ("q_upper", C.c_uint32), ("q_lower", C.c_uint32)]
+
+
+class qsim_info_t(C.Structure):
+    _fields_ = [("precision", C.c_uint32), ("have_circuit", C.c_uint32), ("h_upper", C.c_uint32),
+                ("h_lower", C.c_uint32), ("n_cuts", C.c_uint32), ("n_upper", C.c_uint64),
+                ("n_lower", C.c_uint64), ("device", C.c_int32)]
 
 
 class qsim_stats_t(C.Structure):
@@ -102,6 +110,8 @@ _sig = {
                                     C.c_size_t, _P, _P]),
     "qsim_branch_sum": (C.c_int, [_P, _P, _P, C.c_size_t, C.c_size_t, C.c_size_t, _P]),
     "qsim_branch_state": (C.c_int, [_P, C.c_int, C.c_uint64, _P]),
+    "qsim_branch_values": (C.c_int, [_P, C.c_int, C.c_uint64, _P, C.c_size_t, _P]),
+    "qsim_info": (C.c_int, [_P, C.POINTER(qsim_info_t)]),
     "qsim_nccl_unique_id": (C.c_int, [_P]),
     "qsim_comm_init": (C.c_int, [_P, C.c_int, C.c_int, _P]),
     "qsim_rank_range": (C.c_int, [_P, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
@@ -196,11 +206,17 @@ def qsim_reset_block(ctx):
     _check(ctx, _lib.qsim_reset_block(ctx))
 
 
-def qsim_amplitudes(ctx, upper_block, lower_block, prec: int, out=None, write=True):
-    """Reconstructed block [n_u, n_l] (complex64 / complex128 by ``prec``)."""
+def qsim_amplitudes(ctx, upper_block, lower_block, prec: int = None, out=None, write=True):
+    """Reconstructed block [n_u, n_l] of the ctx precision (``prec``, if given, must match it;
+    a caller-supplied ``out`` must be a C-contiguous array of that dtype and shape)."""
     u, l = _u64(upper_block), _u64(lower_block)
+    dt = _amp_dtype(ctx)
+    if prec is not None and np.dtype(dt) != np.dtype(np.complex128 if prec == QSIM_C128 else np.complex64):
+        raise ValueError("prec differs from the context's precision")
     if write and out is None:
-        out = np.empty((u.size, l.size), dtype=np.complex128 if prec == QSIM_C128 else np.complex64)
+        out = np.empty((u.size, l.size), dtype=dt)
+    if write and (out.dtype != dt or out.size != u.size * l.size or not out.flags.c_contiguous):
+        raise ValueError(f"out must be a C-contiguous {np.dtype(dt)} array of {u.size} x {l.size}")
     _check(ctx, _lib.qsim_amplitudes(ctx, _ptr(u), u.size, _ptr(l), l.size, _ptr(out) if write else None))
     return out
 
@@ -250,9 +266,34 @@ def qsim_branch_sum(ctx, U, L, prec: int):
     return A
 
 
-def qsim_branch_state(ctx, half: int, branch: int, h: int, prec: int):
-    out = np.empty(1 << h, dtype=np.complex128 if prec == QSIM_C128 else np.complex64)
+def qsim_info(ctx) -> dict:
+    r = qsim_info_t()
+    _check(ctx, _lib.qsim_info(ctx, C.byref(r)))
+    return {f: getattr(r, f) for f, _ in qsim_info_t._fields_}
+
+
+def _amp_dtype(ctx):
+    return np.complex128 if qsim_info(ctx)["precision"] == QSIM_C128 else np.complex64
+
+
+def qsim_branch_state(ctx, half: int, branch: int, h: int = None, prec: int = None):
+    """The complete leaf half-state (2^h values of the ctx precision; h / prec are checked)."""
+    inf = qsim_info(ctx)
+    hh = inf["h_upper"] if half == 0 else inf["h_lower"]
+    if h is not None and h != hh:
+        raise ValueError(f"h = {h} but the loaded circuit's half has {hh} qubits")
+    if prec is not None and prec != inf["precision"]:
+        raise ValueError("prec differs from the context's precision")
+    out = np.empty(1 << hh, dtype=_amp_dtype(ctx))
     _check(ctx, _lib.qsim_branch_state(ctx, half, branch, _ptr(out)))
+    return out
+
+
+def qsim_branch_values(ctx, half: int, branch: int, idx):
+    """U_b[idx] / L_b[idx] of one branch through the production path (qsim.h)."""
+    ix = _u64(idx)
+    out = np.empty(ix.size, dtype=_amp_dtype(ctx))
+    _check(ctx, _lib.qsim_branch_values(ctx, half, branch, _ptr(ix), ix.size, _ptr(out)))
     return out
 
 
