@@ -40,7 +40,8 @@ EXPORTED = ["qsim_create", "qsim_destroy", "qsim_last_error", "qsim_version", "q
             "qsim_sample", "qsim_sample_probs", "qsim_branch_sum", "qsim_branch_state",
             "qsim_nccl_unique_id", "qsim_comm_init", "qsim_rank_range", "qsim_stats",
             "qsim_stats_reset", "qsim_synchronize", "qsim_eq2_time", "qsim_cost_model",
-            "qsim_porter_thomas", "qsim_multipart_plan", "qsim_multipart_amplitudes"]
+            "qsim_porter_thomas", "qsim_multipart_plan", "qsim_multipart_amplitudes", "qsim_branch_values",
+            "qsim_info"]
 
 
 class qsim_cut(C.Structure):
