@@ -6,9 +6,11 @@
     python bench.py --impl reference      # the CPU oracle arm
 
 Workload (default, every N): config C5 = the metric's configuration, 64-qubit 8x8 grid,
-depth 22, 16 cut CZs -> 2^16 branches, sampled block 2^14 x 2^14 = 2^28 amplitudes (it fits
-one B200: 32 GiB c64 half states).  --config C4 (56q 8x7) / C3 (42q 6x7) for the smaller
-BASELINE.json configurations.
+depth 22, 16 cut CZs -> 2^16 branches, sampled block 2^14 x 2^14 = 2^28 amplitudes, in c128
+(the paper's double precision: 64 GiB half states on one B200); the c64 figure follows as
+"secondary".  --config C4 (56q 8x7) / C3 (42q 6x7) for the smaller BASELINE.json configurations.
+The timed region carries no per-launch events; the roofline numbers come from one extra
+profiling step with CUDA events around every sweep launch.
 
 One STEP = one of the 2^8 first-period prefix groups of that job (256 branches sharing the
 cuts of layers 7-8): both half-circuit branch trees (all prefix-shared sweeps from layer 1),
@@ -45,7 +47,10 @@ def parse():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="C5", choices=["C3", "C4", "C5"])
-    ap.add_argument("--precision", default="c64", choices=["c64", "c128"])
+    ap.add_argument("--precision", default="c128", choices=["c64", "c128"])
+    ap.add_argument("--secondary-steps", type=int, default=2,
+                    help="timed steps of the other precision (reported as 'secondary'; 0: skip)")
+    ap.add_argument("--ref-gates", type=int, default=4, help="oracle gate applications per reference step")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -134,66 +139,137 @@ def first_period_bits(cuts):
 
 
 # ---------------------------------------------------------------- CPU oracle timing
-def oracle_sample(circ, budget_s: float = 20.0, max_gates: int | None = None):
-    """Time the oracle's gate-by-gate half-circuit evolution (branch 0, upper half, full h)
-    for ~budget_s seconds; extrapolate to the flat partitioned job (§2.3.1: every branch
-    from scratch).  Returns (seconds per gate application, gate applications of the job,
-    gates timed)."""
-    from oracle import partition as OP, statevector as SV
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def oracle_gate_counts(circ):
+    """Gate applications of the oracle's partitioned simulator (oracle/partition.py) on this circuit.
+    flat: every branch from scratch (the oracle as it stands, §2.3.1): per branch and half the
+    initial state (one pass) + the internal gates + the branch gates (P_b on every upper cut endpoint,
+    Z on the lower ones whose bit is 1: c / 2 on average).  shared: the same gate lists with the
+    prefix shared at every cut layer (the paper's §2.3.2 scheme): the gates of layer t run once per
+    distinct branch prefix 2^{#cuts before t}, the branch gates of layer t once per 2^{#cuts <= t}."""
+    from oracle import partition as OP
     cuts = OP.cut_list(circ)
     c = len(cuts)
-    gu = OP.half_gates(circ, OP.UPPER, cuts, 0)
-    gl = OP.half_gates(circ, OP.LOWER, cuts, 0)
-    per_branch = len(gu) + len(gl) + circ.h_upper + circ.h_lower   # + layer-0 H on each qubit
-    job_gate_apps = (1 << c) * per_branch + (1 << max(c - 1, 0)) * c  # + Z gates (popcount)
-    h = circ.h_upper
-    # bounded host memory: above 28 qubits the oracle runs the gates of the first 28 qubits on a
-    # 2^28 state and the time per gate is scaled by 2^(h - 28) (a gate application is one pass
-    # over the state: its cost is linear in the state size)
-    hs = min(h, 28)
-    scale = float(1 << (h - hs))
-    gs = [g for g in gu if int(g[2]) < hs and (g[1] not in (4, "CZ") or int(g[3]) < hs)]
-    psi = np.full(1 << hs, 2.0 ** (-h / 2), dtype=np.complex128)  # H^{(x)h}|0> (pinned closed form)
-    t0 = time.perf_counter()
-    done = 0
-    for g in gs:
-        psi = SV.run_gates(psi, hs, [g])
-        done += 1
-        if time.perf_counter() - t0 > budget_s or (max_gates and done >= max_gates):
-            break
-    dt = time.perf_counter() - t0
-    return dt / done * scale, job_gate_apps, done
+    B = 1 << c
+    hu = circ.h_upper
+    per_layer = {}
+    n_int = 0
+    for (layer, kind, q0, q1) in circ.gates:
+        qs = [int(q0)] if kind != 4 else [int(q0), int(q1)]
+        if all(q < hu for q in qs) or all(q >= hu for q in qs):
+            per_layer[int(layer)] = per_layer.get(int(layer), 0) + 1
+            n_int += 1
+    flat = B * (n_int + 2) + B * c + B * c // 2
+    cut_layers = [cl for (cl, _, _) in cuts]
+    shared = 2.0  # initial states
+    for t in range(1, circ.depth + 1):
+        before = sum(1 for cl in cut_layers if cl < t)
+        at = sum(1 for cl in cut_layers if cl == t)
+        shared += per_layer.get(t, 0) * 2.0 ** before
+        shared += at * 2.0 ** (before + at) * 1.5  # P on the upper endpoint, Z (half of them) on the lower
+    return flat, shared
+
+
+class OracleClock:
+    """The oracle (oracle/fast.py: the numpy oracle's gate lists applied one at a time by the plain C
+    + OpenMP loop) timed on the box's host cores on a FULL half state of the workload (2^h complex128:
+    64 GiB at C5) - branch 0, upper half, gates in list order."""
+
+    def __init__(self, circ):
+        from oracle import fast as OF, partition as OP
+        self.OF = OF
+        self.circ = circ
+        self.h = circ.h_upper
+        self.gates = OP.half_gates(circ, OP.UPPER, OP.cut_list(circ), 0)
+        self.cores = OF.max_threads()
+        t0 = time.perf_counter()
+        self.psi = OF.initial_state(self.h, self.cores)
+        self.t_init = time.perf_counter() - t0
+        self.next = 0
+
+    def run(self, n_gates: int, threads: int) -> float:
+        """Applies the next n_gates gates of the list (cyclically); returns the seconds taken."""
+        gl = [self.gates[(self.next + i) % len(self.gates)] for i in range(n_gates)]
+        self.next += n_gates
+        t0 = time.perf_counter()
+        self.OF.run_gates(self.psi, self.h, gl, threads)
+        return time.perf_counter() - t0
+
+    def per_gate(self, budget_s: float, threads: int):
+        done, spent = 0, 0.0
+        while spent < budget_s or done == 0:
+            spent += self.run(1, threads)
+            done += 1
+        return spent / done, done
+
+
+def cpu_baseline(circ, n_amp, budget_s: float = 12.0):
+    """cpu_baseline of the JSON line: the oracle on all host cores and on one core, extrapolated from
+    the measured time per gate application on the full half state to the flat job (and, for
+    reference, to the prefix-shared job)."""
+    flat, shared = oracle_gate_counts(circ)
+    oc = OracleClock(circ)
+    tg_all, n_all = oc.per_gate(budget_s, oc.cores)
+    tg_one, n_one = oc.per_gate(budget_s, 1)
+    del oc.psi
+    return {
+        "value": n_amp / (tg_all * flat), "unit": UNIT, "cores": oc.cores, "kind": "oracle",
+        "one_core_value": n_amp / (tg_one * flat),
+        "prefix_shared_value": n_amp / (tg_all * shared),
+        "cpu_model": cpu_model(),
+        "sample": f"oracle (oracle/fast.py: numpy oracle gate lists, plain C + OpenMP pair loop, complex128) "
+                  f"on a full 2^{circ.h_upper}-amplitude half state (branch 0, upper half): {n_all} gate "
+                  f"applications on {oc.cores} threads ({tg_all:.3f} s each) and {n_one} on 1 thread "
+                  f"({tg_one:.3f} s each); extrapolated to the flat job's {flat} gate applications "
+                  f"(every branch from scratch, as oracle/partition.py runs it); prefix_shared_value: "
+                  f"the same per-gate time x {shared:.4g} applications with prefixes shared at cut layers",
+    }
 
 
 def run_reference(args):
+    """The reference arm: the oracle as it stands, timed on the host cores, each step a bounded
+    sample of the workload (gate applications on the full half state, all cores)."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     circ, Su, Sl = workload(args.config, args.seed)
     n_amp = Su.size * Sl.size
-    times = []
-    per_gate = None
-    job = None
-    for i in range(args.warmup + args.steps):
-        tg, job, _ = oracle_sample(circ, budget_s=0.0, max_gates=1)   # one gate application
-        if i >= args.warmup:
-            times.append(tg)
-    per_gate = sum(times) / len(times)
-    t_job = per_gate * job
-    value = n_amp / t_job
+    flat, shared = oracle_gate_counts(circ)
+    oc = OracleClock(circ)
+    per_step = max(1, int(args.ref_gates))
+    for _ in range(args.warmup):
+        oc.run(per_step, oc.cores)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        oc.run(per_step, oc.cores)
+    t_steps = time.perf_counter() - t0
+    per_gate = t_steps / (args.steps * per_step)
+    value = n_amp / (per_gate * flat)
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": per_gate * 1e3,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_steps / args.steps * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
-        "config": {"workload": f"{args.config} (oracle, flat partitioned simulator, numpy complex128)",
-                   "extrapolated_job_s": t_job, "gate_applications_per_job": job},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
-                         "sample": f"each step = 1 oracle gate application on a 2^{min(circ.h_upper, 28)} "
-                                   f"complex128 state (branch 0, upper half"
-                                   + (f"; x 2^{circ.h_upper - 28} for the 2^{circ.h_upper} half" if circ.h_upper > 28 else "")
-                                   + f"); job = {job} gate applications (flat: every branch from scratch), "
-                                   "extrapolated"},
+        "config": {"workload": f"{args.config} (oracle: flat partitioned simulator, complex128, "
+                               f"{oc.cores} host threads)",
+                   "step": f"{per_step} oracle gate applications on the full 2^{circ.h_upper} half state",
+                   "extrapolated_job_s": per_gate * flat, "gate_applications_per_job": flat,
+                   "prefix_shared_job_s": per_gate * shared, "state_init_s": oc.t_init},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": oc.cores, "kind": "oracle", "cpu_model": cpu_model(),
+                         "sample": f"each step = {per_step} gate applications of the oracle (plain C + OpenMP "
+                                   f"pair loop) on the full 2^{circ.h_upper} complex128 half state (branch 0, "
+                                   f"upper half); job = {flat} gate applications (flat: every branch from "
+                                   "scratch), extrapolated from the measured steps"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -221,41 +297,15 @@ def main():
 
     from paper_1802_06952_b200 import qsim as Q
 
-    prec = Q.QSIM_C128 if args.precision == "c128" else Q.QSIM_C64
     circ, Su, Sl = workload(args.config, args.seed)
     n_u, n_l = Su.size, Sl.size
     stream = torch.cuda.Stream()          # a real stream (the legacy default stream has handle 0)
     torch.cuda.set_stream(stream)
-    ctx = Q.qsim_create(prec, local)
-    Q.qsim_set_stream(ctx, stream.cuda_stream)
-    Q.qsim_load_circuit(ctx, circ.rows, circ.cols, circ.depth, circ.gate_array(), circ.cut_row)
+    uid = None
     if world > 1:
-        uid = [Q.qsim_nccl_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(uid, src=0)
-        Q.qsim_comm_init(ctx, rank, world, uid[0])
-    c, B, cuts = Q.qsim_partition(ctx)
-    gbits = first_period_bits(cuts)
-    G = 1 << gbits
-    per_group = B // G
-
-    # pinned host buffers for the end-to-end leg
-    pin = lambda shape, dt: torch.empty(shape, dtype=dt, pin_memory=True).numpy()
-    hSu, hSl = pin((n_u,), torch.int64).view(np.uint64), pin((n_l,), torch.int64).view(np.uint64)
-    hSu[:] = Su
-    hSl[:] = Sl
-    hA = pin((n_u, n_l), torch.complex128 if prec == Q.QSIM_C128 else torch.complex64)
-    hX = pin((N_DRAWS,), torch.int64).view(np.uint64)
-
-    Q.qsim_set_blocks(ctx, hSu, hSl)
-
-    def group_of(step):
-        return (step * world + rank) % G
-
-    def step_device(s):
-        g = group_of(s)
-        Q.qsim_reset_block(ctx)
-        Q.qsim_evolve_range(ctx, g * per_group, (g + 1) * per_group)
-        Q.qsim_sample(ctx, 1000 + s, N_DRAWS, to_host=False)
+        box = [Q.qsim_nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(box, src=0)
+        uid = box[0]
 
     def barrier():
         torch.cuda.synchronize()
@@ -263,67 +313,115 @@ def main():
             dist.barrier()
         torch.cuda.synchronize()
 
-    def max_over_ranks(x):
+    def reduce(x, op):
         if not dist:
             return x
         t = torch.tensor([x], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.all_reduce(t, op=op)
         return float(t.item())
 
-    def sum_over_ranks(x):
-        if not dist:
-            return x
-        t = torch.tensor([x], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.SUM)
-        return float(t.item())
+    max_over_ranks = lambda x: reduce(x, dist.ReduceOp.MAX if dist else None)
+    sum_over_ranks = lambda x: reduce(x, dist.ReduceOp.SUM if dist else None)
+    pin = lambda shape, dt: torch.empty(shape, dtype=dt, pin_memory=True).numpy()
+    hSu, hSl = pin((n_u,), torch.int64).view(np.uint64), pin((n_l,), torch.int64).view(np.uint64)
+    hSu[:] = Su
+    hSl[:] = Sl
+    hX = pin((N_DRAWS,), torch.int64).view(np.uint64)
 
-    # ---------------- warmup
-    for s in range(args.warmup):
-        step_device(s)
-    barrier()
+    def run_precision(prec, steps, warmup, full):
+        """warmup + `steps` timed steps (no per-launch events inside the timed region); with `full`:
+        the clocks sampler, one extra profiling step with events around every sweep / GEMM launch (the
+        roofline numbers) and the end-to-end leg through the C-ABI with host buffers."""
+        ctx = Q.qsim_create(prec, local)
+        Q.qsim_set_stream(ctx, stream.cuda_stream)
+        Q.qsim_load_circuit(ctx, circ.rows, circ.cols, circ.depth, circ.gate_array(), circ.cut_row)
+        if world > 1:
+            Q.qsim_comm_init(ctx, rank, world, uid)
+        c, B, cuts = Q.qsim_partition(ctx)
+        G = 1 << first_period_bits(cuts)
+        per_group = B // G
+        Q.qsim_set_blocks(ctx, hSu, hSl)
+        group_of = lambda step: (step * world + rank) % G
 
-    # ---------------- timed region (device events on the launching stream)
-    Q.qsim_set_option(ctx, Q.QSIM_OPT_TIME_SWEEPS, 1)
-    Q.qsim_stats_reset(ctx)
-    clocks = ClockSampler(local)
-    clocks.start()
-    barrier()
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    ev0.record(stream)
-    for s in range(args.warmup, args.warmup + args.steps):
-        step_device(s)
-    ev1.record(stream)
-    barrier()
-    clk = clocks.stop()
-    t_dev = max_over_ranks(ev0.elapsed_time(ev1) / 1e3)
-    st = Q.qsim_stats(ctx)
-    Q.qsim_set_option(ctx, Q.QSIM_OPT_TIME_SWEEPS, 0)
-    launches = int(sum_over_ranks(st["kernel_launches"]))
+        def step_device(s):
+            g = group_of(s)
+            Q.qsim_reset_block(ctx)
+            Q.qsim_evolve_range(ctx, g * per_group, (g + 1) * per_group)
+            Q.qsim_sample(ctx, 1000 + s, N_DRAWS, to_host=False)
 
-    groups_done = world * args.steps
-    value = (n_u * n_l) * groups_done / G / t_dev
+        for s in range(warmup):
+            step_device(s)
+        barrier()
+        Q.qsim_stats_reset(ctx)
+        clocks = ClockSampler(local) if full else None
+        if clocks:
+            clocks.start()
+        barrier()
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev0.record(stream)
+        for s in range(warmup, warmup + steps):
+            step_device(s)
+        ev1.record(stream)
+        barrier()
+        clk = clocks.stop() if clocks else None
+        t_dev = max_over_ranks(ev0.elapsed_time(ev1) / 1e3)
+        st = Q.qsim_stats(ctx)
+        out = {"c": c, "B": B, "G": G, "per_group": per_group, "t_dev": t_dev, "clocks": clk,
+               "launches": int(sum_over_ranks(st["kernel_launches"])),
+               "value": (n_u * n_l) * world * steps / G / t_dev}
+        if full:
+            # profiling step: CUDA events around every sweep / GEMM launch on the launching stream
+            Q.qsim_set_option(ctx, Q.QSIM_OPT_TIME_SWEEPS, 1)
+            Q.qsim_stats_reset(ctx)
+            barrier()
+            ev0.record(stream)
+            step_device(warmup + steps)
+            ev1.record(stream)
+            barrier()
+            out["prof"] = Q.qsim_stats(ctx)
+            out["prof_step_s"] = ev0.elapsed_time(ev1) / 1e3
+            Q.qsim_set_option(ctx, Q.QSIM_OPT_TIME_SWEEPS, 0)
+            # end-to-end through the C-ABI with host buffers
+            hA = pin((n_u, n_l), torch.complex128 if prec == Q.QSIM_C128 else torch.complex64)
+            k_e2e = args.e2e_steps if args.e2e_steps is not None else max(1, min(steps, 3 if circ.n < 64 else 1))
+            barrier()
+            t0 = time.perf_counter()
+            for s in range(k_e2e):  # 0 steps: e2e skipped (profiling runs)
+                g = group_of(warmup + s)
+                Q.qsim_set_blocks(ctx, hSu, hSl)                                        # H2D of the inputs
+                Q.qsim_evolve_range(ctx, g * per_group, (g + 1) * per_group)
+                Q.qsim_amplitudes(ctx, hSu, hSl, out=hA, write=(rank == 0))            # D2H of the block
+                Q.qsim_sample(ctx, 2000 + s, N_DRAWS, to_host=(rank == 0), out=hX)     # D2H of the draws
+            barrier()
+            t_e2e = max_over_ranks(time.perf_counter() - t0)
+            out["e2e"] = (n_u * n_l) * world * k_e2e / G / t_e2e if k_e2e else None
+            out["e2e_steps"] = k_e2e
+            del hA
+        Q.qsim_destroy(ctx)
+        return out
 
-    # ---------------- end-to-end through the C-ABI with host buffers
-    k_e2e = args.e2e_steps if args.e2e_steps is not None else max(1, min(args.steps, 3 if circ.n < 64 else 1))
-    barrier()
-    t0 = time.perf_counter()
-    for s in range(k_e2e):  # 0 steps: e2e skipped (profiling runs)
-        g = group_of(args.warmup + s)
-        Q.qsim_set_blocks(ctx, hSu, hSl)                                        # H2D of the inputs
-        Q.qsim_evolve_range(ctx, g * per_group, (g + 1) * per_group)
-        Q.qsim_amplitudes(ctx, hSu, hSl, prec, out=hA, write=(rank == 0))     # D2H of the block
-        Q.qsim_sample(ctx, 2000 + s, N_DRAWS, to_host=(rank == 0), out=hX)     # D2H of the draws
-    barrier()
-    t_e2e = max_over_ranks(time.perf_counter() - t0)
-    e2e_value = (n_u * n_l) * world * k_e2e / G / t_e2e if k_e2e else None
+    prec = Q.QSIM_C128 if args.precision == "c128" else Q.QSIM_C64
+    main_run = run_precision(prec, args.steps, args.warmup, True)
+    sec = None
+    if args.secondary_steps > 0:
+        other = Q.QSIM_C64 if prec == Q.QSIM_C128 else Q.QSIM_C128
+        r = run_precision(other, args.secondary_steps, 1, False)
+        sec = {"precision": "c64" if other == Q.QSIM_C64 else "c128",
+               "dtype": "f32" if other == Q.QSIM_C64 else "f64", "value": r["value"],
+               "ms_per_step": r["t_dev"] / args.secondary_steps * 1e3, "steps": args.secondary_steps, "warmup": 1}
+
+    c, B, G, per_group = main_run["c"], main_run["B"], main_run["G"], main_run["per_group"]
+    t_dev = main_run["t_dev"]
     amp_bytes = 16 if prec == Q.QSIM_C128 else 8
     h2d = (n_u + n_l) * 8 * world
     d2h = n_u * n_l * amp_bytes + N_DRAWS * 8 + 8
 
-    # ---------------- roofline of the dominant kernel (the gate sweep)
+    # ---------------- roofline of the dominant kernel (the gate sweep), from the profiling step
+    st = main_run["prof"]
     peak, peak_src = peaks()
     sweep_s = st["sweep_ms"] / 1e3
-    achieved = st["sweep_bytes"] / sweep_s / 1e9 if sweep_s > 0 else None
+    alg = st["sweep_bytes"] / sweep_s / 1e9 if sweep_s > 0 else None
+    moved = st["sweep_bytes_moved"] / sweep_s / 1e9 if sweep_s > 0 else None
     traffic = None
     prof = os.path.join(ROOT, "profiles", "ncu_sweep_summary.json")
     if os.path.exists(prof):
@@ -338,19 +436,14 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            tg, job, done = oracle_sample(circ, budget_s=20.0)
-            cpu = {"value": (n_u * n_l) / (tg * job), "unit": UNIT, "cores": 1, "kind": "oracle",
-                   "sample": f"{done} gate applications of the oracle (numpy complex128, 1 thread) on a "
-                             f"2^{min(circ.h_upper, 28)}-amplitude state (branch 0, upper half"
-                             + (f"; x 2^{circ.h_upper - 28} for the 2^{circ.h_upper} half" if circ.h_upper > 28 else "")
-                             + f"); extrapolated to the flat job's {job} gate applications ({B} branches x 2 halves)"}
+            cpu = cpu_baseline(circ, n_u * n_l)
         except MemoryError:
-            cpu = {"value": None, "unit": UNIT, "cores": 1, "kind": "oracle",
+            cpu = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "oracle",
                    "sample": "host out of memory for a full half state"}
 
     if rank == 0:
         line = {
-            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "metric": METRIC, "value": main_run["value"], "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_dev / args.steps * 1e3,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f32" if prec == Q.QSIM_C64 else "f64", "data": "synthetic",
@@ -361,28 +454,33 @@ def main():
                 "precision": f"{args.precision} ({'f32' if prec == Q.QSIM_C64 else 'f64'} half-state sweeps, "
                              "f64 reconstruction GEMM)",
                 "step": f"1 of {G} first-period prefix groups ({per_group} branches) per rank: both half "
-                        f"trees from layer 1, gathers, GEMM-accumulate, |a|^2 + {N_DRAWS} draws",
+                        f"trees from layer 1 (deferred forks), gathers, GEMM-accumulate, |a|^2 + {N_DRAWS} draws",
                 "projected_full_job_s": t_dev / args.steps * G / world,
                 "l2": f"inputs larger than L2: half states of {((1 << circ.h_upper) * amp_bytes) >> 20} MiB",
                 "parallelism": f"branch-sharded dp{world}",
             },
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": (achieved / peak) if achieved else None, "traffic": traffic,
-                         "peak_source": peak_src, "kernel": "tile_sweep_kernel",
+            "roofline": {"bound": "hbm", "achieved": moved, "peak": peak, "unit": "GB/s",
+                         "frac": (moved / peak) if moved else None, "traffic": traffic,
+                         "achieved_algorithmic": alg,
+                         "frac_algorithmic": (alg / peak) if alg else None,
+                         "peak_source": peak_src, "kernel": "tile_sweep_tma_kernel",
+                         "measured_in": "a separate profiling step after the timed region (CUDA events "
+                                        "around every sweep launch on the launching stream)",
                          "launches": st["timed_sweeps"],
                          "bytes_per_launch": st["sweep_bytes"] / max(1, st["sweeps"]),
+                         "moved_bytes_per_launch": st["sweep_bytes_moved"] / max(1, st["sweeps"]),
                          "avg_launch_us": sweep_s / max(1, st["timed_sweeps"]) * 1e6,
-                         "share_of_step": sweep_s / (t_dev * 1.0) if t_dev else None,
+                         "share_of_step": sweep_s / main_run["prof_step_s"] if main_run["prof_step_s"] else None,
                          "gemm_tflops": (st["gemm_flops"] / (st["gemm_ms"] / 1e3) / 1e12)
                          if st["gemm_ms"] > 0 else None},
-            "clocks": clk,
-            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                    "steps": k_e2e},
-            "gpu_launches": launches,
+            "clocks": main_run["clocks"],
+            "e2e": {"value": main_run["e2e"], "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                    "steps": main_run["e2e_steps"]},
+            "gpu_launches": main_run["launches"],
             "cpu_baseline": cpu,
+            "secondary": sec,
         }
         print(json.dumps(line), flush=True)
-    Q.qsim_destroy(ctx)
     if dist:
         dist.barrier()
         dist.destroy_process_group()

@@ -78,6 +78,8 @@ typedef struct {
   uint64_t branches_evolved; /* branch pairs whose slices were gathered                  */
   uint64_t lazy_gathers;     /* leaves whose last sweep was evaluated at the sampled indices only */
   uint64_t layers_applied;   /* gate layers completed by the sweeps (> sweeps when layers are fused) */
+  double sweep_bytes_moved;  /* bytes the sweeps actually read + wrote: sweep_bytes minus the reads of
+                                known-zero tiles that were skipped               */
 } qsim_stats_t;
 
 typedef enum {
@@ -90,8 +92,8 @@ typedef enum {
   QSIM_OPT_LAZY_LAST = 5     /* lazy tail of each leaf, evaluated only at the sampled indices during the
                                 gather instead of full 2^h passes: 0 off, 1 the last sweep, 2 (default)
                                 the last one or two by a cost model, 3 always two when possible      */,
-  QSIM_OPT_FUSE_LAYERS = 6,  /* 1: consecutive layers whose high targets fit one tile share one HBM
-                                pass (up to 3 register passes per tile); 0 (default): one layer per pass */
+  QSIM_OPT_FUSE_LAYERS = 6,  /* reserved: multi-layer tiles were removed (compute-bound, never faster than
+                                one pass per layer); only 0 is accepted             */
   QSIM_OPT_DISTRIBUTE = 7    /* 1: distributed half (§2.3.3): every half state
                                 is sharded over the ranks of qsim_comm_init (1, 2 or 4, by its top
                                 physical bits); every rank runs every branch on its shard; a gate on a

@@ -167,7 +167,6 @@ void Engine::ensure_device() {
   if (!stream_) stream_ = own_stream_;
   check(tile_sweep_setup(&occ1_, &occ2_, c128_), "tile sweep setup");
   check(tile_sweep_tma_setup(c128_), "tma sweep setup");
-  check(fused_sweep_setup(c128_), "fused sweep setup");
   occ1_ = std::max(occ1_, 1);
   occ2_ = std::max(occ2_, 1);
   inited_ = true;
@@ -197,11 +196,8 @@ void Engine::set_option(int key, int64_t value) {
       if (value < 0 || value > 3) throw Error(QSIM_EINVAL, "QSIM_OPT_LAZY_LAST must be 0, 1, 2 or 3");
       lazy_depth_ = (int)value;
       return;
-    case QSIM_OPT_FUSE_LAYERS:
-      if (value < 0 || value > 1) throw Error(QSIM_EINVAL, "QSIM_OPT_FUSE_LAYERS must be 0 or 1");
-      fuse_layers_ = value != 0;
-      if (have_circuit_)
-        for (int h = 0; h < 2; ++h) compile_plans(half_[h]);
+    case QSIM_OPT_FUSE_LAYERS:  // multi-layer tiles were compute-bound, never faster: removed
+      if (value != 0) throw Error(QSIM_EINVAL, "QSIM_OPT_FUSE_LAYERS: layer fusion was removed; only 0 is accepted");
       return;
     case QSIM_OPT_DISTRIBUTE:
       if (value < 0 || value > 1) throw Error(QSIM_EINVAL, "QSIM_OPT_DISTRIBUTE must be 0 or 1");
@@ -307,167 +303,13 @@ static void outer_runs(const std::vector<int> &hb, int L, int h, uint8_t *run_st
   *nruns = nr;
 }
 
-// Plans one fused launch over `stages` (kernels.h FusedSweepParams); false if the high
-// targets exceed the tile or the pass / op / diagonal budgets.
-bool Engine::plan_fused(const HalfProgram &hp, const std::vector<Stage> &stages, const Diag &pre, TilePlan &tp) {
-  const int L = tile_low_bits(c128_), T = L + kHiBits, VB = c128_ ? 0 : 1;
-  std::vector<int> hb;
-  for (auto &st : stages)
-    for (auto &g : st.gates)
-      if (g.bit >= L && std::find(hb.begin(), hb.end(), (int)g.bit) == hb.end()) hb.push_back(g.bit);
-  if ((int)hb.size() > kHiBits) return false;
-  for (int b = L; (int)hb.size() < kHiBits && b < hp.hl; ++b)
-    if (std::find(hb.begin(), hb.end(), b) == hb.end()) hb.push_back(b);
-  std::sort(hb.begin(), hb.end());
-  auto idx_of = [&](int bit) { return (int)(std::find(hb.begin(), hb.end(), bit) - hb.begin()); };
-  FusedSweepParams &f = tp.f;
-  std::memset(&f, 0, sizeof(f));
-  std::vector<std::vector<int>> R(1);
-  std::vector<int> diag_pass;
-  std::vector<Diag> diags;
-  int cur = 0;
-  // the open stage of pass `cur` (diag == -1); a stage is closed by its diagonal (>= 0) or
-  // when a bit would get a second gate (-2)
-  auto open = [&]() -> SweepStage * {
-    if (f.nstage[cur] == 0 || f.stage[cur][f.nstage[cur] - 1].diag != -1) {
-      if (f.nstage[cur] >= kMaxStage) return nullptr;
-      SweepStage &s = f.stage[cur][f.nstage[cur]++];
-      std::memset(&s, 0, sizeof(s));
-      s.diag = -1;
-    }
-    return &f.stage[cur][f.nstage[cur] - 1];
-  };
-  for (auto &st : stages) {
-    for (auto &g : st.gates) {
-      SweepStage *S = nullptr;
-      if (g.bit < L) {
-        if (!(S = open())) return false;
-        if (VB && g.bit == 0) {
-          if (S->vkind) {
-            S->diag = -2;
-            if (!(S = open())) return false;
-          }
-          S->vkind = g.kind;
-        } else {
-          const int lb = g.bit - VB;
-          if (std::find(S->lane_bit, S->lane_bit + S->nlane, lb) != S->lane_bit + S->nlane) {
-            S->diag = -2;
-            if (!(S = open())) return false;
-          }
-          S->lane_bit[S->nlane] = (uint8_t)lb;
-          S->lane_kind[S->nlane++] = g.kind;
-        }
-      } else {
-        const int j = idx_of(g.bit);
-        auto it = std::find(R[cur].begin(), R[cur].end(), j);
-        if (it == R[cur].end()) {
-          if (R[cur].size() == 4) {
-            if (++cur >= kMaxPass) return false;
-            R.emplace_back();
-          }
-          R[cur].push_back(j);
-          it = R[cur].end() - 1;
-        }
-        const int slot = (int)(it - R[cur].begin());
-        if (!(S = open())) return false;
-        if (S->gkind[slot]) {
-          S->diag = -2;
-          if (!(S = open())) return false;
-        }
-        S->gkind[slot] = g.kind;
-      }
-    }
-    if (!st.diag.identity()) {
-      if ((int)diags.size() >= kMaxDiag) return false;
-      SweepStage *S = open();
-      if (!S) return false;
-      S->diag = (int8_t)diags.size();
-      diags.push_back(st.diag);
-      diag_pass.push_back(cur);
-    }
-  }
-  f.npass = cur + 1;
-  for (int q = 0; q < f.npass; ++q) {
-    for (int j = 0; j < kHiBits && R[q].size() < 4; ++j)
-      if (std::find(R[q].begin(), R[q].end(), j) == R[q].end()) R[q].push_back(j);
-    std::vector<int> warps;
-    for (int j = 0; j < kHiBits; ++j)
-      if (std::find(R[q].begin(), R[q].end(), j) == R[q].end()) warps.push_back(j);
-    for (int s = 0; s < 4; ++s) f.gsel[q][s] = (uint8_t)R[q][s];
-    for (int w = 0; w < 3; ++w) f.wsel[q][w] = (uint8_t)warps[w];
-  }
-  for (int j = 0; j < kHiBits; ++j) f.hb[j] = (uint8_t)hb[j];
-  auto regpos = [&](int q) {
-    std::vector<int> pos;
-    if (VB) pos.push_back(0);
-    for (int s = 0; s < 4; ++s) pos.push_back(hb[R[q][s]]);
-    return pos;
-  };
-  f.ndiag = (int)diags.size();
-  for (size_t d = 0; d < diags.size(); ++d) {
-    f.diag[d] = to_dev(diags[d], true);
-    f.diag_s[d] = make_split(diags[d], regpos(diag_pass[d]));
-  }
-  outer_runs(hb, L, hp.hl, f.run_start, f.run_len, &f.nruns);
-  f.log2_ntiles = hp.hl - T;
-  int m = 0;
-  while (m < kHiBits && hb[m] == L + m) ++m;
-  f.run_m = m;
-  tp.fused = true;
-  tp.multi_layer = stages.size() > 1;
-  tp.npass = f.npass;
-  tp.use_pre = true;
-  tp.pre = pre;
-  tp.pass0_regs = regpos(0);
-  return true;
-}
-
-// The launches of `n` leading sweeps of a level: consecutive layers are fused into one
-// HBM pass while their high targets fit the tile (plan_fused); the root's generated first
-// sweep and the register-only kernel (QSIM_OPT_SWEEP_KERNEL 1) use per-sweep legacy plans.
+// The launches of the `n` leading sweeps of a level: one single-layer plan per sweep (a layer wider
+// than the tile is split into several launches, legacy_plans).
 std::vector<TilePlan> Engine::level_launches(const HalfProgram &hp, const Level &lev, size_t n) {
   std::vector<TilePlan> out;
-  const int L = tile_low_bits(c128_);
-  auto nhi = [&](const Sweep &sw) {
-    int c = 0;
-    for (auto &g : sw.gates) c += g.bit >= L;
-    return c;
-  };
-  size_t s = 0;
-  while (s < n) {
-    const Sweep &sw = lev.sweeps[s];
-    // single layers (and layers wider than the tile, split into chunks) use the
-    // single-layer kernels; only multi-layer groups use the fused kernel
-    auto single = [&]() {
-      auto v = legacy_plans(hp, sw);
-      out.insert(out.end(), v.begin(), v.end());
-      ++s;
-    };
-    if (sweep_kernel_ == 1 || sw.gen || !fuse_layers_ || dist_ || nhi(sw) > kHiBits) {
-      single();
-      continue;
-    }
-    std::vector<Stage> stages{Stage{sw.gates, sw.post}};
-    TilePlan best;
-    if (!plan_fused(hp, stages, sw.pre, best)) throw Error(QSIM_EINVAL, "sweep plan");
-    size_t e = s + 1;
-    while (fuse_layers_ && e < n && !lev.sweeps[e].gen && lev.sweeps[e].pre.identity() &&
-           nhi(lev.sweeps[e]) <= kHiBits) {
-      std::vector<Stage> more = stages;
-      more.push_back(Stage{lev.sweeps[e].gates, lev.sweeps[e].post});
-      TilePlan tp;
-      if (!plan_fused(hp, more, sw.pre, tp)) break;
-      stages.swap(more);
-      best = tp;
-      ++e;
-    }
-    if (e == s + 1) {
-      single();
-      continue;
-    }
-    best.layers = (int)(e - s);
-    out.push_back(best);
-    s = e;
+  for (size_t s = 0; s < n; ++s) {
+    auto v = legacy_plans(hp, lev.sweeps[s]);
+    out.insert(out.end(), v.begin(), v.end());
   }
   return out;
 }
@@ -514,8 +356,7 @@ void Engine::plan_levels(const HalfProgram &hp, std::vector<std::vector<std::vec
       if (std::getenv("QSIM_DEBUG_PLANS")) {
         std::fprintf(stderr, "%s level %zu skip %zu: %zu sweeps ->", hp.upper ? "U" : "D", l, skip, n);
         for (auto &tp : plans[l].back())
-          std::fprintf(stderr, " [%s x%d p%d m%d]", tp.fused ? "F" : "legacy", tp.layers, tp.npass,
-                       tp.fused ? tp.f.run_m : tp.p.run_m);
+          std::fprintf(stderr, " [x%d p%d m%d]", tp.layers, tp.npass, tp.p.run_m);
         std::fprintf(stderr, "\n");
       }
     }
@@ -876,7 +717,6 @@ std::vector<TilePlan> Engine::legacy_plans(const HalfProgram &hp, const Sweep &s
         }
         tp.p.nruns = nr;
         tp.p.log2_ntiles = hp.hl - T;
-        tp.fused = false;
         tp.targets = 0;
         for (auto &g : H) tp.targets |= 1u << g.bit;
         if (ci == 0)
@@ -1065,15 +905,8 @@ void Engine::launch_plan(const TilePlan &tp, const Diag &fork, bool first, const
     e1 = get_event();
     check(cudaEventRecord(e0, stream_), "cudaEventRecord");
   }
-  if (tp.fused) {
-    FusedSweepParams f = tp.f;
-    f.pre = to_dev(pre, pre_mode != 0);
-    if (pre_mode == 1) f.pre_s = make_split(pre, tp.pass0_regs);
-    f.src = src;
-    f.dst = dst;
-    const int grid = (int)std::min<uint64_t>(1ull << f.log2_ntiles, (uint64_t)grid_ctas());
-    check(launch_fused_sweep(f, c128_, pre_mode, grid, stream_, tp.multi_layer), "fused sweep launch");
-  } else {
+  skip_pm_last_ = 0;
+  {
     TileSweepParams p = tp.p;
     p.pre = to_dev(pre, pre_mode != 0);
     p.njobs = 1;
@@ -1101,6 +934,7 @@ void Engine::launch_plan(const TilePlan &tp, const Diag &fork, bool first, const
       p.skip_pm = child_fork->pm & tp.zfix & outer;
       p.skip_pv = child_fork->pv & p.skip_pm;
     }
+    skip_pm_last_ = p.skip_pm;
     const uint64_t tiles = 1ull << p.log2_ntiles;
     const bool tma = (sweep_kernel_ != 1 || p.nswap) && (pre_mode != 2 || (gen_tma_ && !dist_));
     if (tma) {
@@ -1124,7 +958,11 @@ void Engine::launch_plan(const TilePlan &tp, const Diag &fork, bool first, const
   st_.sweeps++;
   st_.sweep_states += 1;
   st_.layers_applied += (uint64_t)tp.layers;
-  st_.sweep_bytes += (tp.gen ? 1.0 : 2.0) * std::ldexp(1.0, h) * (double)amp_;
+  const double state = std::ldexp(1.0, h) * (double)amp_;
+  st_.sweep_bytes += (tp.gen ? 1.0 : 2.0) * state;
+  // reads of known-zero tiles (a fraction 1 - 2^-popc(skip_pm) of the tiles) are not issued
+  const double skipped = tp.gen ? 0.0 : 1.0 - std::ldexp(1.0, -__builtin_popcount(skip_pm_last_));
+  st_.sweep_bytes_moved += ((tp.gen ? 1.0 : 2.0) - skipped) * state;
 }
 
 // Runs the sweeps of `level` for fork child `child`, all but the last `skip` of them
@@ -1877,7 +1715,7 @@ void Engine::synchronize() {
 void Engine::launch_nodes(const TilePlan &tp, const void *src, void *dst, int log2_nodes, int shift,
                           const ForkDev &fork, const HalfProgram &hp, bool apply_fork, uint32_t proj_bits,
                           const Diag *extra_pre) {
-  if (tp.fused || tp.gen || !tp.swaps.empty()) throw Error(QSIM_EINVAL, "node-batched sweep of an unsupported plan");
+  if (tp.gen || !tp.swaps.empty()) throw Error(QSIM_EINVAL, "node-batched sweep of an unsupported plan");
   const int h = hp.hl;
   int pre_mode = 0;
   Diag pre;
@@ -1924,6 +1762,8 @@ void Engine::launch_nodes(const TilePlan &tp, const void *src, void *dst, int lo
   st_.sweep_states += (uint64_t)nodes;
   st_.layers_applied += (uint64_t)tp.layers * (uint64_t)nodes;
   st_.sweep_bytes += 2.0 * nodes * std::ldexp(1.0, h) * (double)amp_;
+  st_.sweep_bytes_moved += (2.0 - (1.0 - std::ldexp(1.0, -__builtin_popcount(p.nb_skip)))) * nodes *
+                           std::ldexp(1.0, h) * (double)amp_;
 }
 
 static ForkDev fork_dev(const Level &lev) {
@@ -1941,7 +1781,7 @@ static ForkDev fork_dev(const Level &lev) {
 int Engine::bfs_level(int half, int m0, size_t avail) const {
   const HalfExec &he = half_[half];
   const HalfProgram &hp = he.prog;
-  if (!bfs_ || dist_ || fuse_layers_ || sweep_kernel_ == 1 || !he.tree || he.plans.empty()) return -1;
+  if (!bfs_ || dist_ || sweep_kernel_ == 1 || !he.tree || he.plans.empty()) return -1;
   if (state_bytes_ > ((size_t)256 << 20)) return -1;
   const int F = (int)hp.levels.size() - 1;
   if (F < 1) return -1;
@@ -1949,7 +1789,7 @@ int Engine::bfs_level(int half, int m0, size_t avail) const {
     if (l < F && he.plans[l][0].empty()) return -1;  // only the leaf level may defer its fork
     for (const auto &v : he.plans[l])
       for (const TilePlan &tp : v)
-        if (tp.fused || tp.gen || !tp.swaps.empty()) return -1;
+        if (tp.gen || !tp.swaps.empty()) return -1;
   }
   std::vector<int> sbits(F + 1, 0);
   for (int l = 1; l <= F; ++l) sbits[l] = sbits[l - 1] + hp.levels[l].k;
@@ -2235,7 +2075,7 @@ void Engine::evolve_block(int half, uint64_t b0, int m, void *slice, const uint6
   if (he.prog.hl < T) throw Error(QSIM_EINVAL, "tree mode needs h >= tile bits");
   state_bytes_ = ((size_t)1 << he.prog.hl) * amp_;
   // level-synchronous subtrees for small states (launch-bound otherwise): gather forks pinned
-  const bool bfs = bfs_ && !fuse_layers_ && sweep_kernel_ != 1 && state_bytes_ <= ((size_t)256 << 20);
+  const bool bfs = bfs_ && sweep_kernel_ != 1 && state_bytes_ <= ((size_t)256 << 20);
   if (!bfs) {  // their buffers are state memory now
     bfs_buf_[0].release();
     bfs_buf_[1].release();
@@ -2364,7 +2204,7 @@ bool Engine::bfs_tree(const TreeVariant &v, int lz, int M, const std::vector<int
     const auto &launches = v.plans[q][std::min<size_t>((size_t)skip[q], v.plans[q].size() - 1)];
     if (launches.empty()) return false;
     for (const TilePlan &tp : launches)
-      if (tp.fused || tp.gen || !tp.swaps.empty()) return false;
+      if (tp.gen || !tp.swaps.empty()) return false;
   }
   size_t need[2] = {0, 0};
   for (int q = l + 1; q <= M; ++q) need[q & 1] = std::max(need[q & 1], state_bytes_ << sb[q]);

@@ -40,14 +40,11 @@ struct DevBuf {
   DevBuf &operator=(const DevBuf &) = delete;
 };
 
-// One planned sweep launch: a fused multi-layer TMA sweep (FusedSweepParams) or a legacy
-// single-layer register sweep (TileSweepParams; the generated root sweep, or
-// QSIM_OPT_SWEEP_KERNEL 1).  A layer wider than the tile is split into several launches.
+// One planned sweep launch of one layer (TileSweepParams): the TMA-pipelined sweep (default) or
+// the register-only one (QSIM_OPT_SWEEP_KERNEL 1).  A layer wider than the tile is split into
+// several launches.
 struct TilePlan {
   std::vector<std::pair<int, int>> swaps;  // distributed half: (local bit, global bit index) after it
-  bool fused = false;
-  bool multi_layer = false;  // several layers (stage lists) in this launch
-  FusedSweepParams f;        // src/dst/pre filled at launch
   TileSweepParams p;   // src/dst/job fields filled at launch
   int npass = 1;
   int layers = 1;        // gate layers completed by this launch
@@ -59,11 +56,6 @@ struct TilePlan {
   uint32_t zfix = 0;       // fork bits of the level not targeted by an earlier launch of the level
 };
 
-// A stage of a fused sweep: some gates of one layer, then (optionally) a diagonal.
-struct Stage {
-  std::vector<Gate1> gates;
-  Diag diag;
-};
 
 // The branch tree of one half for one placement of its forks (Engine::choose_tree): the
 // program (levels = the distinct fork-apply layers) and its tile plans [level][lazy skip 0..2].
@@ -150,8 +142,6 @@ class Engine {
   int sweep_kernel_ = 0;  // 0: TMA sweep (auto stages), 1: register-only, 2 / 3: TMA with 2 / 3 stages
   int lazy_depth_ = 2;      // up to this many trailing leaf sweeps evaluated at the sampled indices
   bool full_leaf_ = false; // qsim_branch_state: materialise the complete leaf
-  bool fuse_layers_ = false; // fuse consecutive layers into one HBM pass when they fit a tile
-                             // (off by default: multi-pass tiles are not yet faster)
   bool time_sweeps_ = false;
   // distributed half (§2.3.3): every half state is sharded over the
   // communicator's ranks by its top gbits_ physical bits; all ranks run every branch
@@ -207,7 +197,6 @@ class Engine {
   std::vector<int> choose_perm(const HalfExec &he, int64_t nS = 0) const;
   int lazy_depth_of(const HalfProgram &hp, int64_t nS) const;
   int64_t perm_ns_[2] = {0, 0};  // block sizes the relabelling of each half was chosen for
-  bool plan_fused(const HalfProgram &hp, const std::vector<Stage> &stages, const Diag &pre, TilePlan &tp);
   std::vector<TilePlan> level_launches(const HalfProgram &hp, const Level &lev, size_t n);
   std::vector<TilePlan> legacy_plans(const HalfProgram &hp, const Sweep &sw);
   void upload_small(HalfExec &he);
@@ -232,6 +221,7 @@ class Engine {
   DevBuf rowmap_;
   bool deferred_ = !(std::getenv("QSIM_DEFER") && std::getenv("QSIM_DEFER")[0] == '0');
   int max_ctas_ = 0;  // QSIM_OPT_MAX_CTAS (tests)
+  uint32_t skip_pm_last_ = 0;  // known-zero tile mask of the last planned launch (stats)
   int grid_ctas() const { return max_ctas_ > 0 ? std::min(max_ctas_, num_sms_) : num_sms_; }
 
   // executor

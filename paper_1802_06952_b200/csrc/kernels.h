@@ -110,51 +110,9 @@ struct TileSweepParams {
 cudaError_t launch_tile_sweep(const TileSweepParams &p, bool c128, int pre_mode, int npass,
                               int grid, cudaStream_t s);
 
-// ---------------------------------------------------------------- fused multi-layer sweep
-// One HBM pass applying one or more consecutive layers whose high targets all fit in the
-// tile's 7 hi bits.  The work is up to 3 register passes over the tile (each pass maps 4 hi
-// bits to registers; passes are separated by a shared-memory remap); every pass runs an op
-// list in order: butterflies on a register slot / the vector bit / a lane bit (shuffle),
-// and fused-diagonal applications (the diagonal of a layer follows all of its gates).
-// A pass is a list of stages; a stage applies gates on the vector bit, on lane bits and on
-// the 4 register slots (these commute: distinct bits of one layer), then optionally a diagonal.
-constexpr int kMaxPass = 3;
-constexpr int kMaxStage = 4;
-constexpr int kMaxDiag = 4;
-struct SweepStage {
-  uint8_t gkind[4];  // kind on register slot s (0 none, 1 SX', 2 SY')
-  uint8_t vkind;     // kind on the vector bit (c64)
-  uint8_t nlane;
-  uint8_t lane_bit[5], lane_kind[5];
-  int8_t diag;  // index into diag[] applied after the gates, -1 none
-};
-struct FusedSweepParams {
-  const void *src;
-  void *dst;
-  int32_t log2_ntiles;
-  int32_t nruns;
-  uint8_t run_start[32], run_len[32];
-  uint8_t hb[kHiBits];
-  int32_t run_m;
-  int32_t npass;
-  uint8_t gsel[kMaxPass][4], wsel[kMaxPass][3];
-  int32_t nstage[kMaxPass];
-  SweepStage stage[kMaxPass][kMaxStage];
-  DiagDev pre;
-  DiagSplit pre_s;  // for the pass-0 registers
-  int32_t ndiag;
-  DiagDev diag[kMaxDiag];
-  DiagSplit diag_s[kMaxDiag];  // for the registers of the pass that applies it
-};
-// TMA-pipelined sweep: one CTA per SM, `stages` shared-memory tile stages filled by
-// cp.async.bulk / cp.async under mbarriers, 1 producer warp + two ping-pong groups of 8
-// consumer warps (each group owns alternate tiles).  pre_mode 0 / 1.
-// multi_layer = false: a single layer (the straight-line kernel variant, see sweep_fused.cu)
-cudaError_t launch_fused_sweep(const FusedSweepParams &p, bool c128, int pre_mode, int grid, cudaStream_t s,
-                               bool multi_layer);
-cudaError_t fused_sweep_setup(bool c128);
-// Single-layer TMA-pipelined sweep (sweep_tma.cu, the default): the same producer / ping-pong
-// consumer structure specialised for one layer (TileSweepParams), `stages` = 2 or 3.
+// TMA-pipelined sweep (sweep_tma.cu, the default): one CTA per SM, `stages` (2 or 3) shared-memory
+// tile stages filled by cp.async.bulk / cp.async under mbarriers, 1 producer warp + two ping-pong
+// groups of 8 consumer warps (each group owns alternate tiles); one layer (TileSweepParams).
 cudaError_t launch_tile_sweep_tma(const TileSweepParams &p, bool c128, int pre_mode, int npass, int grid,
                                   cudaStream_t s, int stages);
 cudaError_t tile_sweep_tma_setup(bool c128);

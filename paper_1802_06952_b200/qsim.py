@@ -58,7 +58,7 @@ class qsim_stats_t(C.Structure):
     _fields_ = [("kernel_launches", C.c_uint64), ("sweeps", C.c_uint64), ("sweep_states", C.c_uint64),
                 ("sweep_bytes", C.c_double), ("sweep_ms", C.c_double), ("timed_sweeps", C.c_uint64),
                 ("gemm_flops", C.c_double), ("gemm_ms", C.c_double), ("branches_evolved", C.c_uint64),
-                ("lazy_gathers", C.c_uint64), ("layers_applied", C.c_uint64)]
+                ("lazy_gathers", C.c_uint64), ("layers_applied", C.c_uint64), ("sweep_bytes_moved", C.c_double)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}

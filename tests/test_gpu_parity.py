@@ -129,14 +129,12 @@ def test_tree_mode_h14(prec, h14_reference):
 
 
 @pytest.mark.parametrize("prec", PRECS, ids=PNAME.get)
-@pytest.mark.parametrize("lazy,kernel,fuse", [(0, 0, 1), (1, 1, 1), (0, 1, 0), (1, 0, 1), (3, 0, 1), (3, 1, 1),
-                                              (0, 0, 0), (2, 0, 0)])
-def test_tree_mode_h14_variants(prec, lazy, kernel, fuse, h14_reference):
-    """Lazy tail depth, register-only vs TMA sweep kernel, layer fusion on / off."""
+@pytest.mark.parametrize("lazy,kernel", [(0, 0), (1, 1), (0, 1), (1, 0), (3, 0), (3, 1), (2, 0), (2, 2), (2, 3)])
+def test_tree_mode_h14_variants(prec, lazy, kernel, h14_reference):
+    """Lazy tail depth, register-only vs TMA sweep kernel (auto / 2 / 3 stages)."""
     circ, Su, Sl, ref = h14_reference
-    A = run_block(circ, Su, Sl, prec, opts={Q.QSIM_OPT_LAZY_LAST: lazy, Q.QSIM_OPT_SWEEP_KERNEL: kernel,
-                                            Q.QSIM_OPT_FUSE_LAYERS: fuse})
-    assert_close(A, ref, prec, f"h14 lazy={lazy} kernel={kernel} fuse={fuse}")
+    A = run_block(circ, Su, Sl, prec, opts={Q.QSIM_OPT_LAZY_LAST: lazy, Q.QSIM_OPT_SWEEP_KERNEL: kernel})
+    assert_close(A, ref, prec, f"h14 lazy={lazy} kernel={kernel}")
 
 
 @pytest.mark.parametrize("prec", PRECS, ids=PNAME.get)
@@ -160,19 +158,19 @@ def test_tree_mode_h14_zero_skip(prec, zero_skip, h14_reference, monkeypatch):
 
 @pytest.mark.parametrize("prec", PRECS, ids=PNAME.get)
 @pytest.mark.parametrize("branch", [0, 77])
-def test_fused_sweeps_c3_branch(prec, branch, c3_circuit):
-    """C3-size leaf with and without layer fusion (same kernels as the bench) vs the oracle."""
+def test_c3_branch_sweep_kernels(prec, branch, c3_circuit):
+    """C3-size leaf with the TMA sweep and the register-only sweep vs the oracle."""
     circ = c3_circuit
     ref = OP.branch_state(circ, 0, branch)
-    for fuse in (1, 0):
+    for kernel in (0, 1):
         ctx = Q.qsim_create(prec, 0)
         try:
-            Q.qsim_set_option(ctx, Q.QSIM_OPT_FUSE_LAYERS, fuse)
+            Q.qsim_set_option(ctx, Q.QSIM_OPT_SWEEP_KERNEL, kernel)
             Q.qsim_load_circuit(ctx, 6, 7, 22, circ.gate_array())
             got = Q.qsim_branch_state(ctx, 0, branch, 21, prec)
         finally:
             Q.qsim_destroy(ctx)
-        assert_close(got, ref, prec, f"C3 fused={fuse}")
+        assert_close(got, ref, prec, f"C3 kernel={kernel}")
 
 
 @pytest.fixture

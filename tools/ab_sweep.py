@@ -22,22 +22,19 @@ def main():
     ap.add_argument("--kernels", default="0,1,2")
     ap.add_argument("--branches", type=int, default=128)
     ap.add_argument("--lazy", default="2", help="QSIM_OPT_LAZY_LAST values, comma separated")
-    ap.add_argument("--fuse", default="1", help="QSIM_OPT_FUSE_LAYERS values, comma separated")
+    ap.add_argument("--defer", default="1", help="QSIM_OPT_DEFER values (deferred forks), comma separated")
     a = ap.parse_args()
     rows, cols, depth, lu, ll = CONFIGS[a.config]
     circ = generate(rows, cols, depth, 0)
     prec = Q.QSIM_C128 if a.precision == "c128" else Q.QSIM_C64
     Su, Sl = sample_block(circ.h_upper, 1 << lu, 1), sample_block(circ.h_lower, 1 << ll, 2)
     out = {}
-    for kern, lazy, fuse in [(int(k), int(z), int(f)) for k in a.kernels.split(",") for z in a.lazy.split(",")
-                             for f in a.fuse.split(",")]:
+    for kern, lazy, defer in [(int(k), int(z), int(f)) for k in a.kernels.split(",") for z in a.lazy.split(",")
+                              for f in a.defer.split(",")]:
         ctx = Q.qsim_create(prec, 0)
         Q.qsim_set_option(ctx, Q.QSIM_OPT_SWEEP_KERNEL, kern)
         Q.qsim_set_option(ctx, Q.QSIM_OPT_LAZY_LAST, lazy)
-        try:
-            Q.qsim_set_option(ctx, Q.QSIM_OPT_FUSE_LAYERS, fuse)
-        except Q.QsimError:  # an older library (QSIM_LIB) without the option: no fusion
-            assert fuse == 0
+        Q.qsim_set_option(ctx, Q.QSIM_OPT_DEFER, defer)
         Q.qsim_load_circuit(ctx, rows, cols, depth, circ.gate_array())
         Q.qsim_set_blocks(ctx, Su, Sl)
         Q.qsim_evolve_range(ctx, 0, a.branches)          # warm-up
@@ -50,10 +47,10 @@ def main():
         wall = time.perf_counter() - t0
         st = Q.qsim_stats(ctx)
         Q.qsim_destroy(ctx)
-        out[(kern, lazy, fuse)] = {"kernel": kern, "lazy": lazy, "fuse": fuse, "wall_s": wall, "sweeps": st["sweeps"], "sweep_ms": st["sweep_ms"],
+        out[(kern, lazy, defer)] = {"kernel": kern, "lazy": lazy, "defer": defer, "wall_s": wall, "sweeps": st["sweeps"], "sweep_ms": st["sweep_ms"],
                      "GBps": st["sweep_bytes"] / (st["sweep_ms"] / 1e3) / 1e9,
                      "avg_us": st["sweep_ms"] / max(1, st["timed_sweeps"]) * 1e3}
-        print(json.dumps(out[(kern, lazy, fuse)]), flush=True)
+        print(json.dumps(out[(kern, lazy, defer)]), flush=True)
 
 
 if __name__ == "__main__":
