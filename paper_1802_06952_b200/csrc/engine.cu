@@ -9,7 +9,17 @@
 #include <functional>
 #include <sstream>
 
+#include <nvtx3/nvToolsExt.h>
+
 namespace qsim {
+
+// NVTX range per host phase (visible in nsys / ncu --nvtx; no cost without a tool attached)
+struct Nvtx {
+  explicit Nvtx(const char *name) { nvtxRangePushA(name); }
+  ~Nvtx() { nvtxRangePop(); }
+  Nvtx(const Nvtx &) = delete;
+  Nvtx &operator=(const Nvtx &) = delete;
+};
 
 // ---------------------------------------------------------------- helpers
 void DevBuf::reserve(size_t n) {
@@ -181,6 +191,7 @@ void Engine::set_option(int key, int64_t value) {
     case QSIM_OPT_MODE:
       if (value < 0 || value > 2) throw Error(QSIM_EINVAL, "QSIM_OPT_MODE must be 0, 1 or 2");
       mode_ = (int)value;
+      roles_chosen_ = false;
       if (have_circuit_) {
         for (int h = 0; h < 2; ++h) {
           half_[h].uploaded = false;
@@ -248,6 +259,8 @@ void Engine::load_circuit(uint32_t rows, uint32_t cols, uint32_t depth, const qs
 }
 
 void Engine::compile_all() {
+  roles_chosen_ = false;
+  roles_.clear();
   if (dist_) {
     if (world_ & (world_ - 1) || world_ > 4)
       throw Error(QSIM_EINVAL, "distributed halves need 1, 2 or 4 ranks (qsim_comm_init)");
@@ -263,7 +276,9 @@ void Engine::compile_all() {
       plan_distributed(half_[h]);
       compile_plans(half_[h]);
     } else if (half_[h].tree) {  // relabel qubits to physical bits for long tile runs (choose_perm)
-      const std::vector<int> perm = choose_perm(half_[h], perm_ns_[h]);
+      std::vector<double> lw;
+      if (deferred_) lw = deferred_layer_weights(h, perm_ns_[h]);
+      const std::vector<int> perm = choose_perm(half_[h], perm_ns_[h], deferred_ ? &lw : nullptr);
       bool ident = true;
       for (size_t b = 0; b < perm.size(); ++b) ident = ident && perm[b] == (int)b;
       if (!ident) {
@@ -373,7 +388,29 @@ void Engine::plan_levels(const HalfProgram &hp, std::vector<std::vector<std::vec
 // of a permutation is the sum over the sweeps that run as full passes of (nodes executing the
 // sweep) / speed; a seeded local search over transpositions minimises it.
 // QSIM_PERM = id | rev | rand | auto (default) for tests.
-std::vector<int> Engine::choose_perm(const HalfExec &he, int64_t nS) const {
+// Tree nodes running the sweep of each layer in the deferred-fork tree of the whole branch range
+// (choose_tree): 2^{#cuts whose fork applies at or before the layer}; 0 for the lazy tail.
+std::vector<double> Engine::deferred_layer_weights(int half, int64_t nS) {
+  HalfExec &he = half_[half];
+  const bool up = half == 0;
+  he.glayers = gate_layers(circ_, up ? 0 : circ_.h_u, up ? circ_.h_u : circ_.n);
+  he.ft = first_targets(circ_, half_cuts(circ_, up));
+  const int c = (int)circ_.cuts.size();
+  if (nS <= 0) nS = 4096;
+  const int lz = tree_lazy(half, nS);
+  const TreeChoice tc = choose_tree(half, c, lz, nS, 6, true);
+  std::vector<double> w(circ_.depth + 2, 0.0);
+  const int S = (int)he.glayers.size();
+  for (int i = 0; i + lz < S; ++i) {
+    const int t = he.glayers[i];
+    int n = 0;
+    for (int g = 0; g < c; ++g) n += tc.apply[g] <= t;
+    w[t] = std::ldexp(1.0, n);
+  }
+  return w;
+}
+
+std::vector<int> Engine::choose_perm(const HalfExec &he, int64_t nS, const std::vector<double> *layer_w) const {
   const HalfProgram &hp = he.prog;
   const int h = hp.h, L = tile_low_bits(c128_);
   std::vector<int> perm(h);
@@ -408,12 +445,13 @@ std::vector<int> Engine::choose_perm(const HalfExec &he, int64_t nS) const {
     sbits += hp.levels[l].k;
     const auto &sw = hp.levels[l].sweeps;
     const size_t lazy = (l == F && lazy_depth_ > 0) ? std::min<size_t>(2, sw.size() > 0 ? sw.size() - 1 : 0) : 0;
-    for (size_t i = 0; i + lazy < sw.size(); ++i) {
+    for (size_t i = 0; i < sw.size(); ++i) {
+      if (!layer_w && i + lazy >= sw.size()) continue;
       if (sw[i].gen || sw[i].gates.empty()) continue;
       SW x;
       for (auto &g : sw[i].gates) x.bits.push_back(g.bit);  // identity program: canonical bits
-      x.w = std::ldexp(1.0, sbits);
-      sws.push_back(x);
+      x.w = layer_w ? (*layer_w)[sw[i].first_layer] : std::ldexp(1.0, sbits);
+      if (x.w > 0) sws.push_back(x);
     }
   }
   static const double speed[8] = {4940, 5310, 5680, 5930, 5990, 6020, 6040, 6050};
@@ -822,6 +860,7 @@ void Engine::set_blocks(const uint64_t *up, size_t nu, const uint64_t *lo, size_
     check(cudaMemcpyAsync(d_Sp_[h].ptr, P.data(), P.size() * 8, cudaMemcpyHostToDevice, stream_), "upload S");
     check(cudaStreamSynchronize(stream_), "upload S");  // P is a temporary
   }
+  roles_chosen_ = false;  // the lazy tail, hence the fork placement, depends on the block sizes
   A_acc_.reserve(nu * nl * 16);
   check(cudaMemsetAsync(A_acc_.ptr, 0, nu * nl * 16, stream_), "zero block");
   check(cudaStreamSynchronize(stream_), "set_blocks");
@@ -908,6 +947,7 @@ void Engine::launch_plan(const TilePlan &tp, const Diag &fork, bool first, const
   skip_pm_last_ = 0;
   {
     TileSweepParams p = tp.p;
+    p.no_pskip = pskip_ ? 0 : 1;
     p.pre = to_dev(pre, pre_mode != 0);
     p.njobs = 1;
     if (dist_) {
@@ -1211,6 +1251,7 @@ void Engine::evolve_half(int half, uint64_t b0, uint64_t b1, void *slice, const 
 }
 
 void Engine::gemm(const void *U, const void *L, int64_t K, int64_t M, int64_t N, double *A) {
+  Nvtx nv("branch GEMM");
   const bool timed = time_sweeps_;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (timed) {
@@ -1228,6 +1269,7 @@ void Engine::gemm(const void *U, const void *L, int64_t K, int64_t M, int64_t N,
 }
 
 void Engine::evolve_range(uint64_t b0, uint64_t b1) {
+  Nvtx nv("qsim_evolve_range");
   if (!have_circuit_) throw Error(QSIM_ESTATE, "no circuit loaded");
   if (!have_blocks_) throw Error(QSIM_ESTATE, "no blocks set (qsim_set_blocks)");
   const int c = (int)circ_.cuts.size();
@@ -1251,6 +1293,7 @@ void Engine::evolve_range(uint64_t b0, uint64_t b1) {
   chunk = std::min<uint64_t>(p2, b1 - b0);
   U_.reserve(chunk * nu * amp_);
   L_.reserve(chunk * nl * amp_);
+  if (!roles_chosen_ && deferred_) choose_roles();
   for (uint64_t s = b0; s < b1;) {
     uint64_t e = std::min(b1, (s / p2 + 1) * p2);
     e = std::min(e, s + chunk);
@@ -1281,6 +1324,7 @@ void Engine::evolve_range(uint64_t b0, uint64_t b1) {
 
 // ---------------------------------------------------------------- reduction / outputs
 double *Engine::reduced_block() {
+  Nvtx nv("block reduction");
   const size_t n = Su_.size() * Sl_.size();
   if (world_ == 1) return A_acc_.as<double>();
   if (!reduced_) {
@@ -1295,6 +1339,7 @@ double *Engine::reduced_block() {
 }
 
 void Engine::amplitudes(void *amps) {
+  Nvtx nv("qsim_amplitudes");
   if (!have_blocks_) throw Error(QSIM_ESTATE, "no blocks evolved");
   ensure_device();
   double *A = reduced_block();
@@ -1342,6 +1387,7 @@ void Engine::run_sampler(const double *p, int64_t M, int64_t N, const uint64_t *
 }
 
 void Engine::sample(uint64_t seed, size_t n, uint64_t *out, double *mass) {
+  Nvtx nv("qsim_sample");
   if (!have_blocks_) throw Error(QSIM_ESTATE, "no blocks evolved");
   ensure_device();
   double *A = reduced_block();
@@ -1475,7 +1521,7 @@ void Engine::branch_state(int half, uint64_t b, void *out) {
   full_leaf_ = true;
   try {
     if (deferred_ && !dist_ && he.tree)
-      evolve_tree(half, b, b + 1, slice.ptr, tmp_.as<uint64_t>(), (int64_t)n);
+      evolve_tree(half, b, b + 1, slice.ptr, tmp_.as<uint64_t>(), (int64_t)n, true);
     else
       evolve_half(half, b, b + 1, slice.ptr, tmp_.as<uint64_t>(), (int64_t)n);
   } catch (...) {
@@ -1512,7 +1558,7 @@ void Engine::branch_values(int half, uint64_t b, const uint64_t *idx, size_t n, 
   slice.reserve(n * amp_);
   check(cudaMemcpyAsync(dS.ptr, P.data(), n * 8, cudaMemcpyHostToDevice, stream_), "upload idx");
   if (deferred_ && !dist_ && he.tree)
-    evolve_tree(half, b, b + 1, slice.ptr, dS.as<uint64_t>(), (int64_t)n);
+    evolve_tree(half, b, b + 1, slice.ptr, dS.as<uint64_t>(), (int64_t)n, true);
   else
     evolve_half(half, b, b + 1, slice.ptr, dS.as<uint64_t>(), (int64_t)n);
   if (dist_ && world_ > 1) {
@@ -1730,6 +1776,7 @@ void Engine::launch_nodes(const TilePlan &tp, const void *src, void *dst, int lo
     check(cudaEventRecord(e0, stream_), "cudaEventRecord");
   }
   TileSweepParams p = tp.p;
+  p.no_pskip = pskip_ ? 0 : 1;
   p.pre = to_dev(pre, pre_mode != 0);
   p.njobs = 1;
   p.src[0] = src;
@@ -2035,24 +2082,71 @@ TreeChoice Engine::choose_tree(int half, int m, int lz, int64_t nS, int nbuf, bo
   return best;
 }
 
-TreeVariant &Engine::variant(int half, const std::vector<int> &apply) {
+TreeVariant &Engine::variant(int half, const std::vector<int> &apply, const std::vector<char> &roles) {
   HalfExec &he = half_[half];
-  auto it = he.variants.find(apply);
+  std::vector<int> key = apply;
+  for (char r : roles) key.push_back(r ? -1 : -2);
+  auto it = he.variants.find(key);
   if (it != he.variants.end()) return *it->second;
   if (he.variants.size() >= 64) he.variants.clear();
   auto v = std::make_unique<TreeVariant>();
   const bool up = half == 0;
   const std::vector<int> &perm = he.prog.perm;
-  v->prog = compile_part(circ_, up ? 0 : circ_.h_u, up ? circ_.h_u : circ_.n, up, half_cuts(circ_, up),
+  v->prog = compile_part(circ_, up ? 0 : circ_.h_u, up ? circ_.h_u : circ_.n, up,
+                         half_cuts(circ_, up, roles.empty() ? nullptr : &roles),
                          std::vector<std::vector<int>>(circ_.depth + 2, perm), perm, &apply);
   plan_levels(v->prog, v->plans, true);
   TreeVariant &ref = *v;
-  he.variants[apply] = std::move(v);
+  he.variants[key] = std::move(v);
   return ref;
 }
 
+// Which endpoint of each cut gets the projector (Eq. 1 both ways, program.h half_cuts).  The sweep
+// that applies a deferred P_b fork does not load the half of its tile the projector zeroes
+// (sweep_tma.cu), a Z^b fork saves nothing: P goes to the half whose fork of that cut runs on
+// more tree nodes (2^{forks placed before it} for the whole-range tree of each half).
+void Engine::choose_roles() {
+  roles_chosen_ = true;
+  roles_.clear();
+  const int c = (int)circ_.cuts.size();
+  if (!roles_auto_ || dist_ || c == 0 || !half_[0].tree || !half_[1].tree) return;
+  std::vector<double> w[2];
+  for (int h = 0; h < 2; ++h) {
+    HalfExec &he = half_[h];
+    if (he.glayers.empty()) {
+      const bool up = h == 0;
+      he.glayers = gate_layers(circ_, up ? 0 : circ_.h_u, up ? circ_.h_u : circ_.n);
+      he.ft = first_targets(circ_, half_cuts(circ_, up));
+    }
+    const int64_t nS = (int64_t)(h == 0 ? Su_.size() : Sl_.size());
+    const int lz = tree_lazy(h, nS);
+    const TreeChoice tc = choose_tree(h, c, lz, nS, 6, true);
+    w[h].assign(c, 0.0);
+    const int S = (int)he.glayers.size();
+    const int last_mat = S - lz > 0 ? he.glayers[S - lz - 1] : 0;
+    for (int g = 0; g < c; ++g) {
+      if (tc.apply[g] > last_mat) continue;  // forks in the gather: no sweep reads it
+      int before = 0;
+      for (int x = 0; x < c; ++x) before += tc.apply[x] < tc.apply[g];
+      w[h][g] = std::ldexp(1.0, before);
+    }
+  }
+  roles_.assign(c, 1);
+  bool any = false;
+  for (int g = 0; g < c; ++g)
+    if (w[1][g] > w[0][g]) roles_[g] = 0, any = true;
+  if (!any) roles_.clear();
+  if (std::getenv("QSIM_DEBUG_TREE")) {
+    std::fprintf(stderr, "roles (1 = P on the upper endpoint):");
+    for (int g = 0; g < c; ++g) std::fprintf(stderr, " %d", roles_.empty() ? 1 : (int)roles_[g]);
+    std::fprintf(stderr, "\n");
+  }
+}
+
 // [b0, b1) as aligned power-of-two blocks; slice row r = branch b0 + r
-void Engine::evolve_tree(int half, uint64_t b0, uint64_t b1, void *slice, const uint64_t *dS, int64_t nS) {
+void Engine::evolve_tree(int half, uint64_t b0, uint64_t b1, void *slice, const uint64_t *dS, int64_t nS,
+                         bool canonical) {
+  Nvtx nv(half == 0 ? "upper half tree" : "lower half tree");
   HalfExec &he = half_[half];
   if (he.glayers.empty()) {
     const bool up = half == 0;
@@ -2063,12 +2157,14 @@ void Engine::evolve_tree(int half, uint64_t b0, uint64_t b1, void *slice, const 
   for (uint64_t s = b0; s < b1;) {
     int m = 0;
     while (m < c && ((s >> m) & 1u) == 0 && s + (2ull << m) <= b1) ++m;
-    evolve_block(half, s, m, (char *)slice + (s - b0) * (uint64_t)nS * amp_, dS, nS);
+    static const std::vector<char> none;
+    evolve_block(half, s, m, (char *)slice + (s - b0) * (uint64_t)nS * amp_, dS, nS, canonical ? none : roles_);
     s += 1ull << m;
   }
 }
 
-void Engine::evolve_block(int half, uint64_t b0, int m, void *slice, const uint64_t *dS, int64_t nS) {
+void Engine::evolve_block(int half, uint64_t b0, int m, void *slice, const uint64_t *dS, int64_t nS,
+                          const std::vector<char> &roles) {
   HalfExec &he = half_[half];
   const int c = (int)circ_.cuts.size();
   const int T = tile_low_bits(c128_) + kHiBits;
@@ -2098,7 +2194,12 @@ void Engine::evolve_block(int half, uint64_t b0, int m, void *slice, const uint6
   int nbuf = (int)std::min<size_t>(nfit, 12);
   if (mem_budget_ > 0) nbuf = std::max(1, std::min<int>(nbuf, (int)((size_t)mem_budget_ / state_bytes_)));
   const TreeChoice tc = choose_tree(half, m, lz, nS, nbuf, !bfs);
-  const TreeVariant &v = variant(half, tc.apply);
+  // a swapped cut (P on the lower endpoint) changes the single branches, only the sum over both
+  // values of its bit is CZ: the block's fixed bits keep the canonical roles (qsim.h: U_b, L_b)
+  std::vector<char> eff = roles;
+  for (int g = 0; g < c - m && g < (int)eff.size(); ++g) eff[g] = 1;
+  if (std::find(eff.begin(), eff.end(), 0) == eff.end()) eff.clear();
+  const TreeVariant &v = variant(half, tc.apply, eff);
   ensure_states(half, tc.points + 1);
   size_t bfs_avail = 0;  // memory the level-synchronous buffers may take (0: none)
   if (bfs) {
@@ -2362,6 +2463,7 @@ void Engine::run_tree(int half, const TreeVariant &v, int lz, const std::vector<
 // without sweeps (cuts never targeted again) its post diagonal; one output row per fork value.
 void Engine::gather_tree(const TreeVariant &v, int lz, int M, const std::vector<int> &pin, const void *psi,
                          uint64_t bacc, int m, void *slice, const uint64_t *dS, int64_t nS) {
+  Nvtx nv("leaf gather");
   const HalfProgram &hp = v.prog;
   const int F = (int)hp.levels.size() - 1, c = (int)circ_.cuts.size();
   const uint64_t rmask = m >= 64 ? ~0ull : ((1ull << m) - 1ull);

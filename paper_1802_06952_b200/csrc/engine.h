@@ -194,7 +194,8 @@ class Engine {
   void plan_distributed(HalfExec &he);      // layout schedule with fused local/global swaps
   void dist_buffers(size_t bytes, int nbuf);  // level buffers + IPC peer pointers
   void dist_barrier();                      // stream-ordered barrier over the ranks
-  std::vector<int> choose_perm(const HalfExec &he, int64_t nS = 0) const;
+  std::vector<int> choose_perm(const HalfExec &he, int64_t nS = 0, const std::vector<double> *layer_w = nullptr) const;
+  std::vector<double> deferred_layer_weights(int half, int64_t nS);
   int lazy_depth_of(const HalfProgram &hp, int64_t nS) const;
   int64_t perm_ns_[2] = {0, 0};  // block sizes the relabelling of each half was chosen for
   std::vector<TilePlan> level_launches(const HalfProgram &hp, const Level &lev, size_t n);
@@ -207,9 +208,18 @@ class Engine {
   void plan_levels(const HalfProgram &hp, std::vector<std::vector<std::vector<TilePlan>>> &plans, bool all_skips);
   int tree_lazy(int half, int64_t nS) const;
   TreeChoice choose_tree(int half, int m, int lz, int64_t nS, int nbuf, bool allow_gather) const;
-  TreeVariant &variant(int half, const std::vector<int> &apply);
-  void evolve_tree(int half, uint64_t b0, uint64_t b1, void *slice, const uint64_t *dS, int64_t nS);
-  void evolve_block(int half, uint64_t b0, int m, void *slice, const uint64_t *dS, int64_t nS);
+  TreeVariant &variant(int half, const std::vector<int> &apply, const std::vector<char> &roles);
+  // canonical: P_b on the upper endpoint of every cut (the branch states of qsim_branch_state /
+  // qsim_branch_values); else the per-cut roles_ of the reconstruction (choose_roles)
+  void evolve_tree(int half, uint64_t b0, uint64_t b1, void *slice, const uint64_t *dS, int64_t nS,
+                   bool canonical = false);
+  void evolve_block(int half, uint64_t b0, int m, void *slice, const uint64_t *dS, int64_t nS,
+                    const std::vector<char> &roles);
+  void choose_roles();
+  std::vector<char> roles_;  // per cut: 1 = P on the upper endpoint (empty: all 1)
+  bool roles_chosen_ = false;
+  // off by default: same-box A/B within noise (C5 +0.9 %, C4 -2 %); QSIM_ROLES=1 on
+  bool roles_auto_ = std::getenv("QSIM_ROLES") && std::getenv("QSIM_ROLES")[0] == '1';
   void run_tree(int half, const TreeVariant &v, int lz, const std::vector<int> &pin, int m, void *slice,
                 const uint64_t *dS, int64_t nS, size_t bfs_avail);
   void gather_tree(const TreeVariant &v, int lz, int M, const std::vector<int> &pin, const void *psi,
@@ -221,6 +231,8 @@ class Engine {
   DevBuf rowmap_;
   bool deferred_ = !(std::getenv("QSIM_DEFER") && std::getenv("QSIM_DEFER")[0] == '0');
   int max_ctas_ = 0;  // QSIM_OPT_MAX_CTAS (tests)
+  // rows / tiles the pre projector zeroes are not loaded (QSIM_PSKIP=0: off, A/B only)
+  bool pskip_ = !(std::getenv("QSIM_PSKIP") && std::getenv("QSIM_PSKIP")[0] == '0');
   uint32_t skip_pm_last_ = 0;  // known-zero tile mask of the last planned launch (stats)
   int grid_ctas() const { return max_ctas_ > 0 ? std::min(max_ctas_, num_sms_) : num_sms_; }
 

@@ -103,6 +103,8 @@ struct TileSweepParams {
   // bits there differ from the node's branch bits is zero (not loaded)
   int32_t fork_apply;
   uint32_t nb_skip;
+  // 1: load every row even where the pre projector zeroes it (A/B of the in-tile skip)
+  int32_t no_pskip;
 };
 
 // pre_mode: 0 none, 1 apply pre diagonal to loaded values, 2 generate (no load)

@@ -204,9 +204,13 @@ HalfProgram compile_half(const Circuit &c, bool upper, const std::vector<int> &p
   return compile_half_layers(c, upper, std::vector<std::vector<int>>(c.depth + 2, p), p);
 }
 
-std::vector<PartCut> half_cuts(const Circuit &c, bool upper) {
+std::vector<PartCut> half_cuts(const Circuit &c, bool upper, const std::vector<char> *p_upper) {
   std::vector<PartCut> cuts;
-  for (const qsim_cut &cut : c.cuts) cuts.push_back(PartCut{(int)cut.layer, upper ? cut.q_upper : cut.q_lower, upper});
+  for (size_t g = 0; g < c.cuts.size(); ++g) {
+    const qsim_cut &cut = c.cuts[g];
+    const bool pu = p_upper ? (*p_upper)[g] != 0 : true;
+    cuts.push_back(PartCut{(int)cut.layer, upper ? cut.q_upper : cut.q_lower, upper ? pu : !pu});
+  }
   return cuts;
 }
 

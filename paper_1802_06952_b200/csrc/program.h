@@ -136,8 +136,10 @@ HalfProgram compile_part(const Circuit &c, uint32_t lo, uint32_t hi, bool upper,
 // Layer of the first X^1/2 / Y^1/2 gate on the cut's qubit after the cut layer (depth + 1: none):
 // the latest layer at whose input the cut's fork may be applied.
 std::vector<int> first_targets(const Circuit &c, const std::vector<PartCut> &cuts);
-// The cut list of a half as PartCuts (P on the upper endpoint, Z on the lower one).
-std::vector<PartCut> half_cuts(const Circuit &c, bool upper);
+// The cut list of a half as PartCuts.  p_upper[g] = 1 (default for every cut): P_b on the upper
+// endpoint, Z^b on the lower one (Eq. 1; R6); 0: the same identity read the other
+// way round, CZ = I (x) P0 + Z (x) P1 (P_b on the lower endpoint, Z^b on the upper one).
+std::vector<PartCut> half_cuts(const Circuit &c, bool upper, const std::vector<char> *p_upper = nullptr);
 // Layers in [1, depth] holding at least one X^1/2 / Y^1/2 gate on a qubit in [lo, hi).
 std::vector<int> gate_layers(const Circuit &c, uint32_t lo, uint32_t hi);
 

@@ -197,13 +197,16 @@ __device__ __forceinline__ void fork_masks(const uint32_t tg, const uint64_t nod
   constexpr int VB = NV == 2 ? 1 : 0;
   constexpr uint32_t pat[5] = {0xAAAAAAAAu, 0xCCCCCCCCu, 0xF0F0F0F0u, 0xFF00FF00u, 0xFFFF0000u};
   uint32_t fm = 0, fv = 0, zm = 0;
+  bool empty = false;  // P0 and P1 on one bit (two cuts on one qubit): the child is zero
   for (int j = 0; j < p.fork.n; ++j) {
     const uint32_t cb = (uint32_t)(node >> (p.fork.n - 1 - j)) & 1u;
     const uint32_t m = 1u << p.fork.bit[j];
-    if ((p.fork.pmask >> j) & 1u)
+    if ((p.fork.pmask >> j) & 1u) {
+      if ((fm & m) && ((fv & m) != (cb ? m : 0u))) empty = true;
       fm |= m, fv |= cb ? m : 0u;
-    else if (cb)
-      zm |= m;
+    } else if (cb) {
+      zm ^= m;  // Z^2 = I
+    }
   }
   uint32_t sb[VB + 4];  // state bit of index bit j
   if (VB) sb[0] = 1u;
@@ -212,7 +215,7 @@ __device__ __forceinline__ void fork_masks(const uint32_t tg, const uint64_t nod
   uint32_t smask = 0;
 #pragma unroll
   for (int j = 0; j < VB + 4; ++j) smask |= sb[j];
-  zero = (((tg & fm) ^ fv) & ~smask) ? 0xFFFFFFFFu : 0u;
+  zero = (empty || (((tg & fm) ^ fv) & ~smask)) ? 0xFFFFFFFFu : 0u;
   neg = (__popc(tg & zm & ~smask) & 1) ? 0xFFFFFFFFu : 0u;
 #pragma unroll
   for (int j = 0; j < VB + 4; ++j) {
@@ -281,9 +284,22 @@ __global__ void __launch_bounds__(544, 1) tile_sweep_tma_kernel(const __grid_con
     tab_post[tid].x = (R)(c_omega[2 * tid] * p.post.scale);
     tab_post[tid].y = (R)(c_omega[2 * tid + 1] * p.post.scale);
   }
+  // A projector in the pre diagonal (a deferred fork P_b on a bit of the tile, or on an outer bit)
+  // zeroes every element where it fails, so those rows / tiles are not loaded: the contiguous run
+  // is cut at the lowest projected hi bit (m_eff), and runs / rows / tiles whose projected bits
+  // differ from the projector's values are skipped (their stale shared-memory contents are zeroed
+  // by the projector in apply_split before any arithmetic uses them).
+  const uint32_t ppm = (PRE == 1 && !p.no_pskip) ? p.pre.pm : 0u, ppv = p.pre.pv;
+  int m_eff = p.run_m;
+  for (int j = 0; j < p.run_m; ++j)
+    if ((ppm >> p.hb[j]) & 1u) {
+      m_eff = j;
+      break;
+    }
+  if (m_eff < 2 && p.run_m >= 2) m_eff = p.run_m;  // do not trade bulk runs for per-row loads
   // long contiguous runs: one cp.async.bulk per run (1 arrival + tx bytes); short runs
   // (< 2 KB): per-lane 16-byte cp.async, a warp instruction per 512-byte row (32 arrivals)
-  const bool bulk = p.run_m >= 2;
+  const bool bulk = m_eff >= 2;
   if (tid == 0) {
     for (int s = 0; s < NST; ++s) {
       mbar_init(&full_bar[s][0], bulk ? 1 : 32);
@@ -308,12 +324,21 @@ __global__ void __launch_bounds__(544, 1) tile_sweep_tma_kernel(const __grid_con
   if (warp == 16) {
     if constexpr (PRE == 2) return;  // generated sweep: nothing to load
     // ------------------------------------------------ producer: TMA bulk copies
-    const int m = p.run_m;
+    const int m = m_eff;
     const int rbits = kHiBits - m;
     const int nruns = 1 << rbits;
     const uint32_t run_log2 = L + m;
     const uint32_t run_bytes = (uint32_t)sizeof(C) << run_log2;
     const char *srcb = reinterpret_cast<const char *>(p.src[0]);
+    uint32_t hmask = 0, runmask = 0;  // hi bits of the tile; those enumerating the runs
+    for (int j = 0; j < kHiBits; ++j) {
+      hmask |= 1u << p.hb[j];
+      if (j >= m) runmask |= 1u << p.hb[j];
+    }
+    const uint32_t lowmask = (1u << L) - 1u;
+    const uint32_t pout = ppm & ~(hmask | lowmask);          // projected outer bits: whole tiles
+    const int npb = __popc(ppm & runmask);                   // projected run bits: 2^-npb of the runs
+    const uint32_t tx_bytes = (uint32_t)kTileBytes >> npb;
     for (int it = 0;; ++it) {
       const uint64_t t = blockIdx.x + (uint64_t)it * gridDim.x;
       if (t >= ntiles) break;
@@ -328,7 +353,8 @@ __global__ void __launch_bounds__(544, 1) tile_sweep_tma_kernel(const __grid_con
       uint32_t spm = p.skip_pm, spv = p.skip_pv;
       if constexpr (NB == 1) spv = nb_skip_value(t >> p.log2_ntiles, p), spm = p.nb_skip;
       {
-        if ((outer & spm) != spv) {  // known-zero tile: complete the phase without loading
+        // known-zero tile, or a tile the pre projector zeroes: complete the phase without loading
+        if ((outer & spm) != spv || (((outer | p.gbase) ^ ppv) & pout)) {
           if (bulk) {
             if (lane == 0) mbar_arrive(fb);
           } else {
@@ -338,26 +364,27 @@ __global__ void __launch_bounds__(544, 1) tile_sweep_tma_kernel(const __grid_con
         }
       }
       if (bulk) {
-        if (lane == 0) mbar_arrive_expect_tx(fb, kTileBytes);
+        if (lane == 0) mbar_arrive_expect_tx(fb, tx_bytes);
         __syncwarp();
         for (int q = lane; q < nruns; q += 32) {
           uint32_t gi = outer;
           for (int j = 0; j < rbits; ++j)
             if ((q >> j) & 1) gi |= 1u << p.hb[m + j];
+          if ((gi ^ ppv) & ppm & runmask) continue;  // zeroed by the projector
           bulk_g2s(stage + ((size_t)q << run_log2) * sizeof(C), src + (size_t)gi * sizeof(C), run_bytes, fb);
         }
       } else {
         // vector vi = lane + 32 q: row q of the tile = deposit of q's 7 bits on hb[]
-        uint32_t hmask = 0;
-        for (int j = 0; j < kHiBits; ++j) hmask |= 1u << p.hb[j];
         const char *srcl = src + (size_t)(outer | ((uint32_t)lane << VB)) * sizeof(C);
         char *dstl = stage + (size_t)lane * 16;
+        const uint32_t rpm = ppm & hmask, rpv = ppv & rpm;
         uint32_t d = 0;
 #pragma unroll 8
         for (int q = 0; q < NVEC / 32; ++q) {
-          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_addr(dstl + (size_t)q * 512)),
-                       "l"(srcl + (size_t)d * sizeof(C))
-                       : "memory");
+          if ((d & rpm) == rpv)
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_addr(dstl + (size_t)q * 512)),
+                         "l"(srcl + (size_t)d * sizeof(C))
+                         : "memory");
           d = ((d | ~hmask) + 1u) & hmask;
         }
         asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_addr(fb)) : "memory");
