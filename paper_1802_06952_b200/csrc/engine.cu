@@ -930,8 +930,45 @@ void Engine::launch_plan(const TilePlan &tp, const Diag &fork, bool first, const
   const int h = hp.hl;
   int pre_mode = 0;
   Diag pre;
+  TileSweepParams p = tp.p;
+  // a fork bit this launch targets is applied inside its gate (gate kind k + 2 f, sweep_tma.cu)
+  // instead of through the pre diagonal: a Z^b or P_b fork then costs no per-element multiply
+  uint32_t absorbed_pm = 0, absorbed_pv = 0;
+  Diag fk = fork;
+  if (tp.use_pre && absorb_ && !tp.gen && sweep_kernel_ != 1 && !dist_ && !fork.allzero) {
+    const int L = tile_low_bits(c128_), VB = c128_ ? 0 : 1;
+    const uint32_t cand = (fork.pm ^ fork.zm) & (fork.pm | fork.zm) & tp.targets & ~(fork.t1 | fork.t2);
+    for (int q = 0; q < 32; ++q) {
+      if (!((cand >> q) & 1u)) continue;
+      const uint32_t m = 1u << q;
+      const int f = (fork.pm & m) ? ((fork.pv & m) ? 3 : 2) : 1;
+      uint8_t *k = nullptr;
+      if (q >= L) {
+        for (int j = 0; j < kHiBits && !k; ++j)
+          if (p.hb[j] == q)
+            for (int ps = 0; ps < tp.npass && !k; ++ps)
+              for (int s4 = 0; s4 < 4 && !k; ++s4)
+                if (p.gsel[ps][s4] == j && p.gkind[ps][s4]) k = &p.gkind[ps][s4];
+      } else if (VB && q == 0) {
+        if (p.lowkind[0]) k = &p.lowkind[0];
+      } else {
+        for (int i = 0; i < p.n_lane && !k; ++i)
+          if (p.lane_bit[i] == q - VB) k = &p.lane_kind[i];
+      }
+      if (!k || *k > 2) continue;
+      *k = (uint8_t)(*k + 2 * f);
+      if (f == 1) {
+        fk.zm &= ~m;
+      } else {
+        fk.pm &= ~m;
+        fk.pv &= ~m;
+        absorbed_pm |= m;
+        if (f == 3) absorbed_pv |= m;
+      }
+    }
+  }
   if (tp.use_pre) {
-    pre = Diag::merge(fork, tp.pre);
+    pre = Diag::merge(fk, tp.pre);
     if (tp.gen)
       pre_mode = 2;
     else if (!pre.identity())
@@ -946,9 +983,10 @@ void Engine::launch_plan(const TilePlan &tp, const Diag &fork, bool first, const
   }
   skip_pm_last_ = 0;
   {
-    TileSweepParams p = tp.p;
     p.no_pskip = pskip_ ? 0 : 1;
     p.pre = to_dev(pre, pre_mode != 0);
+    p.ld_pm = (pre_mode == 1 ? p.pre.pm : 0u) | absorbed_pm;
+    p.ld_pv = (pre_mode == 1 ? p.pre.pv : 0u) | absorbed_pv;
     p.njobs = 1;
     if (dist_) {
       p.gbase = (uint32_t)rank_ << hp.hl;
@@ -1778,6 +1816,8 @@ void Engine::launch_nodes(const TilePlan &tp, const void *src, void *dst, int lo
   TileSweepParams p = tp.p;
   p.no_pskip = pskip_ ? 0 : 1;
   p.pre = to_dev(pre, pre_mode != 0);
+  p.ld_pm = pre_mode == 1 ? p.pre.pm : 0u;
+  p.ld_pv = pre_mode == 1 ? p.pre.pv : 0u;
   p.njobs = 1;
   p.src[0] = src;
   p.dst[0] = dst;

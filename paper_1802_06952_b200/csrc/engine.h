@@ -231,6 +231,8 @@ class Engine {
   DevBuf rowmap_;
   bool deferred_ = !(std::getenv("QSIM_DEFER") && std::getenv("QSIM_DEFER")[0] == '0');
   int max_ctas_ = 0;  // QSIM_OPT_MAX_CTAS (tests)
+  // deferred forks on a bit the sweep targets are folded into that gate (QSIM_ABSORB=0: off, A/B)
+  bool absorb_ = !(std::getenv("QSIM_ABSORB") && std::getenv("QSIM_ABSORB")[0] == '0');
   // rows / tiles the pre projector zeroes are not loaded (QSIM_PSKIP=0: off, A/B only)
   bool pskip_ = !(std::getenv("QSIM_PSKIP") && std::getenv("QSIM_PSKIP")[0] == '0');
   uint32_t skip_pm_last_ = 0;  // known-zero tile mask of the last planned launch (stats)

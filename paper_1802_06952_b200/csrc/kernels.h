@@ -70,7 +70,9 @@ struct TileSweepParams {
   uint8_t hb[kHiBits];                 // hi tile bit positions, ascending
   uint8_t gsel[2][4];                  // pass p: hb indices held in registers
   uint8_t wsel[2][3];                  // pass p: hb indices mapped to the 3 warp bits
-  uint8_t gkind[2][4];                 // gate kind (0 none, 1 SX', 2 SY') per register bit
+  // gate kinds: 0 none, 1 SX', 2 SY'; the TMA sweep also takes k + 2 f with a deferred fork on the
+  // gate's own bit applied just before it (f = 1 Z^1, 2 P0, 3 P1; sweep_tma.cu reg_gates)
+  uint8_t gkind[2][4];                 // gate kind per register bit
   uint8_t lowkind[6];                  // gate kind per low bit (lane / vector bits), pass 0
   DiagDev pre, post;
   DiagSplit pre_s, post_s;  // TMA sweep: pre uses the pass-0 registers, post the last pass's
@@ -103,7 +105,9 @@ struct TileSweepParams {
   // bits there differ from the node's branch bits is zero (not loaded)
   int32_t fork_apply;
   uint32_t nb_skip;
-  // 1: load every row even where the pre projector zeroes it (A/B of the in-tile skip)
+  // the projector of this sweep's input (pre diagonal + the P forks folded into gate kinds): rows /
+  // tiles it zeroes are not loaded; no_pskip = 1 loads them anyway (A/B)
+  uint32_t ld_pm, ld_pv;
   int32_t no_pskip;
 };
 

@@ -91,41 +91,64 @@ __device__ __forceinline__ void apply_split(typename Cx2<R>::T (&v)[16][NV], con
   }
 }
 
+// Gate kinds (kernels.h): k = g + 2 f, g = 1 SX' / 2 SY', f = the deferred fork this sweep applies
+// on the gate's own bit just before the gate (0 none, 1 Z^1: negate the bit-1 side, 2 P0: zero
+// the bit-1 side, 3 P1: zero the bit-0 side; Eq. 1 / DESIGN.md §5): cheaper than a pre diagonal.
+__device__ __forceinline__ int kind_gate(int k) { return ((k - 1) & 1) + 1; }
+__device__ __forceinline__ int kind_fork(int k) { return (k - 1) >> 1; }
+template <typename C>
+__device__ __forceinline__ void fork_side(C &x, bool hi, int f) {
+  if (f == 1) {
+    if (hi) x.x = -x.x, x.y = -x.y;
+  } else if ((f == 2 && hi) || (f == 3 && !hi)) {
+    x.x = 0;
+    x.y = 0;
+  }
+}
+template <typename C>
+__device__ __forceinline__ void bfly(C &a, C &b, int g) {
+  using R = decltype(a.x);
+  const R ax = a.x, ay = a.y;
+  if (g == 1) {  // SX' = [[1,-i],[-i,1]]
+    a.x = ax + b.y;
+    a.y = ay - b.x;
+    b.x = b.x + ay;
+    b.y = b.y - ax;
+  } else {  // SY' = [[1,-1],[1,1]]
+    a.x = ax - b.x;
+    a.y = ay - b.y;
+    b.x = ax + b.x;
+    b.y = ay + b.y;
+  }
+}
+
 // gates on the 4 register hi bits of a pass (kinds are uniform: branch outside the loops)
 template <typename R, int NV>
 __device__ __forceinline__ void reg_gates(typename Cx2<R>::T (&v)[16][NV], const uint8_t *kinds) {
 #pragma unroll
   for (int s = 0; s < 4; ++s) {
     const int k = kinds[s];
-    if (k == 1) {
+    if (!k) continue;
+    const int f = kind_fork(k), g = kind_gate(k);
+    if (f) {
+#pragma unroll
+      for (int r = 0; r < 16; ++r)
+#pragma unroll
+        for (int e = 0; e < NV; ++e) fork_side(v[r][e], (r >> s) & 1, f);
+    }
+    if (g == 1) {
 #pragma unroll
       for (int r = 0; r < 16; ++r) {
         if (r & (1 << s)) continue;
 #pragma unroll
-        for (int e = 0; e < NV; ++e) {
-          auto &a = v[r][e];
-          auto &b = v[r | (1 << s)][e];
-          const R ax = a.x, ay = a.y;
-          a.x = ax + b.y;
-          a.y = ay - b.x;
-          b.x = b.x + ay;
-          b.y = b.y - ax;
-        }
+        for (int e = 0; e < NV; ++e) bfly(v[r][e], v[r | (1 << s)][e], 1);
       }
-    } else if (k == 2) {
+    } else {
 #pragma unroll
       for (int r = 0; r < 16; ++r) {
         if (r & (1 << s)) continue;
 #pragma unroll
-        for (int e = 0; e < NV; ++e) {
-          auto &a = v[r][e];
-          auto &b = v[r | (1 << s)][e];
-          const R ax = a.x, ay = a.y;
-          a.x = ax - b.x;
-          a.y = ay - b.y;
-          b.x = ax + b.x;
-          b.y = ay + b.y;
-        }
+        for (int e = 0; e < NV; ++e) bfly(v[r][e], v[r | (1 << s)][e], 2);
       }
     }
   }
@@ -134,35 +157,38 @@ __device__ __forceinline__ void reg_gates(typename Cx2<R>::T (&v)[16][NV], const
 // gates on the vector bit (c64, in registers) and on lane bits (warp shuffles)
 template <typename R, int NV>
 __device__ __forceinline__ void low_gates(typename Cx2<R>::T (&v)[16][NV], const TileSweepParams &p, int lane) {
-  using C = typename Cx2<R>::T;
   if constexpr (NV == 2) {
     const int k = p.lowkind[0];
-    if (k == 1) {
+    if (k) {
+      const int f = kind_fork(k), g = kind_gate(k);
+      if (f) {
 #pragma unroll
-      for (int r = 0; r < 16; ++r) {
-        C &a = v[r][0], &b = v[r][1];
-        const R ax = a.x, ay = a.y;
-        a.x = ax + b.y;
-        a.y = ay - b.x;
-        b.x = b.x + ay;
-        b.y = b.y - ax;
+        for (int r = 0; r < 16; ++r) {
+          fork_side(v[r][0], false, f);
+          fork_side(v[r][1], true, f);
+        }
       }
-    } else if (k == 2) {
+      if (g == 1) {
 #pragma unroll
-      for (int r = 0; r < 16; ++r) {
-        C &a = v[r][0], &b = v[r][1];
-        const R ax = a.x, ay = a.y;
-        a.x = ax - b.x;
-        a.y = ay - b.y;
-        b.x = ax + b.x;
-        b.y = ay + b.y;
+        for (int r = 0; r < 16; ++r) bfly(v[r][0], v[r][1], 1);
+      } else {
+#pragma unroll
+        for (int r = 0; r < 16; ++r) bfly(v[r][0], v[r][1], 2);
       }
     }
   }
   for (int i = 0; i < p.n_lane; ++i) {
     const int lb = p.lane_bit[i];
     const int mask = 1 << lb;
-    if (p.lane_kind[i] == 1) {  // both partners: v - i w
+    const int f = kind_fork(p.lane_kind[i]);
+    if (f) {
+      const bool hi = (lane >> lb) & 1;
+#pragma unroll
+      for (int r = 0; r < 16; ++r)
+#pragma unroll
+        for (int e = 0; e < NV; ++e) fork_side(v[r][e], hi, f);
+    }
+    if (kind_gate(p.lane_kind[i]) == 1) {  // both partners: v - i w
 #pragma unroll
       for (int r = 0; r < 16; ++r)
 #pragma unroll
@@ -289,7 +315,7 @@ __global__ void __launch_bounds__(544, 1) tile_sweep_tma_kernel(const __grid_con
   // is cut at the lowest projected hi bit (m_eff), and runs / rows / tiles whose projected bits
   // differ from the projector's values are skipped (their stale shared-memory contents are zeroed
   // by the projector in apply_split before any arithmetic uses them).
-  const uint32_t ppm = (PRE == 1 && !p.no_pskip) ? p.pre.pm : 0u, ppv = p.pre.pv;
+  const uint32_t ppm = (PRE != 2 && !p.no_pskip) ? p.ld_pm : 0u, ppv = p.ld_pv;
   int m_eff = p.run_m;
   for (int j = 0; j < p.run_m; ++j)
     if ((ppm >> p.hb[j]) & 1u) {
