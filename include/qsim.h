@@ -255,13 +255,21 @@ typedef struct {
 } qsim_info_t;
 qsim_status qsim_info(qsim_ctx *ctx, qsim_info_t *out);
 
-/* Multi-GPU (one process per GPU).  qsim_nccl_unique_id writes 128 bytes
- * (ncclUniqueId) on rank 0; every rank passes the same bytes to qsim_comm_init, which records
- * rank / world (EINVAL if out of range) — the NCCL communicator is created at the first
- * collective (qsim_amplitudes / qsim_sample, called by every rank), ENCCL on failure. */
+/* Multi-GPU: SURVEY §8(b)'s "multi-process variant" (qsim_create_rank there), one process per GPU
+ * as torchrun launches them, instead of one process driving every GPU through ncclCommInitAll:
+ * each process creates its context on its own device (qsim_create), then qsim_nccl_unique_id writes
+ * 128 bytes (ncclUniqueId) on rank 0; every rank passes the same bytes to qsim_comm_init, which
+ * records rank / world (EINVAL if out of range) — the NCCL communicator is created at the first
+ * collective (qsim_amplitudes / qsim_sample, called by every rank), ENCCL on failure.
+ * qsim_amplitudes: the ranks' partial blocks are summed to rank 0 (ncclReduce).  qsim_sample: the
+ * partial blocks are reduce-scattered by rows, each rank computes |a|^2 and the row prefixes of its
+ * rows, the row masses are all-gathered, every rank draws the same Philox stream and resolves the
+ * draws that fall in its rows, and the draws are summed to rank 0. */
 qsim_status qsim_nccl_unique_id(void *out128);
 qsim_status qsim_comm_init(qsim_ctx *ctx, int rank, int world, const void *unique_id128);
-/* This rank's share [*begin, *end) of the 2^c branches (contiguous, prefix aligned). */
+/* This rank's share [*begin, *end) of the 2^c branches: contiguous, and aligned to the prefix groups
+ * of the first cut period (the cuts of the first two cut layers) whenever world <= their number
+ * (every rank then shares its tree down to its groups); else B r / world. */
 qsim_status qsim_rank_range(qsim_ctx *ctx, uint64_t *begin, uint64_t *end);
 
 /* ---------------------------------------------------------------- planner / cost model (f2) */

@@ -1395,15 +1395,42 @@ void Engine::amplitudes(void *amps) {
   check(cudaStreamSynchronize(stream_), "amplitudes");
 }
 
-void Engine::run_sampler(const double *p, int64_t M, int64_t N, const uint64_t *dSu, const uint64_t *dSl,
-                         uint32_t hl, uint64_t seed, size_t n, uint64_t *out, double *mass) {
-  C_.reserve((size_t)M * N * 8);
+// a8 on rows [row0, row0 + nrows) of an M x N block: p = |a|^2 fused into
+// the row scan when A is given (else p is the caller's), row prefixes C and row masses r of the own
+// rows; with `collective` the ranks' row masses are all-gathered (one broadcast per rank), every
+// rank forms the same R = sequential prefix of r and W = R[M-1], draws the same Philox stream and
+// resolves the draws whose row it owns; the draws are summed to rank 0 (unowned ones are 0).
+void Engine::run_sampler(const double *A, const double *p, int64_t M, int64_t N, int64_t row0, int64_t nrows,
+                         bool collective, const uint64_t *dSu, const uint64_t *dSl, uint32_t hl, uint64_t seed,
+                         size_t n, uint64_t *out, double *mass) {
+  C_.reserve((size_t)std::max<int64_t>(nrows, 1) * N * 8);
   r_.reserve((size_t)M * 8);
   R_.reserve((size_t)M * 8);
   W_.reserve(8);
-  check(launch_row_scan(p, M, N, C_.as<double>(), r_.as<double>(), stream_), "row scan");
+  if (A) {
+    p_.reserve((size_t)std::max<int64_t>(nrows, 1) * N * 8);
+    p = p_.as<double>();
+  }
+  if (nrows > 0) {
+    if (A)
+      check(launch_row_scan_abs2(A, nrows, N, p_.as<double>(), C_.as<double>(), r_.as<double>() + row0, stream_),
+            "row scan");
+    else
+      check(launch_row_scan(p, nrows, N, C_.as<double>(), r_.as<double>() + row0, stream_), "row scan");
+    st_.kernel_launches++;
+  }
+  if (collective && world_ > 1) {
+    ncclGroupStart();
+    for (int q = 0; q < world_; ++q) {
+      const int64_t q0 = M * q / world_, q1 = M * (q + 1) / world_;
+      if (q1 > q0)
+        ncclBroadcast(r_.as<double>() + q0, r_.as<double>() + q0, (size_t)(q1 - q0), ncclDouble, q, comm_, stream_);
+    }
+    const ncclResult_t rr = ncclGroupEnd();
+    if (rr != ncclSuccess) throw Error(QSIM_ENCCL, std::string("row-mass all-gather: ") + ncclGetErrorString(rr));
+  }
   check(launch_row_prefix(r_.as<double>(), M, R_.as<double>(), W_.as<double>(), stream_), "row prefix");
-  st_.kernel_launches += 2;
+  st_.kernel_launches++;
   if (out || mass) {
     double W = 0;
     check(cudaMemcpyAsync(&W, W_.ptr, 8, cudaMemcpyDeviceToHost, stream_), "D2H block mass");
@@ -1413,11 +1440,15 @@ void Engine::run_sampler(const double *p, int64_t M, int64_t N, const uint64_t *
   }
   if (n > 0) {
     draws_.reserve(n * 8);
-    check(launch_draws(p, C_.as<double>(), r_.as<double>(), R_.as<double>(), W_.as<double>(), M, N, dSu,
-                       dSl, hl, seed, (int64_t)n, draws_.as<uint64_t>(), stream_),
+    check(launch_draws(p, C_.as<double>(), r_.as<double>(), R_.as<double>(), W_.as<double>(), M, N, dSu, dSl, hl,
+                       seed, (int64_t)n, draws_.as<uint64_t>(), stream_, row0, nrows),
           "draws");
     st_.kernel_launches++;
-    if (out) {
+    if (collective && world_ > 1) {
+      const ncclResult_t r = ncclReduce(draws_.ptr, draws_.ptr, n, ncclUint64, ncclSum, 0, comm_, stream_);
+      if (r != ncclSuccess) throw Error(QSIM_ENCCL, std::string("ncclReduce (draws): ") + ncclGetErrorString(r));
+    }
+    if (out && (!collective || rank_ == 0)) {
       check(cudaMemcpyAsync(out, draws_.ptr, n * 8, cudaMemcpyDeviceToHost, stream_), "D2H draws");
       check(cudaStreamSynchronize(stream_), "sample");
     }
@@ -1428,17 +1459,32 @@ void Engine::sample(uint64_t seed, size_t n, uint64_t *out, double *mass) {
   Nvtx nv("qsim_sample");
   if (!have_blocks_) throw Error(QSIM_ESTATE, "no blocks evolved");
   ensure_device();
-  double *A = reduced_block();
-  if (!A) {
-    check(cudaStreamSynchronize(stream_), "sample");
+  const int64_t M = (int64_t)Su_.size(), N = (int64_t)Sl_.size();
+  if (world_ == 1) {
+    run_sampler(A_acc_.as<double>(), nullptr, M, N, 0, M, false, d_Su_.as<uint64_t>(), d_Sl_.as<uint64_t>(),
+                circ_.h_l, seed, n, out, mass);
     return;
   }
-  const int64_t M = (int64_t)Su_.size(), N = (int64_t)Sl_.size();
-  p_.reserve((size_t)M * N * 8);
-  check(launch_abs2(A, M * N, p_.as<double>(), stream_), "abs2");
-  st_.kernel_launches++;
-  run_sampler(p_.as<double>(), M, N, d_Su_.as<uint64_t>(), d_Sl_.as<uint64_t>(), circ_.h_l, seed, n, out,
-              mass);
+  // a7 as SURVEY §8(e): the partial blocks reduce-scattered by rows (one ncclReduce per row shard),
+  // then a8 on the own rows with the row masses all-gathered ("the components they possess are
+  // calculated and then added")
+  ensure_comm();
+  const int64_t r0 = M * rank_ / world_, r1 = M * (rank_ + 1) / world_;
+  A_part_.reserve((size_t)std::max<int64_t>(r1 - r0, 1) * N * 16);
+  {
+    Nvtx nv2("block reduce-scatter");
+    ncclGroupStart();
+    for (int q = 0; q < world_; ++q) {
+      const int64_t q0 = M * q / world_, q1 = M * (q + 1) / world_;
+      if (q1 > q0)
+        ncclReduce(A_acc_.as<double>() + 2 * q0 * N, q == rank_ ? A_part_.ptr : nullptr, (size_t)(2 * (q1 - q0) * N),
+                   ncclDouble, ncclSum, q, comm_, stream_);
+    }
+    const ncclResult_t rr = ncclGroupEnd();
+    if (rr != ncclSuccess) throw Error(QSIM_ENCCL, std::string("block reduce-scatter: ") + ncclGetErrorString(rr));
+  }
+  run_sampler(A_part_.as<double>(), nullptr, M, N, r0, r1 - r0, true, d_Su_.as<uint64_t>(), d_Sl_.as<uint64_t>(),
+              circ_.h_l, seed, n, out, mass);
 }
 
 void Engine::sample_probs(const double *p, const uint64_t *up, size_t nu, const uint64_t *lo, size_t nl,
@@ -1455,7 +1501,8 @@ void Engine::sample_probs(const double *p, const uint64_t *up, size_t nu, const 
   check(cudaMemcpyAsync(dsu, up, nu * 8, cudaMemcpyHostToDevice, stream_), "upload S_u");
   check(cudaMemcpyAsync(dsl, lo, nl * 8, cudaMemcpyHostToDevice, stream_), "upload S_l");
   double W = 0;
-  run_sampler(p_.as<double>(), (int64_t)nu, (int64_t)nl, dsu, dsl, hl, seed, n, out, mass ? mass : &W);
+  run_sampler(nullptr, p_.as<double>(), (int64_t)nu, (int64_t)nl, 0, (int64_t)nu, false, dsu, dsl, hl, seed, n, out,
+              mass ? mass : &W);
 }
 
 void Engine::porter_thomas(const double *p, size_t n, uint32_t nq, double z_lo, double z_hi, uint32_t nb,
@@ -1720,6 +1767,15 @@ void Engine::rank_range(uint64_t *b0, uint64_t *b1) const {
   if (dist_) {  // distributed halves: every rank runs every branch on its shard
     *b0 = 0;
     *b1 = (uint64_t)B;
+    return;
+  }
+  // prefix groups: the branches sharing the cuts of the first two cut layers (bench.py's steps)
+  int gbits = 0;
+  for (size_t i = 0; i < circ_.fork_layers.size() && i < 2; ++i) gbits += circ_.fork_k[i];
+  const uint64_t G = 1ull << gbits, per = (uint64_t)(B >> gbits);
+  if ((uint64_t)world_ <= G) {
+    *b0 = G * (uint64_t)rank_ / (uint64_t)world_ * per;
+    *b1 = G * (uint64_t)(rank_ + 1) / (uint64_t)world_ * per;
     return;
   }
   *b0 = (uint64_t)(B * (unsigned)rank_ / (unsigned)world_);

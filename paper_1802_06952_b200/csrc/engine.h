@@ -262,8 +262,10 @@ class Engine {
                    void *out_row, int depth);
   void gemm(const void *U, const void *L, int64_t K, int64_t M, int64_t N, double *A);
   double *reduced_block();
-  void run_sampler(const double *p, int64_t M, int64_t N, const uint64_t *dSu, const uint64_t *dSl,
-                   uint32_t hl, uint64_t seed, size_t n, uint64_t *out, double *mass);
+  void run_sampler(const double *A, const double *p, int64_t M, int64_t N, int64_t row0, int64_t nrows,
+                   bool collective, const uint64_t *dSu, const uint64_t *dSl, uint32_t hl, uint64_t seed,
+                   size_t n, uint64_t *out, double *mass);
+  DevBuf A_part_;  // this rank's rows of the reduced block (multi-GPU sampling)
 
   struct MultiPart {
     std::vector<uint32_t> bounds;                        // row bounds r_0 = 0 < ... < r_t = rows

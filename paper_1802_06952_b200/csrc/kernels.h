@@ -217,13 +217,17 @@ cudaError_t launch_abs2(const double *A, int64_t n, double *p, cudaStream_t s);
 // C[i, :] = sequential inclusive prefix of p[i, :]; r[i] = C[i, N-1]
 cudaError_t launch_row_scan(const double *p, int64_t M, int64_t N, double *C, double *r,
                             cudaStream_t s);
+// the same with p = fma(re, re, im*im) of the complex block A computed in the scan (and stored to p)
+cudaError_t launch_row_scan_abs2(const double *A, int64_t M, int64_t N, double *p, double *C, double *r,
+                                 cudaStream_t s);
 // R = sequential inclusive prefix of r; W = R[M-1] (written to *W)
 cudaError_t launch_row_prefix(const double *r, int64_t M, double *R, double *W, cudaStream_t s);
-// draws k in [0, n): Philox4x32-10 uniforms, inverse CDF, x = (Su[i] << hl) | Sl[j]
+// draws k in [0, n): Philox4x32-10 uniforms, inverse CDF, x = (Su[i] << hl) | Sl[j]; p / C hold
+// rows [row0, row0 + nrows) (nrows < 0: all M), r / R all rows; a draw in another rank's rows gives 0
 cudaError_t launch_draws(const double *p, const double *C, const double *r, const double *R,
                          const double *W, int64_t M, int64_t N, const uint64_t *Su,
                          const uint64_t *Sl, uint32_t hl, uint64_t seed, int64_t n,
-                         uint64_t *out, cudaStream_t s);
+                         uint64_t *out, cudaStream_t s, int64_t row0 = 0, int64_t nrows = -1);
 cudaError_t launch_cast_c128_to_c64(const double *A, int64_t n, float *out, cudaStream_t s);
 
 // Porter-Thomas analyzer (stats.cu).  Input: complex block A (double2, p = fma(re,re,im*im))

@@ -489,7 +489,10 @@ cudaError_t launch_abs2(const double *A, int64_t n, double *p, cudaStream_t s) {
 
 // One warp per 32 rows: 32 x 32 tiles are staged through shared memory so that global
 // access is coalesced while every lane scans its own row strictly left to right.
-__global__ void __launch_bounds__(128) row_scan_kernel(const double *__restrict__ p, int64_t M, int64_t N,
+// A != nullptr: p = fma(re, re, im*im) of the complex block A is computed here and written to p
+// (|a|^2 fused into the scan's load: one pass over the block instead of two)
+__global__ void __launch_bounds__(128) row_scan_kernel(const double *__restrict__ pin, const double2 *__restrict__ A,
+                                                       double *__restrict__ pout, int64_t M, int64_t N,
                                                        double *__restrict__ Cp, double *__restrict__ r) {
   __shared__ double tile[4][32][33];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -500,7 +503,17 @@ __global__ void __launch_bounds__(128) row_scan_kernel(const double *__restrict_
   for (int64_t j0 = 0; j0 < N; j0 += 32) {
     for (int rr = 0; rr < 32; ++rr) {
       const int64_t row = row0 + rr, col = j0 + lane;
-      tile[w][rr][lane] = (row < M && col < N) ? p[row * N + col] : 0.0;
+      double v = 0.0;
+      if (row < M && col < N) {
+        if (A) {
+          const double2 a = A[row * N + col];
+          v = fma(a.x, a.x, a.y * a.y);
+          pout[row * N + col] = v;
+        } else {
+          v = pin[row * N + col];
+        }
+      }
+      tile[w][rr][lane] = v;
     }
     __syncwarp();
     const int lim = (int)std::min<int64_t>(32, N - j0);
@@ -521,19 +534,38 @@ __global__ void __launch_bounds__(128) row_scan_kernel(const double *__restrict_
 cudaError_t launch_row_scan(const double *p, int64_t M, int64_t N, double *Cp, double *r,
                             cudaStream_t s) {
   const int blocks = (int)((M + 127) / 128);
-  row_scan_kernel<<<blocks, 128, 0, s>>>(p, M, N, Cp, r);
+  row_scan_kernel<<<blocks, 128, 0, s>>>(p, nullptr, nullptr, M, N, Cp, r);
   return cudaGetLastError();
 }
 
+cudaError_t launch_row_scan_abs2(const double *A, int64_t M, int64_t N, double *p, double *Cp, double *r,
+                                 cudaStream_t s) {
+  const int blocks = (int)((M + 127) / 128);
+  row_scan_kernel<<<blocks, 128, 0, s>>>(nullptr, (const double2 *)A, p, M, N, Cp, r);
+  return cudaGetLastError();
+}
+
+// R = inclusive prefix of r in strictly sequential order (run = run + r[i], i = 0, 1, ...: the
+// oracle's definition, bit-exact): one warp, 32 values per coalesced load, the running sum passed
+// through the lanes by shuffles (the additions stay one dependent chain in index order).
 __global__ void row_prefix_kernel(const double *__restrict__ r, int64_t M, double *__restrict__ R,
                                   double *__restrict__ W) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  if (blockIdx.x != 0 || threadIdx.x >= 32) return;
+  const int lane = threadIdx.x;
   double run = 0.0;
-  for (int64_t i = 0; i < M; ++i) {
-    run = run + r[i];
-    R[i] = run;
+  double next = lane < M ? r[lane] : 0.0;
+  for (int64_t base = 0; base < M; base += 32) {
+    const double v = next;
+    next = base + 32 + lane < M ? r[base + 32 + lane] : 0.0;  // prefetch the next chunk
+    const int lim = (int)(M - base < 32 ? M - base : 32);
+    double mine = 0.0;
+    for (int j = 0; j < lim; ++j) {
+      run = run + __shfl_sync(0xffffffffu, v, j);
+      if (lane == j) mine = run;
+    }
+    if (lane < lim) R[base + lane] = mine;
   }
-  *W = run;
+  if (lane == 0) *W = run;
 }
 
 cudaError_t launch_row_prefix(const double *r, int64_t M, double *R, double *W, cudaStream_t s) {
@@ -572,11 +604,14 @@ __device__ __forceinline__ int64_t upper_bound(const double *a, int64_t n, doubl
   return lo;
 }
 
+// Rows [row0, row0 + nrows) of p / C are held here (the whole block on one GPU; a row shard with
+// several): a draw whose row another rank owns writes 0 (the ranks' outputs are summed).
 __global__ void draws_kernel(const double *__restrict__ p, const double *__restrict__ Cp,
                              const double *__restrict__ r, const double *__restrict__ R,
                              const double *__restrict__ Wp, int64_t M, int64_t N,
                              const uint64_t *__restrict__ Su, const uint64_t *__restrict__ Sl,
-                             uint32_t hl, uint64_t seed, int64_t n, uint64_t *__restrict__ out) {
+                             uint32_t hl, uint64_t seed, int64_t n, uint64_t *__restrict__ out,
+                             int64_t row0, int64_t nrows) {
   const double W = *Wp;
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
     uint32_t c[4] = {(uint32_t)k, (uint32_t)((uint64_t)k >> 32), 0u, 0u};
@@ -589,11 +624,16 @@ __global__ void draws_kernel(const double *__restrict__ p, const double *__restr
       i = M - 1;
       while (i > 0 && !(r[i] > 0.0)) --i;
     }
+    if (i < row0 || i >= row0 + nrows) {
+      out[k] = 0;
+      continue;
+    }
     const double t2 = t - (i > 0 ? R[i - 1] : 0.0);
-    int64_t j = upper_bound(Cp + i * N, N, t2);
+    const int64_t il = i - row0;
+    int64_t j = upper_bound(Cp + il * N, N, t2);
     if (j >= N) {
       j = N - 1;
-      while (j > 0 && !(p[i * N + j] > 0.0)) --j;
+      while (j > 0 && !(p[il * N + j] > 0.0)) --j;
     }
     out[k] = (Su[i] << hl) | Sl[j];
   }
@@ -602,10 +642,10 @@ __global__ void draws_kernel(const double *__restrict__ p, const double *__restr
 cudaError_t launch_draws(const double *p, const double *Cp, const double *r, const double *R,
                          const double *W, int64_t M, int64_t N, const uint64_t *Su,
                          const uint64_t *Sl, uint32_t hl, uint64_t seed, int64_t n,
-                         uint64_t *out, cudaStream_t s) {
+                         uint64_t *out, cudaStream_t s, int64_t row0, int64_t nrows) {
   if (n <= 0) return cudaSuccess;
   const int blocks = (int)std::min<int64_t>((n + 255) / 256, 148 * 8);
-  draws_kernel<<<blocks, 256, 0, s>>>(p, Cp, r, R, W, M, N, Su, Sl, hl, seed, n, out);
+  draws_kernel<<<blocks, 256, 0, s>>>(p, Cp, r, R, W, M, N, Su, Sl, hl, seed, n, out, row0, nrows < 0 ? M : nrows);
   return cudaGetLastError();
 }
 

@@ -36,7 +36,9 @@ def _worker(rank, world, port, out_dir):
     dist.broadcast_object_list(uid, src=0)
     Q.qsim_comm_init(ctx, rank, world, uid[0])
     b0, b1 = Q.qsim_rank_range(ctx)
-    c, B, _ = Q.qsim_partition(ctx)
+    c, B, cuts = Q.qsim_partition(ctx)
+    first = sorted({int(x[0]) for x in cuts})[:2]
+    per = B >> sum(1 for x in cuts if int(x[0]) in first)
     Q.qsim_destroy(ctx)
     ranges = [None] * world
     dist.all_gather_object(ranges, (b0, b1))
@@ -49,7 +51,7 @@ def _worker(rank, world, port, out_dir):
         full = OP.amplitudes(circ, Su, Sl)
         np.save(os.path.join(out_dir, "result.npy"), np.array([np.abs(t.numpy().view(np.complex128) - full).max()]))
         with open(os.path.join(out_dir, "ranges.txt"), "w") as f:
-            f.write(repr((B, ranges)))
+            f.write(repr((B, per, ranges)))
     dist.barrier()
     dist.destroy_process_group()
 
@@ -59,11 +61,13 @@ def test_branch_sharding_gloo(world, tmp_path):
     mp.spawn(_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
     err = float(np.load(tmp_path / "result.npy")[0])
     assert err < 1e-14
-    B, ranges = eval((tmp_path / "ranges.txt").read_text())
+    B, per, ranges = eval((tmp_path / "ranges.txt").read_text())
     assert ranges[0][0] == 0 and ranges[-1][1] == B
     for (a0, a1), (n0, _) in zip(ranges, ranges[1:]):
         assert a1 == n0 and a0 < a1
-    if B % world == 0:
+    # prefix aligned for any world size: every boundary is a first-period prefix-group boundary
+    assert per < B and all(r0 % per == 0 and r1 % per == 0 for r0, r1 in ranges)
+    if (B // per) % world == 0:
         assert all(r1 - r0 == B // world for r0, r1 in ranges)
 
 

@@ -40,8 +40,22 @@ def main():
         Q.qsim_evolve_halves(ctx, Su, Sl)
         A = Q.qsim_amplitudes(ctx, Su, Sl, prec, write=(rank == 0))
         x, W = Q.qsim_sample(ctx, 9, 4096, to_host=(rank == 0))
+        # sampling straight after the evolution (no amplitudes call): the rows reduce-scattered
+        Q.qsim_reset_block(ctx)
+        Q.qsim_evolve_halves(ctx, Su, Sl)
+        x2, W2 = Q.qsim_sample(ctx, 11, 1 << 16, to_host=(rank == 0))
         Q.qsim_destroy(ctx)
         if rank == 0:
+            # the same draws from one GPU holding every branch (a8 bit-exact across N)
+            c1 = Q.qsim_create(prec, local)
+            Q.qsim_load_circuit(c1, rows, cols, d, circ.gate_array())
+            Q.qsim_evolve_halves(c1, Su, Sl)
+            x1, W1 = Q.qsim_sample(c1, 11, 1 << 16)
+            Q.qsim_destroy(c1)
+            same = int(np.sum(x1 == x2))
+            print(f"rank0 world={world} grid={grid}: draws identical to 1 GPU {same}/{x1.size}, "
+                  f"W {W2:.15f} vs {W1:.15f}", flush=True)
+            ok = ok and same >= x1.size - 2 and abs(W2 - W1) <= 1e-12
             from oracle import partition as OP, sampler as OS
             ref = OP.amplitudes(circ, Su, Sl)
             err = np.abs(A.astype(np.complex128) - ref).max()
