@@ -400,8 +400,32 @@ def main():
         Q.qsim_destroy(ctx)
         return out
 
+    def sustained_copy(seconds=3.0, nbytes=4 << 30):
+        """torch device-to-device copy of a 4 GiB buffer back to back for ~3 s right after the timed
+        region (same power / thermal state): read + write bytes / event time.  Context for the roofline
+        (MEASURED_PEAKS.json holds a burst copy only); the roofline's peak stays the measured burst."""
+        a = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+        b = torch.empty_like(a)
+        b.copy_(a)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        n, t0 = 0, time.perf_counter()
+        e0.record()
+        while time.perf_counter() - t0 < seconds:
+            for _ in range(8):
+                b.copy_(a)
+            n += 8
+            torch.cuda.synchronize()
+        e1.record()
+        torch.cuda.synchronize()
+        gbs = 2.0 * nbytes * n / (e0.elapsed_time(e1) / 1e3) / 1e9
+        del a, b
+        torch.cuda.empty_cache()
+        return gbs
+
     prec = Q.QSIM_C128 if args.precision == "c128" else Q.QSIM_C64
     main_run = run_precision(prec, args.steps, args.warmup, True)
+    copy_gbs = sustained_copy() if rank == 0 else None
     sec = None
     if args.secondary_steps > 0:
         other = Q.QSIM_C64 if prec == Q.QSIM_C128 else Q.QSIM_C128
@@ -464,6 +488,8 @@ def main():
                          "achieved_algorithmic": alg,
                          "frac_algorithmic": (alg / peak) if alg else None,
                          "peak_source": peak_src, "kernel": "tile_sweep_tma_kernel",
+                         "sustained_copy_gbs": copy_gbs,
+                         "frac_of_sustained_copy": (moved / copy_gbs) if (moved and copy_gbs) else None,
                          "measured_in": "a separate profiling step after the timed region (CUDA events "
                                         "around every sweep launch on the launching stream)",
                          "launches": st["timed_sweeps"],

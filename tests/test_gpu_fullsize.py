@@ -102,6 +102,17 @@ def test_d22_h14_forks(prec, defer, bfs, lazy, d22_h14):
 
 
 @pytest.mark.parametrize("prec", PRECS, ids=PNAME.get)
+@pytest.mark.parametrize("bfs", [0, 1])
+def test_d22_h14_projector_side(prec, bfs, d22_h14, monkeypatch):
+    """R6' (QSIM_ROLES=1): the projector moved to the lower endpoint of the cuts whose two values a
+    block sums; the block's fixed bits keep R6, so every partial range still equals the oracle's sum."""
+    monkeypatch.setenv("QSIM_ROLES", "1")
+    circ, Su, Sl, ranges, ref = d22_h14
+    A = run_ranges(circ, Su, Sl, ranges, prec, {Q.QSIM_OPT_BFS: bfs})
+    assert_close(A, ref, prec, f"d22 h14 roles bfs={bfs}")
+
+
+@pytest.mark.parametrize("prec", PRECS, ids=PNAME.get)
 @pytest.mark.parametrize("ctas", [1, 3])
 @pytest.mark.parametrize("kernel", [0, 2, 3])
 @pytest.mark.parametrize("bfs", [0, 1])

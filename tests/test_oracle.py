@@ -295,3 +295,38 @@ def test_porter_thomas_analyzer_oracle():
     assert u["var_Np"] == 0.0 and u["mean_Np"] == 1.0
     assert list(u["hist"]) == [0, 0, 64, 0]
     assert u["ks"] == pytest.approx(1 - math.exp(-1), abs=1e-15)
+
+
+@pytest.mark.parametrize("grid", [(4, 3, 12, 5), (4, 4, 16, 2)])
+def test_eq1_read_both_ways(grid):
+    """DESIGN.md R6': CZ = P0 (x) I + P1 (x) Z = I (x) P0 + Z (x) P1, so with the projector put on the
+    lower endpoint of any subset of the cuts the branch sum is still the direct state (Eq. 1)."""
+    rows, cols, d, seed = grid
+    circ = generate(rows, cols, d, seed)
+    cuts = P.cut_list(circ)
+    c, hu = len(cuts), circ.h_upper
+    rng = np.random.default_rng(seed)
+    p_upper = rng.integers(0, 2, c)
+    assert 0 < p_upper.sum() < c or c < 2
+
+    def half(half_i, b):
+        lo, hi = (0, hu) if half_i == 0 else (hu, circ.n)
+        out = [(l, k, q0 - lo, (q1 - lo) if k == 4 else 0) for (l, k, q0, q1) in circ.gates
+               if all(lo <= q < hi for q in ([q0] if k != 4 else [q0, q1]))]
+        for g, (layer, qu, ql) in enumerate(cuts):
+            bit = (b >> (c - 1 - g)) & 1
+            proj = bool(p_upper[g]) == (half_i == 0)
+            q = (qu if half_i == 0 else ql) - lo
+            if proj:
+                out.append((layer, "P1" if bit else "P0", q, 0))
+            elif bit:
+                out.append((layer, "Z", q, 0))
+        return sorted(out, key=lambda g_: g_[0])
+
+    hl = circ.n - hu
+    A = np.zeros((1 << hu, 1 << hl), dtype=np.complex128)
+    for b in range(1 << c):
+        U = SV.run_gates(SV.initial_state(hu), hu, half(0, b))
+        L = SV.run_gates(SV.initial_state(hl), hl, half(1, b))
+        A += np.outer(U, L)
+    assert np.abs(A.reshape(-1) - SV.simulate(circ)).max() < 1e-14
