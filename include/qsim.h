@@ -91,7 +91,8 @@ typedef enum {
                                 (comparison); 2 / 3: the TMA sweep with 2 / 3 shared-memory stages      */
   QSIM_OPT_LAZY_LAST = 5     /* lazy tail of each leaf, evaluated only at the sampled indices during the
                                 gather instead of full 2^h passes: 0 off, 1 the last sweep, 2 (default)
-                                the last one or two by a cost model, 3 always two when possible      */,
+                                the last one to three by a cost model (cones of cones), 3 / 4 always
+                                two / three when possible (tests)                                     */,
   QSIM_OPT_FUSE_LAYERS = 6,  /* reserved: multi-layer tiles were removed (compute-bound, never faster than
                                 one pass per layer); only 0 is accepted             */
   QSIM_OPT_DISTRIBUTE = 7    /* 1: distributed half (§2.3.3): every half state
@@ -136,7 +137,9 @@ qsim_status qsim_set_stream(qsim_ctx *ctx, void *cuda_stream);
  *  gates[n_gates]: host array, any order; each qubit at most once per layer;
  *    CZ only between grid neighbours; single-qubit gates: SX, SY, T.
  *  cut_row: upper half = rows [0, cut_row); 0 = rows/2.  Both halves must have
- *    1 <= h <= 32 qubits.
+ *    1 <= h <= 36 qubits; a half of more than 32 qubits is evolved only as a distributed half
+ *    (QSIM_OPT_DISTRIBUTE over >= 2^(h-32) ranks: at most 32 qubits per shard), else the
+ *    evolve calls return EINVAL.
  *  cut_layers[n_cut_layers]: optional cross-check of the layers holding cut CZs
  *    (e.g. {7, 8, 15, 16}); NULL = derive.  A mismatch is EINVAL.
  * Replaces any previous circuit (and drops blocks / accumulated amplitudes). */

@@ -53,17 +53,20 @@ void Engine::check(cudaError_t e, const char *what) {
 }
 
 static DiagDev to_dev(const Diag &d, bool force_active = false) {
+  // the device form holds bits 0..31 (a distributed half's diagonals are restricted to the shard
+  // first, Diag::restrict_low); anything above is a planning error, not a result
+  if (!d.allzero && !d.below(32)) throw Error(QSIM_EINVAL, "internal: a diagonal above bit 31 reached the device");
   DiagDev o;
   std::memset(&o, 0, sizeof(o));
-  o.t1 = d.t1;
-  o.t2 = d.t2;
-  o.zm = d.zm;
-  o.pm = d.pm;
-  o.pv = d.pv & d.pm;
+  o.t1 = (uint32_t)d.t1;
+  o.t2 = (uint32_t)d.t2;
+  o.zm = (uint32_t)d.zm;
+  o.pm = (uint32_t)d.pm;
+  o.pv = (uint32_t)(d.pv & d.pm);
   for (int k = 1; k < 32; ++k)
     if (d.cz[k]) {
       o.czd[o.ncz] = (uint8_t)k;
-      o.czm[o.ncz++] = d.cz[k];
+      o.czm[o.ncz++] = (uint32_t)d.cz[k];
     }
   o.ph0 = d.ph0 & 7;
   o.active = (force_active || !d.identity()) ? 1 : 0;
@@ -91,7 +94,7 @@ static DiagSplit make_split(const Diag &d, const std::vector<int> &regpos) {
       if ((idx >> j) & 1) R |= 1u << regpos[j];
     int ph = dd.ph0 + __builtin_popcount(R & dd.t1) + 2 * __builtin_popcount(R & dd.t2) +
              4 * __builtin_popcount(R & dd.zm);
-    for (int k = 1; k < 32; ++k) ph += 4 * __builtin_popcount(R & (R >> k) & d.cz[k]);
+    for (int k = 1; k < 32; ++k) ph += 4 * __builtin_popcount(R & (R >> k) & (uint32_t)d.cz[k]);
     const bool okR = (R & dd.pm & Rbits) == (dd.pv & dd.pm & Rbits);
     s.P[idx] = (uint8_t)((ph & 7) << 3);
     if (!okR) s.notok |= 1u << idx;
@@ -204,7 +207,7 @@ void Engine::set_option(int key, int64_t value) {
       mem_budget_ = value;
       return;
     case QSIM_OPT_LAZY_LAST:
-      if (value < 0 || value > 3) throw Error(QSIM_EINVAL, "QSIM_OPT_LAZY_LAST must be 0, 1, 2 or 3");
+      if (value < 0 || value > 4) throw Error(QSIM_EINVAL, "QSIM_OPT_LAZY_LAST must be 0 .. 4");
       lazy_depth_ = (int)value;
       return;
     case QSIM_OPT_FUSE_LAYERS:  // multi-layer tiles were compute-bound, never faster: removed
@@ -275,7 +278,7 @@ void Engine::compile_all() {
     if (dist_) {
       plan_distributed(half_[h]);
       compile_plans(half_[h]);
-    } else if (half_[h].tree) {  // relabel qubits to physical bits for long tile runs (choose_perm)
+    } else if (half_[h].tree && half_[h].prog.h <= 32) {  // relabel qubits to physical bits (choose_perm)
       std::vector<double> lw;
       if (deferred_) lw = deferred_layer_weights(h, perm_ns_[h]);
       const std::vector<int> perm = choose_perm(half_[h], perm_ns_[h], deferred_ ? &lw : nullptr);
@@ -346,6 +349,7 @@ void Engine::compile_plans(HalfExec &he) {
   he.glayers.clear();
   he.ft.clear();
   if ((he.tree && !can_tree) || (!he.tree && !can_small)) return;  // reported at evolve time
+  if (hp.hl > 32) return;  // more than 32 local bits: only the shards of a distributed half are planned
   if (!he.tree) return;
   plan_levels(hp, he.plans, false);
 }
@@ -357,7 +361,7 @@ void Engine::plan_levels(const HalfProgram &hp, std::vector<std::vector<std::vec
   plans.resize(hp.levels.size());
   for (size_t l = 0; l <= F; ++l) {
     const Level &lev = hp.levels[l];
-    const size_t nskip = (l == F || all_skips) ? 3 : 1;
+    const size_t nskip = (l == F || all_skips) ? 4 : 1;  // lazy tails of up to 3 sweeps
     uint32_t forkmask = 0;
     for (int b : lev.cut_bits) forkmask |= 1u << b;
     for (size_t skip = 0; skip < nskip; ++skip) {
@@ -764,7 +768,8 @@ std::vector<TilePlan> Engine::legacy_plans(const HalfProgram &hp, const Sweep &s
         tp.use_pre = ci == 0;
         tp.gen = sw.gen && ci == 0;
         tp.pre = sw.pre;
-        const Diag post = ci == nchunks - 1 ? sw.post : Diag();
+        Diag post = ci == nchunks - 1 ? sw.post : Diag();
+        if (dist_) post = post.restrict_low(hp.hl, (uint64_t)rank_ << hp.hl);  // this rank's shard
         tp.p.post = to_dev(post);
         tp.p.post_s = make_split(post, reg_positions(tp.p, tp.npass - 1, c128_));
         int m = 0;
@@ -937,10 +942,10 @@ void Engine::launch_plan(const TilePlan &tp, const Diag &fork, bool first, const
   Diag fk = fork;
   if (tp.use_pre && absorb_ && !tp.gen && sweep_kernel_ != 1 && !dist_ && !fork.allzero) {
     const int L = tile_low_bits(c128_), VB = c128_ ? 0 : 1;
-    const uint32_t cand = (fork.pm ^ fork.zm) & (fork.pm | fork.zm) & tp.targets & ~(fork.t1 | fork.t2);
+    const uint32_t cand = (uint32_t)((fork.pm ^ fork.zm) & (fork.pm | fork.zm) & tp.targets & ~(fork.t1 | fork.t2));
     for (int q = 0; q < 32; ++q) {
       if (!((cand >> q) & 1u)) continue;
-      const uint32_t m = 1u << q;
+      const uint64_t m = 1ull << q;
       const int f = (fork.pm & m) ? ((fork.pv & m) ? 3 : 2) : 1;
       uint8_t *k = nullptr;
       if (q >= L) {
@@ -962,13 +967,14 @@ void Engine::launch_plan(const TilePlan &tp, const Diag &fork, bool first, const
       } else {
         fk.pm &= ~m;
         fk.pv &= ~m;
-        absorbed_pm |= m;
-        if (f == 3) absorbed_pv |= m;
+        absorbed_pm |= (uint32_t)m;
+        if (f == 3) absorbed_pv |= (uint32_t)m;
       }
     }
   }
   if (tp.use_pre) {
     pre = Diag::merge(fk, tp.pre);
+    if (dist_) pre = pre.restrict_low(hp.hl, (uint64_t)rank_ << hp.hl);  // this rank's shard
     if (tp.gen)
       pre_mode = 2;
     else if (!pre.identity())
@@ -989,7 +995,7 @@ void Engine::launch_plan(const TilePlan &tp, const Diag &fork, bool first, const
     p.ld_pv = (pre_mode == 1 ? p.pre.pv : 0u) | absorbed_pv;
     p.njobs = 1;
     if (dist_) {
-      p.gbase = (uint32_t)rank_ << hp.hl;
+      p.gbase = 0;  // the diagonals were restricted to this rank's shard on the host
       p.rank = (uint32_t)rank_;
       if (!tp.swaps.empty()) {  // fused local/global swap: destination buffers of the ranks
         if (out_buf < 0 || tp.swaps.size() > 2) throw Error(QSIM_EINVAL, "distributed swap plan");
@@ -1009,8 +1015,8 @@ void Engine::launch_plan(const TilePlan &tp, const Diag &fork, bool first, const
       // tiles outside the fork's projector (on qubits no gate of the level has touched) are zero
       uint32_t outer = (h >= 32 ? ~0u : ((1u << h) - 1u)) & ~((1u << tile_low_bits(c128_)) - 1u);
       for (int j = 0; j < kHiBits; ++j) outer &= ~(1u << p.hb[j]);
-      p.skip_pm = child_fork->pm & tp.zfix & outer;
-      p.skip_pv = child_fork->pv & p.skip_pm;
+      p.skip_pm = (uint32_t)child_fork->pm & tp.zfix & outer;
+      p.skip_pv = (uint32_t)child_fork->pv & p.skip_pm;
     }
     skip_pm_last_ = p.skip_pm;
     const uint64_t tiles = 1ull << p.log2_ntiles;
@@ -1050,28 +1056,9 @@ const void *Engine::run_level(int half, int level, uint64_t child, const void *s
   const Diag fork = he.prog.fork_diag(level, child);
   const auto &launches = he.plans[level][std::min<size_t>((size_t)skip, he.plans[level].size() - 1)];
   const size_t n = launches.size();
-  if (!dist_) {
-    for (size_t i = 0; i < n; ++i)
-      launch_plan(launches[i], i == 0 ? fork : Diag(), i == 0, i == 0 ? src : dst, dst, he.prog, -1, &fork);
-    return n ? dst : src;
-  }
-  // distributed half: level buffers 2l, 2l+1 (dst is buffer 2l).  A sweep that swaps local and
-  // global qubits stores into peers' buffers, so it runs out of place into the level's other
-  // buffer, between two barriers (no rank may still read what a peer overwrites).
-  int cur = 2 * level;
-  const void *in = src;
-  for (size_t i = 0; i < n; ++i) {
-    const TilePlan &tp = launches[i];
-    int out = (i == 0) ? 2 * level : cur;
-    if (!tp.swaps.empty() && i > 0) out = cur ^ 1;
-    if (!tp.swaps.empty()) dist_barrier();
-    launch_plan(tp, i == 0 ? fork : Diag(), i == 0, i == 0 ? in : states_[cur]->ptr, states_[out]->ptr, he.prog,
-                out);
-    if (!tp.swaps.empty()) dist_barrier();
-    cur = out;
-  }
-  (void)dst;
-  return n ? states_[cur]->ptr : src;
+  for (size_t i = 0; i < n; ++i)
+    launch_plan(launches[i], i == 0 ? fork : Diag(), i == 0, i == 0 ? src : dst, dst, he.prog, -1, &fork);
+  return n ? dst : src;
 }
 
 static LazyLayer lazy_layer(const Sweep &sw, const Diag &pre) {
@@ -1084,7 +1071,7 @@ static LazyLayer lazy_layer(const Sweep &sw, const Diag &pre) {
     (sw.gates[t].kind == 1 ? ll.sxmask : ll.symask) |= 1u << sw.gates[t].bit;
   }
   ll.pre = to_dev(pre);
-  ll.post = to_dev(sw.post, true);
+  if (sw.post.below(32)) ll.post = to_dev(sw.post, true);  // else the caller restricts it (distributed)
   ll.lmask = ~0ull;
   ll.gsel = 0;
   return ll;
@@ -1126,16 +1113,20 @@ void Engine::gather_leaf(int half, uint64_t child_last, const void *psi, const u
     auto pre_of = [&](size_t s) {
       return s == 0 ? Diag::merge(he.prog.fork_diag(F, child_last), lev.sweeps[0].pre) : lev.sweeps[s].pre;
     };
-    LazyLayer lld = lazy_layer(lev.sweeps[n - 1], pre_of(n - 1));
+    const uint64_t gsel = (uint64_t)rank_ << he.prog.hl;
+    auto shard = [&](const Diag &d) { return dist_ ? d.restrict_low(he.prog.hl, gsel) : d; };
+    LazyLayer lld = lazy_layer(lev.sweeps[n - 1], shard(pre_of(n - 1)));
     if (dist_) {
+      lld.post = to_dev(shard(lev.sweeps[n - 1].post), true);
       lld.lmask = (1ull << he.prog.hl) - 1ull;
-      lld.gsel = (uint64_t)rank_ << he.prog.hl;
+      lld.gsel = gsel;
     }
     if (depth == 1) {
       check(launch_gather_layer(psi, dS, nS, out_row, lld, c128_, stream_), "gather_layer launch");
       st_.kernel_launches++;
     } else {
-      LazyLayer ll1 = lazy_layer(lev.sweeps[n - 2], pre_of(n - 2));
+      LazyLayer ll1 = lazy_layer(lev.sweeps[n - 2], shard(pre_of(n - 2)));
+      if (dist_) ll1.post = to_dev(shard(lev.sweeps[n - 2].post), true);
       ll1.lmask = lld.lmask;
       ll1.gsel = lld.gsel;
       const int64_t ncone = nS << lld.k;
@@ -1155,6 +1146,7 @@ void Engine::gather_leaf(int half, uint64_t child_last, const void *psi, const u
   if (F >= 1 && lev.sweeps.empty()) pend = he.prog.fork_diag(F, child_last);
   const uint64_t lmask = dist_ ? (1ull << he.prog.hl) - 1ull : ~0ull;
   const uint64_t gsel = dist_ ? (uint64_t)rank_ << he.prog.hl : 0ull;
+  if (dist_) pend = pend.restrict_low(he.prog.hl, gsel);
   check(launch_gather(psi, dS, nS, out_row, to_dev(pend), c128_, stream_, lmask, gsel), "gather launch");
   st_.kernel_launches++;
 }
@@ -1180,6 +1172,71 @@ void Engine::ensure_states(int half, int nbuf) {
   (void)half;
   while ((int)states_.size() < nbuf) states_.push_back(new DevBuf());
   for (int i = 0; i < nbuf; ++i) states_[i]->reserve(state_bytes_);
+}
+
+// Distributed half: the shards run the paper's branch tree depth-first.  A level
+// state is kept (its own buffer pair) only when more than one of its children lies in [b0, b1);
+// other levels continue in the pair of their parent, in place, so a single branch needs one pair.
+// A sweep that swaps local and global qubits stores into the peers' copy of the pair's other
+// buffer between two stream-ordered barriers (run_level_dist).
+void Engine::evolve_half_dist(int half, uint64_t b0, uint64_t b1, void *slice, const uint64_t *dS, int64_t nS) {
+  HalfExec &he = half_[half];
+  const HalfProgram &hp = he.prog;
+  const int c = hp.ncuts, F = (int)hp.levels.size() - 1;
+  std::vector<int> sbits(F + 1, 0);
+  for (int l = 1; l <= F; ++l) sbits[l] = sbits[l - 1] + hp.levels[l].k;
+  // pair[l]: the buffer pair of level l (a new pair after each kept level)
+  std::vector<int> pair(F + 1, 0);
+  int npair = 1;
+  for (int l = 0; l < F; ++l) {
+    const int sh = c - sbits[l + 1];
+    const bool keep = sbits[l + 1] > sbits[l] && (b0 >> sh) != ((b1 - 1) >> sh);
+    pair[l + 1] = keep ? npair++ : pair[l];
+  }
+  const int hmax = std::max(half_[0].prog.hl, half_[1].prog.hl);
+  dist_buffers(((size_t)1 << hmax) * amp_, 2 * std::max(npair, dist_pairs_));
+  dist_pairs_ = std::max(npair, dist_pairs_);
+  state_bytes_ = ((size_t)1 << hp.hl) * amp_;
+  const int lazy = lazy_depth(half, nS);
+  auto skip = [&](int l) { return l == F ? lazy : 0; };
+  std::function<void(int, uint64_t, int)> node = [&](int l, uint64_t prefix, int idx) {
+    if (l == F) {
+      const uint64_t b = prefix;
+      const uint64_t ch = F >= 1 ? (b & ((1ull << hp.levels[F].k) - 1ull)) : 0;
+      gather_leaf(half, ch, states_[idx]->ptr, dS, nS, (char *)slice + (b - b0) * (uint64_t)nS * amp_, lazy);
+      return;
+    }
+    const int k = hp.levels[l + 1].k;
+    const int shift = c - sbits[l + 1];
+    for (uint64_t ch = 0; ch < (1ull << k); ++ch) {
+      const uint64_t cp = (prefix << k) | ch;
+      const uint64_t lo = cp << shift, hi = (cp + 1) << shift;
+      if (hi <= b0 || lo >= b1) continue;
+      node(l + 1, cp, run_level_dist(half, l + 1, ch, idx, pair[l + 1], skip(l + 1)));
+    }
+  };
+  node(0, 0, run_level_dist(half, 0, 0, -1, 0, skip(0)));
+}
+
+int Engine::run_level_dist(int half, int level, uint64_t child, int src, int pair, int skip) {
+  HalfExec &he = half_[half];
+  const Diag fork = he.prog.fork_diag(level, child);
+  const auto &launches = he.plans[level][std::min<size_t>((size_t)skip, he.plans[level].size() - 1)];
+  int cur = src;
+  for (size_t i = 0; i < launches.size(); ++i) {
+    const TilePlan &tp = launches[i];
+    int out;
+    if (i == 0 && (src < 0 || src / 2 != pair))
+      out = 2 * pair;  // a fresh pair: out of place from the parent
+    else
+      out = tp.swaps.empty() ? cur : (cur ^ 1);  // in place, or the pair's other buffer when swapping
+    if (!tp.swaps.empty()) dist_barrier();
+    launch_plan(tp, i == 0 ? fork : Diag(), i == 0, cur < 0 ? nullptr : states_[cur]->ptr, states_[out]->ptr,
+                he.prog, out);
+    if (!tp.swaps.empty()) dist_barrier();
+    cur = out;
+  }
+  return cur;
 }
 
 void Engine::evolve_half(int half, uint64_t b0, uint64_t b1, void *slice, const uint64_t *dS, int64_t nS) {
@@ -1213,10 +1270,8 @@ void Engine::evolve_half(int half, uint64_t b0, uint64_t b1, void *slice, const 
   const int T = tile_low_bits(c128_) + kHiBits;
   if (hp.hl < T) throw Error(QSIM_EINVAL, "tree mode needs h >= tile bits");
   if (dist_) {
-    // shards of both halves share 2 buffers per level (sized for the larger half)
-    const int hmax = std::max(half_[0].prog.hl, half_[1].prog.hl);
-    const int nlev = (int)std::max(half_[0].prog.levels.size(), half_[1].prog.levels.size());
-    dist_buffers(((size_t)1 << hmax) * amp_, 2 * nlev);
+    evolve_half_dist(half, b0, b1, slice, dS, nS);
+    return;
   }
   state_bytes_ = ((size_t)1 << hp.hl) * amp_;
   size_t free_b = 0, total_b = 0;
@@ -1318,6 +1373,12 @@ void Engine::evolve_range(uint64_t b0, uint64_t b1) {
   for (int h = 0; h < 2; ++h) {
     const HalfExec &he = half_[h];
     const int T = tile_low_bits(c128_) + kHiBits;
+    if (he.prog.hl > 32) {
+      std::ostringstream m;
+      m << "a " << he.prog.h << "-qubit half needs QSIM_OPT_DISTRIBUTE over at least " << (1 << (he.prog.h - 32))
+        << " ranks (at most 32 qubits per shard)";
+      throw Error(QSIM_EINVAL, m.str());
+    }
     if (he.tree && he.prog.h < T) throw Error(QSIM_EINVAL, "tree mode needs h >= 13 (c64) / 12 (c128)");
     if (!he.tree && he.prog.h > small_max_h(c128_)) throw Error(QSIM_EINVAL, "flat mode needs h <= 12");
   }
@@ -2038,24 +2099,46 @@ void Engine::bfs_subtree(int half, int m, const void *state, void *out, const ui
 // places the forks of a block of branches (a dynamic programme over the half's sweeps, bounded by
 // the state buffers that fit in HBM); the executor below runs the resulting tree depth-first.
 
+// Lazy tail of a tree path: its last L sweeps (L <= 3) evaluated at the sampled indices (stage 0 on
+// a cone of nS * 2^{k_1 + .. + k_{L-1}} points, each summing 2^{k_0} scattered reads of the state;
+// later stages from those values).  Cost in bytes: ~64 per scattered read (32-byte sectors shared
+// by neighbouring targets; the C5 launch lists give ~9e10 reads/s), ~16 per compact read, against
+// 2 * 2^h * amp per sweep saved.  QSIM_OPT_LAZY_LAST: 0 off, 1 one sweep, 2 (default) up to three by
+// this model, 3 / 4 two / three whenever possible (tests).
 int Engine::tree_lazy(int half, int64_t nS) const {
   const HalfProgram &hp = half_[half].prog;
   std::vector<const Sweep *> sw;
   for (auto &l : hp.levels)
     for (auto &s : l.sweeps) sw.push_back(&s);
   if (full_leaf_ || lazy_depth_ < 1 || sw.size() < 2) return 0;
-  const Sweep &d = *sw.back();
-  if (d.gen || d.gates.size() > 12) return 0;
-  if (lazy_depth_ < 2 || sw.size() < 3) return 1;
-  const Sweep &d1 = *sw[sw.size() - 2];
-  if (d1.gen) return 1;
-  const int kd = (int)d.gates.size(), kd1 = (int)d1.gates.size();
-  if (kd + kd1 > 20 || ((double)nS * std::ldexp(1.0, kd)) > (double)(1 << 26)) return 1;
-  if (lazy_depth_ == 3) return 2;  // forced (tests)
+  const int S = (int)sw.size();
   const double sweep = 2.0 * std::ldexp(1.0, hp.hl) * (double)amp_;
-  const double lazy1 = 96.0 * (double)nS * std::ldexp(1.0, kd);
-  const double lazy2 = 96.0 * (double)nS * std::ldexp(1.0, kd + kd1) + 2.0 * lazy1;
-  return lazy2 < sweep + lazy1 ? 2 : 1;
+  auto feasible = [&](int L) {
+    if (L + 1 > S) return false;
+    double pts = (double)nS;
+    for (int s = S - 1; s >= S - L; --s) {
+      if (sw[s]->gen || sw[s]->gates.size() > 12) return false;
+      if (s > S - L) pts *= std::ldexp(1.0, (int)sw[s]->gates.size());
+    }
+    return pts <= (double)(1 << 27);
+  };
+  auto cost = [&](int L) {  // bytes of the lazy stages minus the sweeps they save
+    double pts = (double)nS, c = 0.0;
+    for (int s = S - 1; s >= S - L; --s) {
+      const double terms = std::ldexp(1.0, (int)sw[s]->gates.size());
+      c += (s == S - L ? 64.0 : 16.0) * pts * terms;
+      pts *= terms;
+    }
+    return c - L * sweep;
+  };
+  if (!feasible(1)) return 0;
+  if (lazy_depth_ == 1) return 1;
+  if (lazy_depth_ == 3) return feasible(2) ? 2 : 1;
+  if (lazy_depth_ == 4) return feasible(3) ? 3 : feasible(2) ? 2 : 1;
+  int best = 1;
+  for (int L = 2; L <= 3; ++L)
+    if (feasible(L) && cost(L) < cost(best)) best = L;
+  return best;
 }
 
 // Fork placement for the aligned block of 2^m branches whose top c - m cut bits are fixed.
@@ -2267,8 +2350,7 @@ void Engine::evolve_block(int half, uint64_t b0, int m, void *slice, const uint6
   if (he.prog.hl < T) throw Error(QSIM_EINVAL, "tree mode needs h >= tile bits");
   state_bytes_ = ((size_t)1 << he.prog.hl) * amp_;
   // level-synchronous subtrees for small states (launch-bound otherwise): gather forks pinned
-  const bool bfs = bfs_ && sweep_kernel_ != 1 && state_bytes_ <= ((size_t)256 << 20);
-  if (!bfs) {  // their buffers are state memory now
+  if (!(bfs_ && sweep_kernel_ != 1 && state_bytes_ <= ((size_t)256 << 20))) {  // their buffers are state memory now
     bfs_buf_[0].release();
     bfs_buf_[1].release();
   }
@@ -2276,9 +2358,19 @@ void Engine::evolve_block(int half, uint64_t b0, int m, void *slice, const uint6
   check(cudaMemGetInfo(&free_b, &total_b), "cudaMemGetInfo");
   size_t have = bfs_buf_[0].bytes + bfs_buf_[1].bytes;
   for (auto *b : states_) have += b->bytes;
-  const int lz = tree_lazy(half, nS);
+  const bool bfs = bfs_ && sweep_kernel_ != 1 && state_bytes_ <= ((size_t)256 << 20);
+  const int lz = bfs ? std::min(2, tree_lazy(half, nS)) : tree_lazy(half, nS);  // bfs_tree: <= 2 stages
   size_t margin = (size_t)512 << 20;
-  if (lz == 2) margin += (size_t)nS * 256 * (amp_ + 8);  // cone buffers of the lazy tail
+  {  // cone index / value buffers of the lazy tail
+    std::vector<const Sweep *> sw;
+    for (auto &l : he.prog.levels)
+      for (auto &x : l.sweeps) sw.push_back(&x);
+    double pts = (double)nS;
+    for (int s2 = (int)sw.size() - 1; s2 > (int)sw.size() - lz; --s2) {
+      pts *= std::ldexp(1.0, (int)sw[s2]->gates.size());
+      margin += (size_t)(pts * (double)(amp_ + 8));
+    }
+  }
   const size_t avail = free_b + have > margin ? free_b + have - margin : 0;
   const size_t nfit = avail / state_bytes_;
   if (nfit < 1) {
@@ -2530,8 +2622,10 @@ void Engine::run_tree(int half, const TreeVariant &v, int lz, const std::vector<
     if (mat > 0) M = l;
     skip[l] = n - mat;
   }
+  for (int l = 0; l <= F; ++l)
+    if ((size_t)skip[l] >= v.plans[l].size()) throw Error(QSIM_EINVAL, "internal: lazy tail longer than the plans");
   auto run = [&](int l, const Diag &fork, const void *src, void *dst) {
-    const auto &launches = v.plans[l][std::min<size_t>((size_t)skip[l], v.plans[l].size() - 1)];
+    const auto &launches = v.plans[l][(size_t)skip[l]];
     for (size_t i = 0; i < launches.size(); ++i)
       launch_plan(launches[i], i == 0 ? fork : Diag(), i == 0, i == 0 ? src : dst, dst, hp, -1, &fork);
   };
@@ -2602,36 +2696,42 @@ void Engine::gather_tree(const TreeVariant &v, int lz, int M, const std::vector<
     }
     return;
   }
-  if (lz == 1) {
-    const Sweep &sw = *st[0].first;
-    for (const Combo &cb : combos(st[0].second, pl)) {
-      const LazyLayer ll = lazy(sw, Diag::merge(sw.pre, cb.d[0]), Diag::merge(sw.post, cb.d[1]));
-      check(launch_gather_layer(psi, dS, nS, row(bacc | cb.bits), ll, c128_, stream_), "gather_layer launch");
-      st_.kernel_launches++;
-      st_.lazy_gathers++;
-    }
-    return;
-  }
-  const Sweep &s1 = *st[0].first, &s2 = *st[1].first;
-  const LazyLayer shape = lazy_layer(s2, s2.pre);
-  const int64_t ncone = nS << shape.k;
-  cone_idx_.reserve((size_t)ncone * 8);
-  cone_val_.reserve((size_t)ncone * amp_);
-  check(launch_cone_indices(dS, nS, shape, cone_idx_.as<uint64_t>(), stream_), "cone launch");
-  st_.kernel_launches++;
-  for (const Combo &ca : combos(st[0].second, -1)) {
-    const LazyLayer l1 = lazy(s1, Diag::merge(s1.pre, ca.d[0]), s1.post);
-    check(launch_gather_layer(psi, cone_idx_.as<uint64_t>(), ncone, cone_val_.ptr, l1, c128_, stream_),
-          "gather_layer launch");
+  // lz >= 1 stages: index lists deepest first (idx[L-1] = the block; idx[s-1] = the cone of idx[s]
+  // over stage s's targets), values of stage s at idx[s] from psi (s = 0) or from stage s-1's values
+  // (compact); the forks of a stage's level enter its pre diagonal, the trailing level's its post
+  const int L = (int)st.size();
+  std::vector<const uint64_t *> idx(L);
+  std::vector<int64_t> cnt(L);
+  idx[L - 1] = dS;
+  cnt[L - 1] = nS;
+  for (int s2 = L - 1; s2 >= 1; --s2) {
+    const LazyLayer shape = lazy_layer(*st[s2].first, Diag());
+    cnt[s2 - 1] = cnt[s2] << shape.k;
+    lazy_idx_[s2 - 1].reserve((size_t)cnt[s2 - 1] * 8);
+    check(launch_cone_indices(idx[s2], cnt[s2], shape, lazy_idx_[s2 - 1].as<uint64_t>(), stream_), "cone launch");
     st_.kernel_launches++;
-    for (const Combo &cb : combos(st[1].second, pl)) {
-      const LazyLayer l2 = lazy(s2, Diag::merge(s2.pre, cb.d[0]), Diag::merge(s2.post, cb.d[1]));
-      check(launch_gather_layer_compact(cone_val_.ptr, dS, nS, row(bacc | ca.bits | cb.bits), l2, c128_, stream_),
-            "gather_layer_compact launch");
-      st_.kernel_launches++;
-      st_.lazy_gathers++;
-    }
+    idx[s2 - 1] = lazy_idx_[s2 - 1].as<uint64_t>();
   }
+  for (int s2 = 0; s2 + 1 < L; ++s2) lazy_val_[s2].reserve((size_t)cnt[s2] * amp_);
+  std::function<void(int, uint64_t, const void *)> stage = [&](int s2, uint64_t bits, const void *prev) {
+    const Sweep &sw = *st[s2].first;
+    const bool last = s2 == L - 1;
+    for (const Combo &cb : combos(st[s2].second, last ? pl : -1)) {
+      const LazyLayer ll = lazy(sw, Diag::merge(sw.pre, cb.d[0]), last ? Diag::merge(sw.post, cb.d[1]) : sw.post);
+      void *out = last ? (void *)row(bacc | bits | cb.bits) : lazy_val_[s2].ptr;
+      if (s2 == 0)
+        check(launch_gather_layer(psi, idx[0], cnt[0], out, ll, c128_, stream_), "gather_layer launch");
+      else
+        check(launch_gather_layer_compact(prev, idx[s2], cnt[s2], out, ll, c128_, stream_),
+              "gather_layer_compact launch");
+      st_.kernel_launches++;
+      if (last)
+        st_.lazy_gathers++;
+      else
+        stage(s2 + 1, bits | cb.bits, lazy_val_[s2].ptr);
+    }
+  };
+  stage(0, 0, nullptr);
 }
 
 // ---------------------------------------------------------------- multi-part partitions (f4)

@@ -229,6 +229,7 @@ class Engine {
                 int l, const void *state, uint64_t bacc, int m, void *slice, const uint64_t *dS, int64_t nS,
                 size_t avail);
   DevBuf rowmap_;
+  DevBuf lazy_idx_[2], lazy_val_[2];  // cone index lists / stage values of the lazy tail (<= 3 stages)
   bool deferred_ = !(std::getenv("QSIM_DEFER") && std::getenv("QSIM_DEFER")[0] == '0');
   int max_ctas_ = 0;  // QSIM_OPT_MAX_CTAS (tests)
   // deferred forks on a bit the sweep targets are folded into that gate (QSIM_ABSORB=0: off, A/B)
@@ -237,6 +238,11 @@ class Engine {
   bool pskip_ = !(std::getenv("QSIM_PSKIP") && std::getenv("QSIM_PSKIP")[0] == '0');
   uint32_t skip_pm_last_ = 0;  // known-zero tile mask of the last planned launch (stats)
   int grid_ctas() const { return max_ctas_ > 0 ? std::min(max_ctas_, num_sms_) : num_sms_; }
+
+  // distributed halves (f3): depth-first over the shards, buffer pairs only for kept levels
+  void evolve_half_dist(int half, uint64_t b0, uint64_t b1, void *slice, const uint64_t *dS, int64_t nS);
+  int run_level_dist(int half, int level, uint64_t child, int src, int pair, int skip);
+  int dist_pairs_ = 0;
 
   // executor
   void evolve_half(int half, uint64_t b0, uint64_t b1, void *slice, const uint64_t *dS, int64_t nS);

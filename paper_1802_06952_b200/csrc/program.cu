@@ -15,15 +15,15 @@ int Diag::count(int bit) const {
 
 void Diag::set_count(int bit, int c) {
   c &= 7;
-  const uint32_t m = 1u << bit;
-  t1 = (t1 & ~m) | ((c & 1) ? m : 0u);
-  t2 = (t2 & ~m) | ((c & 2) ? m : 0u);
-  zm = (zm & ~m) | ((c & 4) ? m : 0u);
+  const uint64_t m = 1ull << bit;
+  t1 = (t1 & ~m) | ((c & 1) ? m : 0ull);
+  t2 = (t2 & ~m) | ((c & 2) ? m : 0ull);
+  zm = (zm & ~m) | ((c & 4) ? m : 0ull);
 }
 
 void Diag::add_proj(int bit, int value) {
-  const uint32_t m = 1u << bit;
-  const uint32_t v = value ? m : 0u;
+  const uint64_t m = 1ull << bit;
+  const uint64_t v = value ? m : 0ull;
   if ((pm & m) && ((pv & m) != v)) allzero = true;  // P0 P1 = 0
   pm |= m;
   pv = (pv & ~m) | v;
@@ -31,23 +31,23 @@ void Diag::add_proj(int bit, int value) {
 
 void Diag::add_cz(int b0, int b1) {
   const int lo = std::min(b0, b1), d = std::abs(b0 - b1);
-  cz[d] ^= 1u << lo;  // CZ^2 = I
+  cz[d] ^= 1ull << lo;  // CZ^2 = I
 }
 
-int Diag::phase(uint32_t i) const {
-  int ph = ph0 + __builtin_popcount(i & t1) + 2 * __builtin_popcount(i & t2) + 4 * __builtin_popcount(i & zm);
-  for (int d = 1; d < 32; ++d) ph += 4 * __builtin_popcount(i & (i >> d) & cz[d]);
+int Diag::phase(uint64_t i) const {
+  int ph = ph0 + __builtin_popcountll(i & t1) + 2 * __builtin_popcountll(i & t2) + 4 * __builtin_popcountll(i & zm);
+  for (int d = 1; d < 64; ++d) ph += 4 * __builtin_popcountll(i & (i >> d) & cz[d]);
   return ph & 7;
 }
 
 Diag Diag::merge(const Diag &a, const Diag &b) {
   Diag d = a;
-  for (int bit = 0; bit < 32; ++bit) {
+  for (int bit = 0; bit < 64; ++bit) {
     const int cb = b.count(bit);
     if (cb) d.set_count(bit, d.count(bit) + cb);
   }
-  for (int k = 0; k < 32; ++k) d.cz[k] ^= b.cz[k];  // CZ^2 = I
-  const uint32_t overlap = a.pm & b.pm;
+  for (int k = 0; k < 64; ++k) d.cz[k] ^= b.cz[k];  // CZ^2 = I
+  const uint64_t overlap = a.pm & b.pm;
   if ((a.pv & overlap) != (b.pv & overlap)) d.allzero = true;
   d.pm = a.pm | b.pm;
   d.pv = (a.pv & a.pm) | (b.pv & b.pm);
@@ -55,6 +55,47 @@ Diag Diag::merge(const Diag &a, const Diag &b) {
   d.nhalf = a.nhalf + b.nhalf;
   d.allzero = d.allzero || a.allzero || b.allzero;
   return d;
+}
+
+Diag Diag::restrict_low(int hl, uint64_t g) const {
+  if (hl >= 64) return *this;
+  const uint64_t low = (1ull << hl) - 1ull;
+  Diag r = *this;
+  for (int bit = hl; bit < 64; ++bit) {  // counts on fixed bits: constants
+    const int c = count(bit);
+    if (!c) continue;
+    if ((g >> bit) & 1u) r.ph0 = (r.ph0 + c) & 7;
+    r.set_count(bit, 0);
+  }
+  const uint64_t fixed_pm = pm & ~low;  // projectors on fixed bits: pass or zero
+  if ((g & fixed_pm) != (pv & fixed_pm)) r.allzero = true;
+  r.pm &= low;
+  r.pv &= low;
+  for (int d = 1; d < 64; ++d) {
+    uint64_t keep = 0;
+    for (int a = 0; a + d < 64; ++a) {
+      if (!((cz[d] >> a) & 1u)) continue;
+      const int b = a + d;
+      const bool fa = a >= hl, fb = b >= hl;
+      if (!fa && !fb) {
+        keep |= 1ull << a;
+      } else if (fa && fb) {
+        if (((g >> a) & 1u) && ((g >> b) & 1u)) r.ph0 = (r.ph0 + 4) & 7;
+      } else if (fb && ((g >> b) & 1u)) {  // CZ with a set fixed bit: Z on the other one
+        r.set_count(a, r.count(a) + 4);
+      }
+    }
+    r.cz[d] = keep;
+  }
+  return r;
+}
+
+bool Diag::below(int bits) const {
+  const uint64_t hi = bits >= 64 ? 0ull : ~((1ull << bits) - 1ull);
+  if ((t1 | t2 | zm | pm | pv) & hi) return false;
+  for (int d = 1; d < 64; ++d)
+    if (cz[d] && (d >= bits || (cz[d] & hi))) return false;
+  return true;
 }
 
 double Diag::scale() const {
@@ -107,8 +148,8 @@ std::string build_circuit(uint32_t rows, uint32_t cols, uint32_t depth, const qs
   c.n = rows * cols;
   c.h_u = cut_row * cols;
   c.h_l = c.n - c.h_u;
-  if (c.h_u > 32 || c.h_l > 32) {
-    err << "each half must have at most 32 qubits (h_u=" << c.h_u << ", h_l=" << c.h_l << ")";
+  if (c.h_u > 36 || c.h_l > 36) {  // > 32: only as distributed halves (QSIM_OPT_DISTRIBUTE)
+    err << "each half must have at most 36 qubits (h_u=" << c.h_u << ", h_l=" << c.h_l << ")";
     return err.str();
   }
   if (n_gates && !gates) return "gates is NULL";

@@ -25,15 +25,18 @@ namespace qsim {
 // (bit b with bit b+d, mask bit at b; CZ = w^4 on |11>) — in the identity layout the
 // horizontal pairs sit at d = 1 and the vertical ones at d = cols, under a qubit relabelling
 // anywhere — pm/pv the projector constraint (P0 / P1, Eq. 1), nhalf the 1/sqrt2 factors.
+// Masks are 64-bit on the host (halves of up to 36 qubits); the device form
+// (kernels.h DiagDev) is 32-bit: a distributed half's diagonals are first restricted to the shard
+// (restrict_low: its global bits are constants of the rank).
 struct Diag {
-  uint32_t t1 = 0, t2 = 0, zm = 0, pm = 0, pv = 0;
-  uint32_t cz[32] = {};
+  uint64_t t1 = 0, t2 = 0, zm = 0, pm = 0, pv = 0;
+  uint64_t cz[64] = {};
   int ph0 = 0;
   int nhalf = 0;
   bool allzero = false;
 
   bool has_cz() const {
-    for (uint32_t m : cz)
+    for (uint64_t m : cz)
       if (m) return true;
     return false;
   }
@@ -49,7 +52,12 @@ struct Diag {
   // the product of two diagonals (they commute)
   static Diag merge(const Diag &a, const Diag &b);
   double scale() const;  // 2^(-nhalf/2)
-  int phase(uint32_t i) const;  // ph(i) mod 8 (host reference of the device formula)
+  int phase(uint64_t i) const;  // ph(i) mod 8 (host reference of the device formula)
+  // The diagonal on the indices whose bits >= hl equal those of g, as a diagonal over bits < hl:
+  // T / Z counts and projectors on fixed bits become constants, a CZ pair with one fixed bit a Z
+  // (or nothing) on the other bit, a pair of fixed bits a constant.
+  Diag restrict_low(int hl, uint64_t g) const;
+  bool below(int bits) const;  // every mask is below bit `bits`
 };
 
 // One non-diagonal gate of a sweep after factoring out its global phase:

@@ -92,9 +92,10 @@ def run_ranges(circ, Su, Sl, ranges, prec, opts):
 @pytest.mark.parametrize("prec", PRECS, ids=PNAME.get)
 @pytest.mark.parametrize("defer", [0, 1])
 @pytest.mark.parametrize("bfs", [0, 1])
-@pytest.mark.parametrize("lazy", [0, 2])
+@pytest.mark.parametrize("lazy", [0, 2, 3, 4])
 def test_d22_h14_forks(prec, defer, bfs, lazy, d22_h14):
-    """Deferred (default) and eager forks, depth-first and level-synchronous, lazy tail on / off."""
+    """Deferred (default) and eager forks, depth-first and level-synchronous, lazy tail off / by the
+    cost model / forced to two / three stages (cones of cones)."""
     circ, Su, Sl, ranges, ref = d22_h14
     A = run_ranges(circ, Su, Sl, ranges, prec,
                    {Q.QSIM_OPT_DEFER: defer, Q.QSIM_OPT_BFS: bfs, Q.QSIM_OPT_LAZY_LAST: lazy})

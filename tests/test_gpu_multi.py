@@ -40,3 +40,28 @@ def test_distributed_halves():
         r = subprocess.run(cmd, capture_output=True, text=True, timeout=1200)
         print(r.stdout[-4000:], r.stderr[-3000:])
         assert r.returncode == 0, n
+
+
+def _host_gib():
+    try:
+        with open("/proc/meminfo") as f:
+            for line in f:
+                if line.startswith("MemTotal"):
+                    return int(line.split()[1]) / (1 << 20)
+    except OSError:
+        pass
+    return 0.0
+
+
+@pytest.mark.slow
+@pytest.mark.skipif(_ngpus() < 2, reason="needs >= 2 GPUs")
+@pytest.mark.skipif(_host_gib() < 150, reason="the oracle's 2^33 leaf needs 128 GiB of host memory")
+def test_distributed_halves_above_32_qubits():
+    """66-qubit 6x11 grid: 33-qubit halves sharded over 2 GPUs (32-qubit shards, 64-bit host diagonals
+    restricted to each shard), leaf values of branches 0 and B-1 of both halves vs the oracle's 2^33 leaf."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr", "127.0.0.1", "--master-port", "29541", os.path.join(ROOT, "tools", "dist_big.py"),
+           "check", "10"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=3000)
+    print(r.stdout[-4000:], r.stderr[-3000:])
+    assert r.returncode == 0
