@@ -80,6 +80,8 @@ typedef struct {
   uint64_t layers_applied;   /* gate layers completed by the sweeps (> sweeps when layers are fused) */
   double sweep_bytes_moved;  /* bytes the sweeps actually read + wrote: sweep_bytes minus the reads of
                                 known-zero tiles that were skipped               */
+  uint64_t flip_siblings;    /* tree children reached as sibling flips of child 0 (no sweep of their own) */
+  uint64_t undo_sweeps;      /* inverse sweeps that restored a state overwritten in place (included in sweeps) */
 } qsim_stats_t;
 
 typedef enum {
@@ -114,7 +116,15 @@ typedef enum {
                                 phase wrap, stage rotation) in the parity tests                       */
   QSIM_OPT_DEFER = 10        /* 1 (default): deferred forks — each cut's P_b / Z^b is applied at the first
                                 layer that targets its qubit (branches share their state until then,
-                                DESIGN.md §5); 0: at the layer after the cut (A/B and tests)          */
+                                DESIGN.md §5); 0: at the layer after the cut (A/B and tests)          */,
+  QSIM_OPT_FLIP = 11,        /* 1 (default): sibling flips in qsim_evolve_range for half states above
+                                256 MiB — the 2^k children of a Z^b fork are one state seen through a bit
+                                flip and a diagonal, so only child 0 runs the fork's sweep; the free cuts
+                                of a block take Z^b on both endpoints (CZ = sum_ab H_ab Z^a (x) Z^b, the
+                                lower slices Walsh-Hadamard transformed); DESIGN.md §5. 0: off (A/B)  */
+  QSIM_OPT_FLIP_NB = 12      /* test only: at most this many state buffers beyond the first for the
+                                sibling-flip executor; further states run in place and are restored by
+                                inverse sweeps (-1, the default: as many as fit)                      */
 } qsim_option;
 
 /* Create a context bound to CUDA device `device` (no device call is made until the

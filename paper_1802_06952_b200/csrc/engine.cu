@@ -231,6 +231,14 @@ void Engine::set_option(int key, int64_t value) {
       if (value < 0 || value > 1) throw Error(QSIM_EINVAL, "QSIM_OPT_DEFER must be 0 or 1");
       deferred_ = value != 0;
       return;
+    case QSIM_OPT_FLIP:
+      if (value < 0 || value > 1) throw Error(QSIM_EINVAL, "QSIM_OPT_FLIP must be 0 or 1");
+      flip_ = value != 0;
+      return;
+    case QSIM_OPT_FLIP_NB:
+      if (value < -1 || value > 64) throw Error(QSIM_EINVAL, "QSIM_OPT_FLIP_NB must be -1 .. 64");
+      flip_max_nb_ = (int)value;
+      return;
     case QSIM_OPT_SWEEP_KERNEL:
       if (value < 0 || value > 3) throw Error(QSIM_EINVAL, "QSIM_OPT_SWEEP_KERNEL must be 0, 1, 2 or 3");
       sweep_kernel_ = (int)value;
@@ -327,6 +335,7 @@ std::vector<TilePlan> Engine::level_launches(const HalfProgram &hp, const Level 
   std::vector<TilePlan> out;
   for (size_t s = 0; s < n; ++s) {
     auto v = legacy_plans(hp, lev.sweeps[s]);
+    for (auto &tp : v) tp.sweep = (int)s;
     out.insert(out.end(), v.begin(), v.end());
   }
   return out;
@@ -760,9 +769,15 @@ std::vector<TilePlan> Engine::legacy_plans(const HalfProgram &hp, const Sweep &s
         tp.p.nruns = nr;
         tp.p.log2_ntiles = hp.hl - T;
         tp.targets = 0;
-        for (auto &g : H) tp.targets |= 1u << g.bit;
+        for (auto &g : H) {
+          tp.targets |= 1u << g.bit;
+          if (g.kind == 2) tp.sy_targets |= 1u << g.bit;
+        }
         if (ci == 0)
-          for (auto &g : low) tp.targets |= 1u << g.bit;
+          for (auto &g : low) {
+            tp.targets |= 1u << g.bit;
+            if (g.kind == 2) tp.sy_targets |= 1u << g.bit;
+          }
         tp.layers = ci == nchunks - 1 ? 1 : 0;
         if (ci == nchunks - 1) tp.swaps = sw.swaps;
         tp.use_pre = ci == 0;
@@ -770,6 +785,7 @@ std::vector<TilePlan> Engine::legacy_plans(const HalfProgram &hp, const Sweep &s
         tp.pre = sw.pre;
         Diag post = ci == nchunks - 1 ? sw.post : Diag();
         if (dist_) post = post.restrict_low(hp.hl, (uint64_t)rank_ << hp.hl);  // this rank's shard
+        tp.post = post;
         tp.p.post = to_dev(post);
         tp.p.post_s = make_split(post, reg_positions(tp.p, tp.npass - 1, c128_));
         int m = 0;
@@ -931,16 +947,20 @@ int Engine::tma_stages(const TilePlan &tp) const {
 }
 
 void Engine::launch_plan(const TilePlan &tp, const Diag &fork, bool first, const void *src, void *dst,
-                         const HalfProgram &hp, int out_buf, const Diag *child_fork) {
+                         const HalfProgram &hp, int out_buf, const Diag *child_fork, const Diag *pre_ov,
+                         const Diag *post_ov) {
   const int h = hp.hl;
   int pre_mode = 0;
   Diag pre;
   TileSweepParams p = tp.p;
+  // pre_ov / post_ov (sibling-flip executor): the complete pre / post diagonals of this launch
+  const bool use_pre = tp.use_pre || pre_ov;
   // a fork bit this launch targets is applied inside its gate (gate kind k + 2 f, sweep_tma.cu)
   // instead of through the pre diagonal: a Z^b or P_b fork then costs no per-element multiply
   uint32_t absorbed_pm = 0, absorbed_pv = 0;
-  Diag fk = fork;
-  if (tp.use_pre && absorb_ && !tp.gen && sweep_kernel_ != 1 && !dist_ && !fork.allzero) {
+  Diag fk = pre_ov ? *pre_ov : fork;
+  if (use_pre && absorb_ && !tp.gen && sweep_kernel_ != 1 && !dist_ && !fk.allzero) {
+    const Diag &fork = fk;
     const int L = tile_low_bits(c128_), VB = c128_ ? 0 : 1;
     const uint32_t cand = (uint32_t)((fork.pm ^ fork.zm) & (fork.pm | fork.zm) & tp.targets & ~(fork.t1 | fork.t2));
     for (int q = 0; q < 32; ++q) {
@@ -972,8 +992,8 @@ void Engine::launch_plan(const TilePlan &tp, const Diag &fork, bool first, const
       }
     }
   }
-  if (tp.use_pre) {
-    pre = Diag::merge(fk, tp.pre);
+  if (use_pre) {
+    pre = pre_ov ? fk : Diag::merge(fk, tp.pre);
     if (dist_) pre = pre.restrict_low(hp.hl, (uint64_t)rank_ << hp.hl);  // this rank's shard
     if (tp.gen)
       pre_mode = 2;
@@ -1019,6 +1039,10 @@ void Engine::launch_plan(const TilePlan &tp, const Diag &fork, bool first, const
       p.skip_pv = (uint32_t)child_fork->pv & p.skip_pm;
     }
     skip_pm_last_ = p.skip_pm;
+    if (post_ov) {
+      p.post = to_dev(*post_ov);
+      p.post_s = make_split(*post_ov, reg_positions(p, tp.npass - 1, c128_));
+    }
     const uint64_t tiles = 1ull << p.log2_ntiles;
     const bool tma = (sweep_kernel_ != 1 || p.nswap) && (pre_mode != 2 || (gen_tma_ && !dist_));
     if (tma) {
@@ -1396,13 +1420,26 @@ void Engine::evolve_range(uint64_t b0, uint64_t b1) {
   for (uint64_t s = b0; s < b1;) {
     uint64_t e = std::min(b1, (s / p2 + 1) * p2);
     e = std::min(e, s + chunk);
+    // sibling flips need Z^b forks: in the upper half (P_b canonically) the blocks' free cuts then
+    // take Z^b on both endpoints and the lower slices the Walsh-Hadamard transform (R-zz)
+    const bool zz = flip_half(0) && deferred_;
     for (int h = 0; h < 2; ++h) {
       void *sl = h == 0 ? U_.ptr : L_.ptr;
       const int64_t ns = h == 0 ? nu : nl;
       if (deferred_ && !dist_ && half_[h].tree)
-        evolve_tree(h, s, e, sl, d_Sp_[h].as<uint64_t>(), ns);
+        evolve_tree(h, s, e, sl, d_Sp_[h].as<uint64_t>(), ns, false, flip_half(h), zz);
       else
         evolve_half(h, s, e, sl, d_Sp_[h].as<uint64_t>(), ns);
+    }
+    if (zz) {  // the same aligned blocks as evolve_tree
+      for (uint64_t a = s; a < e;) {
+        int m = 0;
+        while (m < c && ((a >> m) & 1u) == 0 && a + (2ull << m) <= e) ++m;
+        check(launch_wht_rows((char *)L_.ptr + (size_t)(a - s) * (size_t)nl * amp_, c128_, m, nl, stream_),
+              "wht launch");
+        st_.kernel_launches += (uint64_t)m;
+        a += 1ull << m;
+      }
     }
     if (dist_ && world_ > 1) {
       // §2.3.3: each rank gathered the sampled entries it owns (zeros elsewhere).  The lower
@@ -2324,7 +2361,7 @@ void Engine::choose_roles() {
 
 // [b0, b1) as aligned power-of-two blocks; slice row r = branch b0 + r
 void Engine::evolve_tree(int half, uint64_t b0, uint64_t b1, void *slice, const uint64_t *dS, int64_t nS,
-                         bool canonical) {
+                         bool canonical, bool flip, bool zz) {
   Nvtx nv(half == 0 ? "upper half tree" : "lower half tree");
   HalfExec &he = half_[half];
   if (he.glayers.empty()) {
@@ -2337,13 +2374,16 @@ void Engine::evolve_tree(int half, uint64_t b0, uint64_t b1, void *slice, const 
     int m = 0;
     while (m < c && ((s >> m) & 1u) == 0 && s + (2ull << m) <= b1) ++m;
     static const std::vector<char> none;
-    evolve_block(half, s, m, (char *)slice + (s - b0) * (uint64_t)nS * amp_, dS, nS, canonical ? none : roles_);
+    // zz: Z^b on the upper endpoint of every free cut of the block (evolve_block keeps the fixed ones)
+    const std::vector<char> zroles(zz && half == 0 ? (size_t)c : 0, 0);
+    evolve_block(half, s, m, (char *)slice + (s - b0) * (uint64_t)nS * amp_, dS, nS,
+                 canonical ? none : zz ? (half == 0 ? zroles : none) : roles_, flip);
     s += 1ull << m;
   }
 }
 
 void Engine::evolve_block(int half, uint64_t b0, int m, void *slice, const uint64_t *dS, int64_t nS,
-                          const std::vector<char> &roles) {
+                          const std::vector<char> &roles, bool flip) {
   HalfExec &he = half_[half];
   const int c = (int)circ_.cuts.size();
   const int T = tile_low_bits(c128_) + kHiBits;
@@ -2381,12 +2421,24 @@ void Engine::evolve_block(int half, uint64_t b0, int m, void *slice, const uint6
   }
   int nbuf = (int)std::min<size_t>(nfit, 12);
   if (mem_budget_ > 0) nbuf = std::max(1, std::min<int>(nbuf, (int)((size_t)mem_budget_ / state_bytes_)));
-  const TreeChoice tc = choose_tree(half, m, lz, nS, nbuf, !bfs);
   // a swapped cut (P on the lower endpoint) changes the single branches, only the sum over both
   // values of its bit is CZ: the block's fixed bits keep the canonical roles (qsim.h: U_b, L_b)
   std::vector<char> eff = roles;
   for (int g = 0; g < c - m && g < (int)eff.size(); ++g) eff[g] = 1;
   if (std::find(eff.begin(), eff.end(), 0) == eff.end()) eff.clear();
+  std::vector<int> pin(c, -1);
+  for (int g = 0; g < c - m; ++g) pin[g] = (int)((b0 >> (c - 1 - g)) & 1u);
+  if (flip && !bfs) {  // sibling flips (run_tree_flip); false: not applicable, the executor below
+    const TreeChoice fc = flip_choice(half, m);
+    const TreeVariant &fv = variant(half, fc.apply, eff);
+    if (std::getenv("QSIM_DEBUG_TREE")) {
+      std::fprintf(stderr, "flip tree half %d b0=%llu m=%d nbuf=%d levels", half, (unsigned long long)b0, m, nbuf);
+      for (auto &l : fv.prog.levels) std::fprintf(stderr, " [%d:k%d s%zu]", l.fork_layer + 1, l.k, l.sweeps.size());
+      std::fprintf(stderr, "\n");
+    }
+    if (run_tree_flip(half, fv, lz, pin, m, slice, dS, nS, nbuf)) return;
+  }
+  const TreeChoice tc = choose_tree(half, m, lz, nS, nbuf, !bfs);
   const TreeVariant &v = variant(half, tc.apply, eff);
   ensure_states(half, tc.points + 1);
   size_t bfs_avail = 0;  // memory the level-synchronous buffers may take (0: none)
@@ -2401,8 +2453,6 @@ void Engine::evolve_block(int half, uint64_t b0, int m, void *slice, const uint6
     for (auto &l : v.prog.levels) std::fprintf(stderr, " [%d:k%d s%zu]", l.fork_layer + 1, l.k, l.sweeps.size());
     std::fprintf(stderr, "\n");
   }
-  std::vector<int> pin(c, -1);
-  for (int g = 0; g < c - m; ++g) pin[g] = (int)((b0 >> (c - 1 - g)) & 1u);
   const size_t nq = tc.qlist.size();
   for (uint64_t q = 0; q < (1ull << nq); ++q) {
     for (size_t i = 0; i < nq; ++i) pin[tc.qlist[i]] = (int)((q >> i) & 1u);
@@ -2606,6 +2656,260 @@ bool Engine::bfs_tree(const TreeVariant &v, int lz, int M, const std::vector<int
   return true;
 }
 
+// ---------------------------------------------------------------- sibling flips
+// DESIGN.md §5 "Sibling flips".  Let G = post . gates . pre be the first sweep of a fork level
+// and Z^b the fork (the block's free cuts carry Z^b on both endpoints in qsim_evolve_range, R-zz).
+// For a qubit q that G targets with g, G Z_q G^-1 = post (g Z g^-1)_q post^-1 with g Z g^-1 = -Y
+// for X^1/2 and X for Y^1/2 (the factored forms I - iX, I - iY); Z_q on a qubit G does not target
+// commutes with G.  So child b of the fork is child 0 seen through a bit flip and a diagonal:
+//   c_b(x) = Phi_b(x) c_0(x ^ m_b),   Phi_b = post / post^{m_b} * psi_b * Z^{untargeted bits of b},
+// m_b = the targeted fork qubits of b, psi_b(x) = i (-1)^{x_q} per X^1/2-targeted one (-Y is a
+// flip with that phase), D^m(x) = D(x ^ m) (Diag::shift).  Only child 0 runs G.  A sweep reading a
+// state V(x) = phi(x) buf[x ^ m] runs conjugated by the flip,
+//   G V = X^m [post^m Z_Ym] gates [Z_Ym pre^m phi^m] buf,
+// (X^m SY' X^m = Z SY' Z on the Y^1/2 targets Ym in m; X^1/2 commutes with X), so no kernel reads a
+// permuted address: the output stays in the flipped coordinates and the leaf gather reads x ^ m.
+bool Engine::flip_half(int half) const {
+  const HalfExec &he = half_[half];
+  if (!flip_ || !deferred_ || dist_ || !he.tree || sweep_kernel_ == 1 || he.prog.hl > 32) return false;
+  const size_t sb = ((size_t)1 << he.prog.hl) * amp_;
+  return !(bfs_ && sb <= ((size_t)256 << 20));
+}
+
+// every free cut forks at the input of its first target layer (latest placement; with sibling flips
+// a level costs one sweep per parent plus its remaining sweeps per child, so later is never worse),
+// or in the leaf gather (lazy tail / never targeted); the block's fixed cuts at the first gate layer
+// after the cut (their P_b / Z^b are constants of the block)
+TreeChoice Engine::flip_choice(int half, int m) const {
+  const HalfExec &he = half_[half];
+  const int c = (int)circ_.cuts.size();
+  const std::vector<int> &gl = he.glayers;
+  TreeChoice tc;
+  tc.apply.assign(c, 0);
+  for (int g = 0; g < c; ++g) {
+    if (g >= c - m) {
+      tc.apply[g] = he.ft[g];
+      continue;
+    }
+    size_t i = 0;
+    while (i < gl.size() && gl[i] <= (int)circ_.cuts[g].layer) ++i;
+    tc.apply[g] = i < gl.size() ? gl[i] : (int)circ_.depth + 1;
+  }
+  return tc;
+}
+
+// runs the launches `tps` (one or more sweeps of a level) on the state `in` into buffer dst (in
+// place when dst == in.buf), conjugated by in's flip; `fork` joins the first launch's pre diagonal
+void Engine::flip_exec(const std::vector<const TilePlan *> &tps, const Diag &fork, const VState &in, int dst,
+                       const HalfProgram &hp, std::vector<Executed> *rec) {
+  for (size_t i = 0; i < tps.size(); ++i) {
+    const TilePlan &tp = *tps[i];
+    Diag zy;  // Z on the Y^1/2 targets of this launch inside the flip
+    for (int q = 0; q < 32; ++q)
+      if (((tp.sy_targets & (uint32_t)in.m) >> q) & 1u) zy.add_Z(q);
+    const Diag base = i == 0 ? Diag::merge(fork, tp.pre) : (tp.use_pre ? tp.pre : Diag());
+    Diag pre = Diag::merge(zy, base.shift(in.m));
+    if (i == 0 && in.has_phi) pre = Diag::merge(pre, in.phi.shift(in.m));
+    const Diag post = Diag::merge(tp.post.shift(in.m), zy);
+    const void *src = tp.gen ? nullptr : states_[i == 0 ? in.buf : dst]->ptr;
+    launch_plan(tp, Diag(), i == 0, src, states_[dst]->ptr, hp, -1, nullptr, &pre, &post);
+    if (rec) rec->push_back(Executed{&tp, pre, post});
+  }
+}
+
+// restores the input of the executed launches `rec` (run in place on buf) by their inverses, last
+// first: (post . gates . pre)^-1 = pre^-1 (Z_T gates Z_T / 2^nt) post^-1, since (I - iX)^-1 =
+// Z (I - iX) Z / 2 and (I - iY)^-1 = Z (I - iY) Z / 2 — the same kernel with other diagonals
+void Engine::flip_undo(const std::vector<Executed> &rec, int buf, const HalfProgram &hp) {
+  for (size_t i = rec.size(); i-- > 0;) {
+    const Executed &e = rec[i];
+    Diag zt;
+    int nt = 0;
+    for (int q = 0; q < 32; ++q)
+      if ((e.tp->targets >> q) & 1u) zt.add_Z(q), ++nt;
+    const Diag pre = Diag::merge(zt, e.post.inverse());
+    Diag post = Diag::merge(e.pre.inverse(), zt);
+    post.nhalf += 2 * nt;
+    launch_plan(*e.tp, Diag(), true, states_[buf]->ptr, states_[buf]->ptr, hp, -1, nullptr, &pre, &post);
+    st_.undo_sweeps++;
+  }
+}
+
+// The tree of one block with sibling flips (depth-first).  Buffers: the root path runs in buffer 0;
+// a level's child-0 state whose source must survive (more siblings to come) goes to a buffer of its
+// own ("slot") when one is left, else in place over the source and is undone after its subtree.
+// Slots are given buffers by the launches the undo would cost (instances x launches).  false: not
+// applicable (a free fork that is a projector, or an in-place slot that could not be inverted).
+bool Engine::run_tree_flip(int half, const TreeVariant &v, int lz, const std::vector<int> &pin, int m, void *slice,
+                           const uint64_t *dS, int64_t nS, int nbuf) {
+  const HalfProgram &hp = v.prog;
+  const int F = (int)hp.levels.size() - 1, c = (int)circ_.cuts.size();
+  std::vector<int> start(F + 2, 0);
+  for (int l = 0; l <= F; ++l) start[l + 1] = start[l] + (int)hp.levels[l].sweeps.size();
+  const int Sm = start[F + 1] - lz;
+  int M = 0;
+  std::vector<int> skip(F + 1, 0);
+  for (int l = 0; l <= F; ++l) {
+    const int n = (int)hp.levels[l].sweeps.size();
+    const int mat = std::max(0, std::min(n, Sm - start[l]));
+    if (mat > 0) M = l;
+    skip[l] = n - mat;
+  }
+  std::vector<std::vector<const TilePlan *>> first(F + 1), rest(F + 1);
+  for (int l = 0; l <= M; ++l) {
+    if ((size_t)skip[l] >= v.plans[l].size()) throw Error(QSIM_EINVAL, "internal: lazy tail longer than the plans");
+    for (const TilePlan &tp : v.plans[l][(size_t)skip[l]]) {
+      if (!tp.swaps.empty()) return false;
+      (tp.sweep == 0 ? first[l] : rest[l]).push_back(&tp);
+    }
+  }
+  std::vector<ChildSet> cs(F + 1);
+  for (int l = 1; l <= F; ++l) {
+    cs[l] = child_set(hp.levels[l], pin);
+    if (l <= M)
+      for (int j : cs[l].free)
+        if ((hp.levels[l].pmask >> j) & 1u) return false;  // a free projector fork: no sibling flips
+  }
+  // slots: X(l) = level l's first sweep from a shared parent state (once per parent), D(l) = the
+  // rest of level l from the shared child-0 state (once per child)
+  struct Slot {
+    double cost;
+    int level;
+    bool d, must;
+  };
+  std::vector<Slot> slots;
+  int fb = 0;
+  for (int l = 1; l <= M; ++l) {
+    if (fb > 0) {
+      const bool proj = hp.fork_diag(l, cs[l].base).pm != 0;  // pinned projector: not invertible
+      slots.push_back(Slot{std::ldexp(1.0, fb) * (double)first[l].size(), l, false, proj});
+    }
+    fb += (int)cs[l].free.size();
+    if (!rest[l].empty() && fb > 0) slots.push_back(Slot{std::ldexp(1.0, fb) * (double)rest[l].size(), l, true, false});
+  }
+  std::sort(slots.begin(), slots.end(), [](const Slot &a, const Slot &b) {
+    return a.must != b.must ? a.must : a.cost > b.cost;
+  });
+  int budget = std::max(0, nbuf - 1);
+  if (flip_max_nb_ >= 0) budget = std::min(budget, flip_max_nb_);
+  std::vector<char> nbX(F + 1, 0), nbD(F + 1, 0);
+  int nb = 0;
+  for (const Slot &s : slots) {
+    if (nb < budget) {
+      (s.d ? nbD : nbX)[s.level] = 1;
+      ++nb;
+    } else if (s.must) {
+      return false;
+    }
+  }
+  ensure_states(half, 1 + nb);
+  std::vector<int> freebuf;
+  for (int i = nb; i >= 1; --i) freebuf.push_back(i);
+  auto alloc = [&]() {
+    const int b = freebuf.back();
+    freebuf.pop_back();
+    return b;
+  };
+  if (std::getenv("QSIM_DEBUG_TREE")) {
+    std::fprintf(stderr, "flip tree half %d m=%d lz=%d M=%d buffers=%d slots:", half, m, lz, M, 1 + nb);
+    for (const Slot &s : slots)
+      std::fprintf(stderr, " %c%d(%.0f%s)", s.d ? 'D' : 'X', s.level, s.cost,
+                   (s.d ? nbD : nbX)[s.level] ? ",own" : ",in place");
+    std::fprintf(stderr, "\n");
+  }
+  // C = T_f X: child f (free fork bits, relative to child 0) of level lev, first sweep s0
+  auto sibling = [&](const Level &lev, const ChildSet &cq, uint64_t f, const VState &X) {
+    uint64_t zq = 0;
+    for (size_t t = 0; t < cq.free.size(); ++t)
+      if ((f >> t) & 1u) zq ^= 1ull << lev.cut_bits[cq.free[t]];
+    if (!zq) return X;
+    const Sweep &s0 = lev.sweeps[0];
+    uint64_t tg = 0, sx = 0;
+    for (const Gate1 &g : s0.gates) {
+      tg |= 1ull << g.bit;
+      if (g.kind == 1) sx |= 1ull << g.bit;
+    }
+    const uint64_t mf = zq & tg;
+    Diag phi;
+    for (int b = 0; b < 64; ++b) {
+      if (!((zq >> b) & 1u)) continue;
+      if (!((mf >> b) & 1u)) {
+        phi.add_Z(b);  // untargeted: Z commutes with the sweep
+      } else if ((sx >> b) & 1u) {
+        phi.add_Z(b);  // X^1/2: -Y = flip with phase i (-1)^{x_q}
+        phi.ph0 = (phi.ph0 + 2) & 7;
+      }
+    }
+    const Diag post = s0.post.phase_only();
+    phi = Diag::merge(phi, Diag::merge(post, post.shift(mf).inverse()));
+    VState C;
+    C.buf = X.buf;
+    C.m = X.m ^ mf;
+    C.phi = X.has_phi ? Diag::merge(phi, X.phi.shift(mf)) : phi;
+    C.has_phi = true;
+    st_.flip_siblings++;
+    return C;
+  };
+  std::function<void(int, const VState &, bool, uint64_t)> node = [&](int l, const VState &V, bool keepV,
+                                                                       uint64_t bacc) {
+    if (l == M) {
+      gather_tree(v, lz, M, pin, states_[V.buf]->ptr, bacc, m, slice, dS, nS, V.m, V.has_phi ? &V.phi : nullptr);
+      return;
+    }
+    const int q = l + 1;
+    const Level &lev = hp.levels[q];
+    const ChildSet &cq = cs[q];
+    const uint64_t nch = 1ull << cq.free.size();
+    int xb = V.buf;
+    bool xnew = false, xip = false;
+    if (keepV) {
+      if (nbX[q])
+        xb = alloc(), xnew = true;
+      else
+        xip = true;
+    }
+    std::vector<Executed> rx;
+    flip_exec(first[q], hp.fork_diag(q, cq.base), V, xb, hp, xip ? &rx : nullptr);
+    VState X;
+    X.buf = xb;
+    X.m = V.m;
+    for (uint64_t f = 0; f < nch; ++f) {
+      const bool keepX = f + 1 < nch || xip;
+      const VState C = sibling(lev, cq, f, X);
+      const uint64_t bits = bacc | branch_bits(lev, child_of(lev, cq, f), c);
+      if (rest[q].empty()) {
+        node(q, C, keepX, bits);
+        continue;
+      }
+      int db = xb;
+      bool dnew = false, dip = false;
+      if (keepX) {
+        if (nbD[q])
+          db = alloc(), dnew = true;
+        else
+          dip = true;
+      }
+      std::vector<Executed> rd;
+      flip_exec(rest[q], Diag(), C, db, hp, dip ? &rd : nullptr);
+      VState D;
+      D.buf = db;
+      D.m = C.m;
+      node(q, D, dip, bits);
+      if (dip) flip_undo(rd, db, hp);
+      if (dnew) freebuf.push_back(db);
+    }
+    if (xip) flip_undo(rx, xb, hp);
+    if (xnew) freebuf.push_back(xb);
+  };
+  VState root;
+  root.buf = 0;
+  std::vector<const TilePlan *> all0 = first[0];
+  all0.insert(all0.end(), rest[0].begin(), rest[0].end());
+  flip_exec(all0, Diag(), root, 0, hp, nullptr);
+  node(0, root, false, 0);
+  return true;
+}
+
 void Engine::run_tree(int half, const TreeVariant &v, int lz, const std::vector<int> &pin, int m, void *slice,
                       const uint64_t *dS, int64_t nS, size_t bfs_avail) {
   (void)half;
@@ -2652,7 +2956,8 @@ void Engine::run_tree(int half, const TreeVariant &v, int lz, const std::vector<
 // the levels that start at a lazy sweep enter that stage's pre diagonal, those of a trailing level
 // without sweeps (cuts never targeted again) its post diagonal; one output row per fork value.
 void Engine::gather_tree(const TreeVariant &v, int lz, int M, const std::vector<int> &pin, const void *psi,
-                         uint64_t bacc, int m, void *slice, const uint64_t *dS, int64_t nS) {
+                         uint64_t bacc, int m, void *slice, const uint64_t *dS, int64_t nS, uint64_t xmask,
+                         const Diag *phi) {
   Nvtx nv("leaf gather");
   const HalfProgram &hp = v.prog;
   const int F = (int)hp.levels.size() - 1, c = (int)circ_.cuts.size();
@@ -2689,9 +2994,13 @@ void Engine::gather_tree(const TreeVariant &v, int lz, int M, const std::vector<
     ll.post = to_dev(post, true);
     return ll;
   };
+  // a sibling-flip state (flip_node): psi read at x ^ xmask, phi joins the first diagonal
+  auto with_phi = [&](const Diag &d) { return phi ? Diag::merge(d, *phi) : d; };
   if (lz == 0) {
     for (const Combo &cb : combos(pl, -1)) {
-      check(launch_gather(psi, dS, nS, row(bacc | cb.bits), to_dev(cb.d[0]), c128_, stream_), "gather launch");
+      check(launch_gather(psi, dS, nS, row(bacc | cb.bits), to_dev(with_phi(cb.d[0])), c128_, stream_, ~0ull, 0,
+                          xmask),
+            "gather launch");
       st_.kernel_launches++;
     }
     return;
@@ -2717,7 +3026,9 @@ void Engine::gather_tree(const TreeVariant &v, int lz, int M, const std::vector<
     const Sweep &sw = *st[s2].first;
     const bool last = s2 == L - 1;
     for (const Combo &cb : combos(st[s2].second, last ? pl : -1)) {
-      const LazyLayer ll = lazy(sw, Diag::merge(sw.pre, cb.d[0]), last ? Diag::merge(sw.post, cb.d[1]) : sw.post);
+      const Diag pre0 = Diag::merge(sw.pre, cb.d[0]);
+      LazyLayer ll = lazy(sw, s2 == 0 ? with_phi(pre0) : pre0, last ? Diag::merge(sw.post, cb.d[1]) : sw.post);
+      if (s2 == 0) ll.xmask = xmask;
       void *out = last ? (void *)row(bacc | bits | cb.bits) : lazy_val_[s2].ptr;
       if (s2 == 0)
         check(launch_gather_layer(psi, idx[0], cnt[0], out, ll, c128_, stream_), "gather_layer launch");

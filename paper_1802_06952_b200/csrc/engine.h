@@ -54,6 +54,11 @@ struct TilePlan {
   std::vector<int> pass0_regs;  // global bits of the pass-0 register slots (pre DiagSplit)
   uint32_t targets = ~0u;  // bits this launch applies gates on (all: unknown)
   uint32_t zfix = 0;       // fork bits of the level not targeted by an earlier launch of the level
+  // host forms for the sibling-flip executor (Engine::flip_node): the post diagonal (identity
+  // except on the last launch of a sweep), the Y^1/2 targets, the sweep's index in its level
+  Diag post;
+  uint32_t sy_targets = 0;
+  int sweep = 0;
 };
 
 
@@ -211,10 +216,33 @@ class Engine {
   TreeVariant &variant(int half, const std::vector<int> &apply, const std::vector<char> &roles);
   // canonical: P_b on the upper endpoint of every cut (the branch states of qsim_branch_state /
   // qsim_branch_values); else the per-cut roles_ of the reconstruction (choose_roles)
+  // flip: the sibling-flip executor may run the blocks (flip_node); zz: Z^b forks on the upper
+  // endpoints of the blocks' free cuts (the lower slices then take the Walsh-Hadamard transform)
   void evolve_tree(int half, uint64_t b0, uint64_t b1, void *slice, const uint64_t *dS, int64_t nS,
-                   bool canonical = false);
+                   bool canonical = false, bool flip = false, bool zz = false);
   void evolve_block(int half, uint64_t b0, int m, void *slice, const uint64_t *dS, int64_t nS,
-                    const std::vector<char> &roles);
+                    const std::vector<char> &roles, bool flip = false);
+  // ---- sibling-flip executor (DESIGN.md §5 "Sibling flips").  A node state is a buffer seen
+  // through a bit flip and a diagonal: V(x) = phi(x) * buf[x ^ m].
+  struct VState {
+    int buf = 0;
+    uint64_t m = 0;
+    Diag phi;
+    bool has_phi = false;
+  };
+  struct Executed {  // a launch as run (pre / post as passed to launch_plan), for its inverse
+    const TilePlan *tp;
+    Diag pre, post;
+  };
+  bool flip_half(int half) const;
+  TreeChoice flip_choice(int half, int m) const;
+  bool run_tree_flip(int half, const TreeVariant &v, int lz, const std::vector<int> &pin, int m, void *slice,
+                     const uint64_t *dS, int64_t nS, int nbuf);
+  void flip_exec(const std::vector<const TilePlan *> &tps, const Diag &fork, const VState &in, int dst,
+                 const HalfProgram &hp, std::vector<Executed> *rec);
+  void flip_undo(const std::vector<Executed> &rec, int buf, const HalfProgram &hp);
+  bool flip_ = !(std::getenv("QSIM_FLIP") && std::getenv("QSIM_FLIP")[0] == '0');
+  int flip_max_nb_ = -1;  // QSIM_OPT_FLIP_NB (tests): at most this many extra buffers (in-place + undo beyond)
   void choose_roles();
   std::vector<char> roles_;  // per cut: 1 = P on the upper endpoint (empty: all 1)
   bool roles_chosen_ = false;
@@ -223,7 +251,8 @@ class Engine {
   void run_tree(int half, const TreeVariant &v, int lz, const std::vector<int> &pin, int m, void *slice,
                 const uint64_t *dS, int64_t nS, size_t bfs_avail);
   void gather_tree(const TreeVariant &v, int lz, int M, const std::vector<int> &pin, const void *psi,
-                   uint64_t bacc, int m, void *slice, const uint64_t *dS, int64_t nS);
+                   uint64_t bacc, int m, void *slice, const uint64_t *dS, int64_t nS, uint64_t xmask = 0,
+                   const Diag *phi = nullptr);
   // level-synchronous subtree of a tree path below level l (node-batched sweeps; small states)
   bool bfs_tree(const TreeVariant &v, int lz, int M, const std::vector<int> &skip, const std::vector<int> &pin,
                 int l, const void *state, uint64_t bacc, int m, void *slice, const uint64_t *dS, int64_t nS,
@@ -263,7 +292,8 @@ class Engine {
   int lazy_depth(int half, int64_t nS) const;
   int tma_stages(const TilePlan &tp) const;
   void launch_plan(const TilePlan &tp, const Diag &fork, bool first_chunk_of_level, const void *src,
-                   void *dst, const HalfProgram &hp, int out_buf = -1, const Diag *child_fork = nullptr);
+                   void *dst, const HalfProgram &hp, int out_buf = -1, const Diag *child_fork = nullptr,
+                   const Diag *pre_ov = nullptr, const Diag *post_ov = nullptr);
   void gather_leaf(int half, uint64_t child_last, const void *psi, const uint64_t *dS, int64_t nS,
                    void *out_row, int depth);
   void gemm(const void *U, const void *L, int64_t K, int64_t M, int64_t N, double *A);

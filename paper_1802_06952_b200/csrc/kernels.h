@@ -158,10 +158,11 @@ cudaError_t launch_small(const SmallParams &p, bool c128, uint64_t nb, cudaStrea
 int small_max_h(bool c128);
 
 // ---------------------------------------------------------------- gather / reconstruction
-// out[j] = pend(S[j]) psi[S[j] & lmask] if (S[j] & ~lmask) == gsel (the shard owns it), else 0
+// out[j] = pend(S[j]) psi[(S[j] ^ xmask) & lmask] if (S[j] & ~lmask) == gsel (the shard owns it),
+// else 0; xmask: the state is a sibling flip of the buffer (Engine::flip_node)
 cudaError_t launch_gather(const void *psi, const uint64_t *S, int64_t n, void *out,
                           const DiagDev &pend, bool c128, cudaStream_t s, uint64_t lmask = ~0ull,
-                          uint64_t gsel = 0);
+                          uint64_t gsel = 0, uint64_t xmask = 0);
 
 // Leaves of a node-batched level: out[row(node) * n + j] = pend(S[j]) fork(node, S[j]) *
 // psi[(node >> shift) * stride + S[j]], row(node) = rowmap ? rowmap[node] : node
@@ -175,6 +176,9 @@ struct RowMapDev {
   uint8_t pos[32];
 };
 cudaError_t launch_rowmap(uint32_t *out, int64_t n, const RowMapDev &rm, cudaStream_t s);
+// rows [0, 2^m) of a slice (ncols entries each, ctx precision): Walsh-Hadamard transform over the m
+// row-index bits with 1/2 per bit (m launches)
+cudaError_t launch_wht_rows(void *A, bool c128, int m, int64_t ncols, cudaStream_t s);
 // Lazy last layer: the leaf's final sweep evaluated only at the sampled indices,
 //   out[j] = post(x) * sum_y  prod_t M'_t[x_t, y_t] * pre(y) * psi[y],   x = S[j],
 // y ranging over the 2^k values of the sweep's target bits (others equal to x).
@@ -191,6 +195,8 @@ struct LazyLayer {
   uint64_t node_stride;
   int64_t nper;
   const uint32_t *rowmap;
+  // psi read at y ^ xmask (launch_gather_layer only): the state is a sibling flip of the buffer
+  uint64_t xmask;
 };
 cudaError_t launch_gather_layer(const void *psi, const uint64_t *S, int64_t n, void *out,
                                 const LazyLayer &ll, bool c128, cudaStream_t s);

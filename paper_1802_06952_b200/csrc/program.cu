@@ -99,9 +99,55 @@ bool Diag::below(int bits) const {
 }
 
 double Diag::scale() const {
-  double s = std::ldexp(1.0, -(nhalf / 2));
-  if (nhalf & 1) s *= 0.70710678118654752440;
+  // 2^(-nhalf/2) for either sign of nhalf (inverse diagonals carry nhalf < 0)
+  const int q = nhalf >= 0 ? nhalf / 2 : -((1 - nhalf) / 2);  // floor(nhalf / 2)
+  double s = std::ldexp(1.0, -q);
+  if (nhalf - 2 * q) s *= 0.70710678118654752440;
   return s;
+}
+
+Diag Diag::shift(uint64_t m) const {
+  Diag r = *this;
+  if (!m) return r;
+  r.pv = (pv ^ (m & pm)) & pm;
+  for (int a = 0; a < 64; ++a) {
+    if (!((m >> a) & 1u)) continue;
+    const int c = count(a);
+    r.ph0 = (r.ph0 + c) & 7;
+    r.set_count(a, (8 - c) & 7);
+  }
+  for (int d = 1; d < 64; ++d) {
+    if (!cz[d]) continue;
+    for (int a = 0; a + d < 64; ++a) {
+      if (!((cz[d] >> a) & 1u)) continue;
+      const int b = a + d;
+      const bool fa = (m >> a) & 1u, fb = (m >> b) & 1u;
+      if (fa) r.set_count(b, r.count(b) + 4);
+      if (fb) r.set_count(a, r.count(a) + 4);
+      if (fa && fb) r.ph0 = (r.ph0 + 4) & 7;
+    }
+  }
+  return r;
+}
+
+Diag Diag::inverse() const {
+  if (pm || allzero) throw std::invalid_argument("inverse of a projector");
+  Diag r = *this;
+  for (int a = 0; a < 64; ++a) {
+    const int c = count(a);
+    if (c) r.set_count(a, (8 - c) & 7);
+  }
+  r.ph0 = (8 - ph0) & 7;
+  r.nhalf = -nhalf;
+  return r;
+}
+
+Diag Diag::phase_only() const {
+  Diag r = *this;
+  r.pm = r.pv = 0;
+  r.nhalf = 0;
+  r.allzero = false;
+  return r;
 }
 
 Diag HalfProgram::fork_diag(int level, uint64_t child) const {

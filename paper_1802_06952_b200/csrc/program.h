@@ -58,6 +58,14 @@ struct Diag {
   // (or nothing) on the other bit, a pair of fixed bits a constant.
   Diag restrict_low(int hl, uint64_t g) const;
   bool below(int bits) const;  // every mask is below bit `bits`
+  // D^m(i) = D(i ^ m): the diagonal conjugated by the bit flip X^m (sibling flips of the tree
+  // executor, Engine::flip_node).  Per bit a in m: count c_a -> -c_a with c_a added to ph0; a CZ
+  // pair with one flipped bit adds Z on the other bit, with both flipped Z on both and ph0 += 4.
+  Diag shift(uint64_t m) const;
+  // 1 / D (no projector): phases negated (CZ terms are their own negation mod 8), scale inverted
+  Diag inverse() const;
+  // the phase of D only (scale 1, no projector)
+  Diag phase_only() const;
 };
 
 // One non-diagonal gate of a sweep after factoring out its global phase:

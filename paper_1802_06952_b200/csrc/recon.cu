@@ -28,7 +28,7 @@ struct CxT<double> {
 template <typename R>
 __global__ void gather_kernel(const typename CxT<R>::T *__restrict__ psi, const uint64_t *__restrict__ S,
                               int64_t n, typename CxT<R>::T *__restrict__ out, DiagDev d, uint64_t lmask,
-                              uint64_t gsel) {
+                              uint64_t gsel, uint64_t xmask) {
   using C = typename CxT<R>::T;
   for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n;
        j += (int64_t)gridDim.x * blockDim.x) {
@@ -37,7 +37,7 @@ __global__ void gather_kernel(const typename CxT<R>::T *__restrict__ psi, const 
       out[j].x = out[j].y = (R)0;
       continue;
     }
-    C x = psi[i & lmask];
+    C x = psi[(i ^ xmask) & lmask];
     if (d.active) {
       const uint32_t ii = (uint32_t)i;
       const int ph = diag_phase(ii, d, d.zm);
@@ -53,13 +53,51 @@ __global__ void gather_kernel(const typename CxT<R>::T *__restrict__ psi, const 
 }
 
 cudaError_t launch_gather(const void *psi, const uint64_t *S, int64_t n, void *out,
-                          const DiagDev &pend, bool c128, cudaStream_t s, uint64_t lmask, uint64_t gsel) {
+                          const DiagDev &pend, bool c128, cudaStream_t s, uint64_t lmask, uint64_t gsel,
+                          uint64_t xmask) {
   const int threads = 256;
   const int blocks = (int)std::min<int64_t>((n + threads - 1) / threads, 4096);
   if (c128)
-    gather_kernel<double><<<blocks, threads, 0, s>>>((const double2 *)psi, S, n, (double2 *)out, pend, lmask, gsel);
+    gather_kernel<double><<<blocks, threads, 0, s>>>((const double2 *)psi, S, n, (double2 *)out, pend, lmask, gsel,
+                                                     xmask);
   else
-    gather_kernel<float><<<blocks, threads, 0, s>>>((const float2 *)psi, S, n, (float2 *)out, pend, lmask, gsel);
+    gather_kernel<float><<<blocks, threads, 0, s>>>((const float2 *)psi, S, n, (float2 *)out, pend, lmask, gsel,
+                                                    xmask);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------- Walsh-Hadamard rows (R-zz)
+// With Z^b forks on both endpoints of a block's free cuts, CZ = sum_{a,b} H_ab Z^a (x) Z^b with
+// H = [[1, 1], [1, -1]] / 2 per cut, so the lower slice rows are replaced by sum_b H_ab L_b (DESIGN.md
+// R-zz): one butterfly pass per branch bit, (a + b) / 2 and (a - b) / 2 (exact scaling).
+template <typename R>
+__global__ void wht_rows_kernel(typename CxT<R>::T *__restrict__ A, int bit, int64_t npairs, int64_t ncols) {
+  using C = typename CxT<R>::T;
+  const int64_t total = npairs * ncols;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t p = e / ncols, j = e - p * ncols;
+    const int64_t r0 = ((p >> bit) << (bit + 1)) | (p & ((1ll << bit) - 1)), r1 = r0 | (1ll << bit);
+    const C a = A[r0 * ncols + j], b = A[r1 * ncols + j];
+    C s, d;
+    s.x = (a.x + b.x) * (R)0.5;
+    s.y = (a.y + b.y) * (R)0.5;
+    d.x = (a.x - b.x) * (R)0.5;
+    d.y = (a.y - b.y) * (R)0.5;
+    A[r0 * ncols + j] = s;
+    A[r1 * ncols + j] = d;
+  }
+}
+
+cudaError_t launch_wht_rows(void *A, bool c128, int m, int64_t ncols, cudaStream_t s) {
+  const int64_t npairs = m > 0 ? (1ll << (m - 1)) : 0;
+  if (npairs == 0 || ncols <= 0) return cudaSuccess;
+  const int blocks = (int)std::min<int64_t>((npairs * ncols + 255) / 256, 148 * 16);
+  for (int bit = 0; bit < m; ++bit) {
+    if (c128)
+      wht_rows_kernel<double><<<blocks, 256, 0, s>>>((double2 *)A, bit, npairs, ncols);
+    else
+      wht_rows_kernel<float><<<blocks, 256, 0, s>>>((float2 *)A, bit, npairs, ncols);
+  }
   return cudaGetLastError();
 }
 
@@ -174,7 +212,7 @@ __global__ void __launch_bounds__(256) gather_layer_kernel(const typename CxT<R>
     uint32_t y = base;
 #pragma unroll 4
     for (int t = 0; t < ll.k; ++t) y |= ((m >> t) & 1u) << ll.bit[t];
-    C v = psi[y & (uint32_t)ll.lmask];
+    C v = psi[(y ^ (uint32_t)ll.xmask) & (uint32_t)ll.lmask];
     int ph = 6 * __popc((x ^ y) & ll.sxmask) + 4 * __popc(~x & y & ll.symask);
     if (ll.pre.active) {
       ph += diag_phase(y, ll.pre, ll.pre.zm);

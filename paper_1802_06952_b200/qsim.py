@@ -33,6 +33,8 @@ QSIM_OPT_DISTRIBUTE = 7
 QSIM_OPT_BFS = 8
 QSIM_OPT_MAX_CTAS = 9
 QSIM_OPT_DEFER = 10
+QSIM_OPT_FLIP = 11
+QSIM_OPT_FLIP_NB = 12
 
 EXPORTED = ["qsim_create", "qsim_destroy", "qsim_last_error", "qsim_version", "qsim_set_option",
             "qsim_set_stream", "qsim_load_circuit", "qsim_partition", "qsim_set_blocks",
@@ -58,7 +60,8 @@ class qsim_stats_t(C.Structure):
     _fields_ = [("kernel_launches", C.c_uint64), ("sweeps", C.c_uint64), ("sweep_states", C.c_uint64),
                 ("sweep_bytes", C.c_double), ("sweep_ms", C.c_double), ("timed_sweeps", C.c_uint64),
                 ("gemm_flops", C.c_double), ("gemm_ms", C.c_double), ("branches_evolved", C.c_uint64),
-                ("lazy_gathers", C.c_uint64), ("layers_applied", C.c_uint64), ("sweep_bytes_moved", C.c_double)]
+                ("lazy_gathers", C.c_uint64), ("layers_applied", C.c_uint64), ("sweep_bytes_moved", C.c_double),
+                ("flip_siblings", C.c_uint64), ("undo_sweeps", C.c_uint64)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
