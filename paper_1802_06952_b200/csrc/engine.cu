@@ -411,13 +411,16 @@ std::vector<double> Engine::deferred_layer_weights(int half, int64_t nS) {
   const int c = (int)circ_.cuts.size();
   if (nS <= 0) nS = 4096;
   const int lz = tree_lazy(half, nS);
-  const TreeChoice tc = choose_tree(half, c, lz, nS, 6, true);
+  // sibling flips: a level's first sweep runs once per parent, its later ones once per child, so the
+  // sweep of layer t runs 2^{#forks applied before t} times; else 2^{#forks applied at or before t}
+  const bool flip = flip_half(half);
+  const TreeChoice tc = flip ? flip_choice(half, c) : choose_tree(half, c, lz, nS, 6, true);
   std::vector<double> w(circ_.depth + 2, 0.0);
   const int S = (int)he.glayers.size();
   for (int i = 0; i + lz < S; ++i) {
     const int t = he.glayers[i];
     int n = 0;
-    for (int g = 0; g < c; ++g) n += tc.apply[g] <= t;
+    for (int g = 0; g < c; ++g) n += flip ? tc.apply[g] < t : tc.apply[g] <= t;
     w[t] = std::ldexp(1.0, n);
   }
   return w;
@@ -478,13 +481,21 @@ std::vector<int> Engine::choose_perm(const HalfExec &he, int64_t nS, const std::
   double gpoints = 0.0;
   static const bool gather_term = !(std::getenv("QSIM_PERM_GATHER") && std::getenv("QSIM_PERM_GATHER")[0] == '0');
   if (gather_term && nS > 0 && F >= 1) {
-    lz = lazy_depth_of(hp, nS);
-    const auto &sw = hp.levels[F].sweeps;
-    if (lz >= 1 && sw.size() >= (size_t)lz) {
-      const Sweep &g = sw[sw.size() - (size_t)lz];
-      for (auto &x : g.gates) gbits.push_back(x.bit);
-      gpoints = (double)nS * (lz == 2 ? std::ldexp(1.0, (int)sw.back().gates.size()) : 1.0) *
-                std::ldexp(1.0, sbits);
+    // the lazy tail (tree_lazy_of: up to three stages, cones of cones): per leaf nS * 2^{sum k_s}
+    // reads, at the sampled indices with every lazy target bit varied; a sector serves the reads
+    // that differ only in lazy target bits below the sector size
+    std::vector<const Sweep *> all;
+    for (auto &l : hp.levels)
+      for (auto &s : l.sweeps) all.push_back(&s);
+    lz = tree_lazy_of(hp, nS);
+    if (lz >= 1 && all.size() >= (size_t)lz) {
+      int ksum = 0;
+      for (size_t s = all.size() - (size_t)lz; s < all.size(); ++s)
+        for (auto &x : all[s]->gates) {
+          ++ksum;
+          if (std::find(gbits.begin(), gbits.end(), (int)x.bit) == gbits.end()) gbits.push_back(x.bit);
+        }
+      gpoints = (double)nS * std::ldexp(1.0, ksum) * std::ldexp(1.0, sbits);
     }
   }
   const int sector_bits = c128_ ? 1 : 2;
@@ -520,7 +531,7 @@ std::vector<int> Engine::choose_perm(const HalfExec &he, int64_t nS, const std::
     if (!gbits.empty()) {
       int in_sector = 0;
       for (int b : gbits) in_sector += p[b] < sector_bits;
-      const double sectors = gpoints * std::ldexp(1.0, (int)gbits.size() - in_sector);
+      const double sectors = gpoints * std::ldexp(1.0, -in_sector);
       c += sectors * 32.0 / sweep_bytes / 4400.0;
     }
     return c;
@@ -2142,8 +2153,9 @@ void Engine::bfs_subtree(int half, int m, const void *state, void *out, const ui
 // by neighbouring targets; the C5 launch lists give ~9e10 reads/s), ~16 per compact read, against
 // 2 * 2^h * amp per sweep saved.  QSIM_OPT_LAZY_LAST: 0 off, 1 one sweep, 2 (default) up to three by
 // this model, 3 / 4 two / three whenever possible (tests).
-int Engine::tree_lazy(int half, int64_t nS) const {
-  const HalfProgram &hp = half_[half].prog;
+int Engine::tree_lazy(int half, int64_t nS) const { return tree_lazy_of(half_[half].prog, nS); }
+
+int Engine::tree_lazy_of(const HalfProgram &hp, int64_t nS) const {
   std::vector<const Sweep *> sw;
   for (auto &l : hp.levels)
     for (auto &s : l.sweeps) sw.push_back(&s);
@@ -2388,6 +2400,7 @@ void Engine::evolve_block(int half, uint64_t b0, int m, void *slice, const uint6
   const int c = (int)circ_.cuts.size();
   const int T = tile_low_bits(c128_) + kHiBits;
   if (he.prog.hl < T) throw Error(QSIM_EINVAL, "tree mode needs h >= tile bits");
+  lazy_idx_valid_ = false;  // the block's indices may have been re-uploaded since the last block
   state_bytes_ = ((size_t)1 << he.prog.hl) * amp_;
   // level-synchronous subtrees for small states (launch-bound otherwise): gather forks pinned
   if (!(bfs_ && sweep_kernel_ != 1 && state_bytes_ <= ((size_t)256 << 20))) {  // their buffers are state memory now
@@ -3013,14 +3026,24 @@ void Engine::gather_tree(const TreeVariant &v, int lz, int M, const std::vector<
   std::vector<int64_t> cnt(L);
   idx[L - 1] = dS;
   cnt[L - 1] = nS;
+  // the cone index lists depend only on the stages' target bits and the block: computed once per block
+  // (evolve_block invalidates them) and reused by every leaf
+  std::vector<uint64_t> key = {(uint64_t)(uintptr_t)dS, (uint64_t)nS, (uint64_t)L};
+  for (int s2 = L - 1; s2 >= 1; --s2)
+    for (const Gate1 &g : st[s2].first->gates) key.push_back(((uint64_t)s2 << 8) | g.bit);
+  const bool reuse = lazy_idx_valid_ && key == lazy_idx_key_;
   for (int s2 = L - 1; s2 >= 1; --s2) {
     const LazyLayer shape = lazy_layer(*st[s2].first, Diag());
     cnt[s2 - 1] = cnt[s2] << shape.k;
-    lazy_idx_[s2 - 1].reserve((size_t)cnt[s2 - 1] * 8);
-    check(launch_cone_indices(idx[s2], cnt[s2], shape, lazy_idx_[s2 - 1].as<uint64_t>(), stream_), "cone launch");
-    st_.kernel_launches++;
+    if (!reuse) {
+      lazy_idx_[s2 - 1].reserve((size_t)cnt[s2 - 1] * 8);
+      check(launch_cone_indices(idx[s2], cnt[s2], shape, lazy_idx_[s2 - 1].as<uint64_t>(), stream_), "cone launch");
+      st_.kernel_launches++;
+    }
     idx[s2 - 1] = lazy_idx_[s2 - 1].as<uint64_t>();
   }
+  lazy_idx_key_ = key;
+  lazy_idx_valid_ = true;
   for (int s2 = 0; s2 + 1 < L; ++s2) lazy_val_[s2].reserve((size_t)cnt[s2] * amp_);
   std::function<void(int, uint64_t, const void *)> stage = [&](int s2, uint64_t bits, const void *prev) {
     const Sweep &sw = *st[s2].first;

@@ -212,6 +212,7 @@ class Engine {
   // deferred-fork tree executor (non-distributed tree halves)
   void plan_levels(const HalfProgram &hp, std::vector<std::vector<std::vector<TilePlan>>> &plans, bool all_skips);
   int tree_lazy(int half, int64_t nS) const;
+  int tree_lazy_of(const HalfProgram &hp, int64_t nS) const;
   TreeChoice choose_tree(int half, int m, int lz, int64_t nS, int nbuf, bool allow_gather) const;
   TreeVariant &variant(int half, const std::vector<int> &apply, const std::vector<char> &roles);
   // canonical: P_b on the upper endpoint of every cut (the branch states of qsim_branch_state /
@@ -259,6 +260,8 @@ class Engine {
                 size_t avail);
   DevBuf rowmap_;
   DevBuf lazy_idx_[2], lazy_val_[2];  // cone index lists / stage values of the lazy tail (<= 3 stages)
+  std::vector<uint64_t> lazy_idx_key_;  // what lazy_idx_ holds (gather_tree), valid within one evolve_block
+  bool lazy_idx_valid_ = false;
   bool deferred_ = !(std::getenv("QSIM_DEFER") && std::getenv("QSIM_DEFER")[0] == '0');
   int max_ctas_ = 0;  // QSIM_OPT_MAX_CTAS (tests)
   // deferred forks on a bit the sweep targets are folded into that gate (QSIM_ABSORB=0: off, A/B)

@@ -283,21 +283,26 @@ __global__ void __launch_bounds__(256) gather_layer_compact_kernel(const typenam
                                                                    typename CxT<R>::T *__restrict__ out,
                                                                    const __grid_constant__ LazyLayer ll) {
   using C = typename CxT<R>::T;
+  // 2^min(k,5) lanes per output (as gather_layer_kernel): a stage with few targets keeps every lane busy
   const int lane = threadIdx.x & 31;
-  const int64_t j = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  if (j >= n) return;
-  const int64_t jj = ll.node_stride ? j % ll.nper : j;  // node-batched: V, out are [node][nper]
-  const int64_t jo = (ll.node_stride && ll.rowmap) ? (int64_t)ll.rowmap[j / ll.nper] * ll.nper + jj : j;
-  if ((S[jj] & ~ll.lmask) != ll.gsel) {  // another shard's index
-    if (lane == 0) out[jo].x = out[jo].y = (R)0;
-    return;
+  const int sb = ll.k < 5 ? ll.k : 5;
+  const int sub = lane & ((1 << sb) - 1);
+  const int64_t j = ((((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) << (5 - sb)) + (lane >> sb);
+  const bool valid = j < n;
+  int64_t jo = j;
+  bool own = false;
+  uint32_t x = 0;
+  if (valid) {
+    const int64_t jj = ll.node_stride ? j % ll.nper : j;  // node-batched: V, out are [node][nper]
+    if (ll.node_stride && ll.rowmap) jo = (int64_t)ll.rowmap[j / ll.nper] * ll.nper + jj;
+    own = (S[jj] & ~ll.lmask) == ll.gsel;  // else another shard's index
+    x = (uint32_t)S[jj];
   }
-  const uint32_t x = (uint32_t)S[jj];
   const uint32_t base = x & ~ll.tmask;
-  const uint32_t nterm = 1u << ll.k;
-  const C *Vj = V + ((size_t)j << ll.k);
+  const uint32_t nterm = own ? (1u << ll.k) : 0u;
+  const C *Vj = V + ((size_t)(valid ? j : 0) << ll.k);
   R sr = 0, si = 0;
-  for (uint32_t m = lane; m < nterm; m += 32) {
+  for (uint32_t m = sub; m < nterm; m += (1u << sb)) {
     uint32_t y = base;
     for (int t = 0; t < ll.k; ++t) y |= ((m >> t) & 1u) << ll.bit[t];
     C v = Vj[m];
@@ -311,12 +316,15 @@ __global__ void __launch_bounds__(256) gather_layer_compact_kernel(const typenam
     sr += v.x * wr - v.y * wi;
     si += v.x * wi + v.y * wr;
   }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
+  for (int o = (1 << sb) >> 1; o > 0; o >>= 1) {
     sr += __shfl_xor_sync(0xffffffffu, sr, o);
     si += __shfl_xor_sync(0xffffffffu, si, o);
   }
-  if (lane == 0) {
+  if (sub == 0 && valid) {
+    if (!own) {
+      out[jo].x = out[jo].y = (R)0;
+      return;
+    }
     const double pre_scale = ll.pre.active ? ll.pre.scale : 1.0;
     const int ph = diag_phase(x, ll.post, ll.post.zm);
     const double sc = ll.post.scale * pre_scale;
@@ -332,7 +340,9 @@ __global__ void __launch_bounds__(256) gather_layer_compact_kernel(const typenam
 cudaError_t launch_gather_layer_compact(const void *V, const uint64_t *S, int64_t n, void *out, const LazyLayer &ll,
                                         bool c128, cudaStream_t s) {
   if (n <= 0) return cudaSuccess;
-  const int64_t blocks = (n * 32 + 255) / 256;
+  const int sb = ll.k < 5 ? ll.k : 5;
+  const int64_t warps = (n + (32 >> sb) - 1) / (32 >> sb);
+  const int64_t blocks = (warps * 32 + 255) / 256;
   if (c128)
     gather_layer_compact_kernel<double>
         <<<(unsigned)blocks, 256, 0, s>>>((const double2 *)V, S, n, (double2 *)out, ll);
