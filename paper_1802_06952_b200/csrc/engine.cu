@@ -2449,6 +2449,7 @@ void Engine::evolve_block(int half, uint64_t b0, int m, void *slice, const uint6
       for (auto &l : fv.prog.levels) std::fprintf(stderr, " [%d:k%d s%zu]", l.fork_layer + 1, l.k, l.sweeps.size());
       std::fprintf(stderr, "\n");
     }
+    if (frames_ && run_tree_frames(half, fv, pin, m, slice, dS, nS, nbuf)) return;
     if (run_tree_flip(half, fv, lz, pin, m, slice, dS, nS, nbuf)) return;
   }
   const TreeChoice tc = choose_tree(half, m, lz, nS, nbuf, !bfs);
@@ -2920,6 +2921,193 @@ bool Engine::run_tree_flip(int half, const TreeVariant &v, int lz, const std::ve
   all0.insert(all0.end(), rest[0].begin(), rest[0].end());
   flip_exec(all0, Diag(), root, 0, hp, nullptr);
   node(0, root, false, 0);
+  return true;
+}
+
+// ---------------------------------------------------------------- Pauli frames (tree executor)
+// DESIGN.md §5 "Frames".  Every node of the block's tree is a real state (a buffer) seen through a
+// frame F = phi . X^m (program.h frame_through): a fork Z^b multiplies the frames of the children,
+// and a sweep runs ONCE on the buffer while each node's frame moves through it (F -> G F G^-1).
+// Nodes whose frame breaks at a sweep (a T phase met a gate on a flipped qubit) get a buffer of
+// their own: the sweep runs conjugated by the frame (flip_exec); nodes whose frame relative to such
+// a representative does move through the sweep share it.  The leaves are gathered through their
+// frames (x ^ m, phi).  In the App. A.1 circuits a Z inserted after the second cut period mostly
+// survives to the last layer, so a 256-branch block needs a handful of real states instead of one
+// per branch.  false: not applicable (a free projector fork, a pinned projector after a free fork).
+bool Engine::run_tree_frames(int half, const TreeVariant &v, const std::vector<int> &pin, int m, void *slice,
+                             const uint64_t *dS, int64_t nS, int nbuf) {
+  const HalfProgram &hp = v.prog;
+  const int F = (int)hp.levels.size() - 1, c = (int)circ_.cuts.size();
+  struct Step {
+    int level, s;
+    std::vector<const TilePlan *> tps;
+  };
+  std::vector<Step> steps;
+  std::vector<int> lstart(F + 1, 0);
+  bool free_seen = false;
+  for (int l = 0; l <= F; ++l) {
+    lstart[l] = (int)steps.size();
+    const Level &lev = hp.levels[l];
+    const ChildSet cs = child_set(lev, pin);
+    for (int j : cs.free)
+      if ((lev.pmask >> j) & 1u) return false;  // projector fork: no frames
+    if (l >= 1 && free_seen && pinned_diag(lev, pin).pm && !lev.sweeps.empty()) return false;
+    if (!cs.free.empty()) free_seen = true;
+    if (v.plans[l].empty()) return false;
+    const auto &launches = v.plans[l][0];
+    for (size_t s = 0; s < lev.sweeps.size(); ++s) {
+      Step st;
+      st.level = l;
+      st.s = (int)s;
+      for (const TilePlan &tp : launches) {
+        if (!tp.swaps.empty()) return false;
+        if (tp.sweep == (int)s) st.tps.push_back(&tp);
+      }
+      if (st.tps.empty()) return false;
+      steps.push_back(st);
+    }
+  }
+  const int nsteps = (int)steps.size();
+  struct FNode {
+    Diag phi;
+    uint64_t m = 0;
+    uint64_t bits = 0;
+    bool ident = true;
+  };
+  std::vector<int> freebuf;
+  const int extra = std::max(0, std::min(nbuf - 1, flip_max_nb_ >= 0 ? flip_max_nb_ : 64));
+  ensure_states(half, 1 + extra);
+  for (int i = extra; i >= 1; --i) freebuf.push_back(i);
+  const uint64_t rmask = m >= 64 ? ~0ull : ((1ull << m) - 1ull);
+  const bool dbg = std::getenv("QSIM_DEBUG_TREE") != nullptr;
+  int nreal = 1;
+  std::function<void(int, int, std::vector<FNode>, bool, Diag)> process = [&](int pos, int raw, std::vector<FNode> nodes,
+                                                                               bool keepRaw, Diag pend) {
+    std::vector<Executed> rec;  // in-place sweeps on raw, undone at the end when the caller keeps raw
+    for (;; ++pos) {
+      for (int l = 1; l <= F; ++l) {
+        if (lstart[l] != pos) continue;
+        const Level &lev = hp.levels[l];
+        const ChildSet cs = child_set(lev, pin);
+        const Diag pd = pinned_diag(lev, pin);
+        if (!pd.identity()) {
+          if (nodes.size() == 1 && nodes[0].ident && pos < nsteps) {
+            pend = Diag::merge(pend, pd);  // the real sweep applies it (the root path)
+          } else {
+            for (FNode &n : nodes) n.phi = Diag::merge(pd, n.phi), n.ident = false;
+          }
+        }
+        for (FNode &n : nodes) n.bits |= branch_bits(lev, cs.base, c);
+        if (cs.free.empty()) continue;
+        std::vector<FNode> out;
+        out.reserve(nodes.size() << cs.free.size());
+        for (const FNode &n : nodes)
+          for (uint64_t f = 0; f < (1ull << cs.free.size()); ++f) {
+            FNode x = n;
+            Diag z;
+            for (size_t t = 0; t < cs.free.size(); ++t)
+              if ((f >> t) & 1u) z.add_Z(lev.cut_bits[cs.free[t]]);
+            if (f) {
+              x.phi = Diag::merge(z, x.phi);
+              x.ident = false;
+            }
+            x.bits |= branch_bits(lev, child_of(lev, cs, f), c) & ~branch_bits(lev, cs.base, c);
+            out.push_back(x);
+          }
+        nodes.swap(out);
+      }
+      if (pos == nsteps) break;
+      const Step &st = steps[pos];
+      const Sweep &sw = hp.levels[st.level].sweeps[st.s];
+      std::vector<FNode> surv, fail;
+      for (FNode &n : nodes) {
+        if (n.ident || frame_through(sw, n.phi, n.m))
+          surv.push_back(n);
+        else
+          fail.push_back(n);
+      }
+      // classes of the breaking nodes: a member's frame relative to the representative moves through
+      struct Cls {
+        FNode rep;
+        std::vector<FNode> mem;  // phi / m relative to the representative's result
+      };
+      std::vector<Cls> cls;
+      for (const FNode &n : fail) {
+        bool placed = false;
+        for (Cls &k : cls) {
+          Diag ri, rp;
+          uint64_t rm;
+          frame_inverse(k.rep.phi, k.rep.m, ri);
+          frame_compose(n.phi, n.m, ri, k.rep.m, rp, rm);
+          if (frame_through(sw, rp, rm)) {
+            FNode x = n;
+            x.phi = rp;
+            x.m = rm;
+            k.mem.push_back(x);
+            placed = true;
+            break;
+          }
+        }
+        if (!placed) cls.push_back(Cls{n, {}});
+      }
+      for (size_t ci = 0; ci < cls.size(); ++ci) {
+        const Cls &k = cls[ci];
+        const bool last = ci + 1 == cls.size() && surv.empty() && !keepRaw;
+        int dst = raw;
+        bool dnew = false, dip = false;
+        if (!last) {
+          if (!freebuf.empty())
+            dst = freebuf.back(), freebuf.pop_back(), dnew = true;
+          else
+            dip = true;
+        }
+        std::vector<Executed> rd;
+        VState V;
+        V.buf = raw;
+        V.m = k.rep.m;
+        V.phi = k.rep.phi;
+        V.has_phi = true;
+        flip_exec(st.tps, Diag(), V, dst, hp, dip ? &rd : nullptr);
+        ++nreal;
+        // nodes on dst: the representative is X^{m_rep} dst, a member R' X^{m_rep} dst
+        std::vector<FNode> nn;
+        FNode r = k.rep;
+        r.phi = Diag();
+        r.ident = k.rep.m == 0;
+        nn.push_back(r);
+        for (const FNode &x : k.mem) {
+          FNode y = x;
+          frame_compose(x.phi, x.m, Diag(), k.rep.m, y.phi, y.m);
+          y.ident = false;
+          nn.push_back(y);
+        }
+        process(pos + 1, dst, nn, dip, Diag());
+        if (dip) flip_undo(rd, dst, hp);
+        if (dnew) freebuf.push_back(dst);
+      }
+      if (surv.empty()) {
+        nodes.clear();
+        break;
+      }
+      VState V;
+      V.buf = raw;
+      flip_exec(st.tps, pend, V, raw, hp, keepRaw ? &rec : nullptr);
+      pend = Diag();
+      nodes.swap(surv);
+    }
+    for (const FNode &n : nodes) {
+      if (!n.ident) st_.flip_siblings++;
+      char *row = (char *)slice + (size_t)(n.bits & rmask) * (size_t)nS * amp_;
+      check(launch_gather(states_[raw]->ptr, dS, nS, row, to_dev(n.phi), c128_, stream_, ~0ull, 0, n.m),
+            "gather launch");
+      st_.kernel_launches++;
+    }
+    if (keepRaw) flip_undo(rec, raw, hp);
+  };
+  FNode root;
+  process(0, 0, std::vector<FNode>{root}, false, Diag());
+  if (dbg) std::fprintf(stderr, "frames half %d m=%d: %d real states, %d steps, %d extra buffers\n", half, m, nreal,
+                        nsteps, extra);
   return true;
 }
 

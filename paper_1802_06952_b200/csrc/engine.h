@@ -236,6 +236,9 @@ class Engine {
     Diag pre, post;
   };
   bool flip_half(int half) const;
+  bool run_tree_frames(int half, const TreeVariant &v, const std::vector<int> &pin, int m, void *slice,
+                       const uint64_t *dS, int64_t nS, int nbuf);
+  bool frames_ = !(std::getenv("QSIM_FRAMES") && std::getenv("QSIM_FRAMES")[0] == '0');
   TreeChoice flip_choice(int half, int m) const;
   bool run_tree_flip(int half, const TreeVariant &v, int lz, const std::vector<int> &pin, int m, void *slice,
                      const uint64_t *dS, int64_t nS, int nbuf);

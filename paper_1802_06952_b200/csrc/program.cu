@@ -110,16 +110,15 @@ Diag Diag::shift(uint64_t m) const {
   Diag r = *this;
   if (!m) return r;
   r.pv = (pv ^ (m & pm)) & pm;
-  for (int a = 0; a < 64; ++a) {
-    if (!((m >> a) & 1u)) continue;
+  for (uint64_t rest = m; rest; rest &= rest - 1) {
+    const int a = __builtin_ctzll(rest);
     const int c = count(a);
     r.ph0 = (r.ph0 + c) & 7;
     r.set_count(a, (8 - c) & 7);
   }
   for (int d = 1; d < 64; ++d) {
-    if (!cz[d]) continue;
-    for (int a = 0; a + d < 64; ++a) {
-      if (!((cz[d] >> a) & 1u)) continue;
+    for (uint64_t rest = cz[d]; rest; rest &= rest - 1) {
+      const int a = __builtin_ctzll(rest);
       const int b = a + d;
       const bool fa = (m >> a) & 1u, fb = (m >> b) & 1u;
       if (fa) r.set_count(b, r.count(b) + 4);
@@ -149,6 +148,64 @@ Diag Diag::phase_only() const {
   r.allzero = false;
   return r;
 }
+
+// ---------------------------------------------------------------- Pauli frames (program.h)
+static bool cz_touches(const Diag &d, int t) {
+  for (int k = 1; k < 64; ++k) {
+    if (!d.cz[k]) continue;
+    if ((d.cz[k] >> t) & 1u) return true;
+    if (t >= k && ((d.cz[k] >> (t - k)) & 1u)) return true;
+  }
+  return false;
+}
+
+// phi * D / D^m (phases only; a projector of D must not meet m)
+static bool frame_ratio(Diag &phi, const Diag &D, uint64_t m) {
+  if (!m) return true;
+  if (D.pm & m) return false;
+  const Diag p = D.phase_only();
+  phi = Diag::merge(phi, Diag::merge(p, p.shift(m).inverse()));
+  return true;
+}
+
+bool frame_through(const Sweep &sw, Diag &phi0, uint64_t &m0) {
+  Diag phi = phi0;
+  uint64_t m = m0;
+  if (sw.gen) return false;
+  if (!frame_ratio(phi, sw.pre, m)) return false;
+  for (const Gate1 &g : sw.gates) {
+    const int t = g.bit;
+    if ((phi.pm >> t) & 1u) return false;
+    const int c = phi.count(t);
+    if ((c & 3) || cz_touches(phi, t)) return false;
+    // D X^f with D = diag(1, w^c) on t, conjugated by I - iX (kind 1) / I - iY (kind 2):
+    // I - iX: X -> X, Z -> -Y = w^2 Z X, Z X (= iY) -> iZ = w^2 Z
+    // I - iY: X -> -Z = w^4 Z, Z -> X, Z X -> Z X
+    const int f = (int)((m >> t) & 1u), z = c >> 2;
+    int nf = f, nz = z, ph = 0;
+    if (g.kind == 1) {
+      if (!f && z) nf = 1, nz = 1, ph = 2;
+      else if (f && z) nf = 0, nz = 1, ph = 2;
+    } else {
+      if (f && !z) nf = 0, nz = 1, ph = 4;
+      else if (!f && z) nf = 1, nz = 0;
+    }
+    phi.set_count(t, 4 * nz);
+    phi.ph0 = (phi.ph0 + ph) & 7;
+    m = (m & ~(1ull << t)) | ((uint64_t)nf << t);
+  }
+  if (!frame_ratio(phi, sw.post, m)) return false;
+  phi0 = phi;
+  m0 = m;
+  return true;
+}
+
+void frame_compose(const Diag &phi2, uint64_t m2, const Diag &phi1, uint64_t m1, Diag &phi, uint64_t &m) {
+  phi = Diag::merge(phi2, phi1.shift(m2));
+  m = m1 ^ m2;
+}
+
+void frame_inverse(const Diag &phi, uint64_t m, Diag &inv_phi) { inv_phi = phi.inverse().shift(m); }
 
 Diag HalfProgram::fork_diag(int level, uint64_t child) const {
   Diag d;

@@ -159,6 +159,19 @@ std::vector<PartCut> half_cuts(const Circuit &c, bool upper, const std::vector<c
 // Layers in [1, depth] holding at least one X^1/2 / Y^1/2 gate on a qubit in [lo, hi).
 std::vector<int> gate_layers(const Circuit &c, uint32_t lo, uint32_t hi);
 
+// ---- Pauli frames of the branch tree (DESIGN.md §5 "Frames").  A frame F = phi . X^m (X^m: flip
+// of the bits in m, then the diagonal phi) relates a branch state to another one: psi_b = F psi_a.
+// A fork Z^b is a frame; it moves through a sweep G = post . gates . pre as G F G^-1 = F' while
+// every target t of G sees F as I or Z (phi's count at t in {0, 4}, no CZ term on t): the factored
+// gates I - iX, I - iY are Clifford, and diagonals conjugate a flip into a flip times a ratio
+// D / D^m.  frame_through replaces (phi, m) by F' and returns true, or returns false (F unchanged)
+// where the frame breaks: from there the two states need sweeps of their own.
+bool frame_through(const Sweep &sw, Diag &phi, uint64_t &m);
+// F2 . F1 (apply F1 first): phi2 . phi1^{m2} . X^{m1 ^ m2}
+void frame_compose(const Diag &phi2, uint64_t m2, const Diag &phi1, uint64_t m1, Diag &phi, uint64_t &m);
+// F^-1 = (1 / phi)^m . X^m
+void frame_inverse(const Diag &phi, uint64_t m, Diag &inv_phi);
+
 // perm: physical bit of each canonical local bit (identity when empty); every bit position of the
 // program (gates, diagonals, forks) is physical.
 HalfProgram compile_half(const Circuit &c, bool upper, const std::vector<int> &perm = {});

@@ -105,11 +105,14 @@ def test_d22_h14_forks(prec, defer, bfs, lazy, d22_h14):
 @pytest.mark.parametrize("prec", PRECS, ids=PNAME.get)
 @pytest.mark.parametrize("nb", [0, 1, 2, -1])
 @pytest.mark.parametrize("lazy", [0, 2, 4])
-def test_d22_h14_sibling_flips(prec, nb, lazy, d22_h14):
-    """Sibling flips: children of a Z^b fork read as child 0 through a bit flip and a
-    diagonal, Z^b on both endpoints of the free cuts with the lower rows Walsh-Hadamard transformed
-    (R-zz), and with 0 / 1 / 2 extra buffers the states overwritten in place restored by inverse
-    sweeps (QSIM_OPT_FLIP_NB).  Every ragged range against the oracle's sum of outer products."""
+@pytest.mark.parametrize("frames", [0, 1])
+def test_d22_h14_sibling_flips(prec, nb, lazy, frames, d22_h14, monkeypatch):
+    """Sibling flips and Pauli frames: children of a Z^b fork read as child 0 through
+    a bit flip and a diagonal (frames=0: for one sweep; frames=1: for as long as the frame moves
+    through the sweeps), Z^b on both endpoints of the free cuts with the lower rows Walsh-Hadamard
+    transformed (R-zz), and with 0 / 1 / 2 extra buffers the states overwritten in place restored by
+    inverse sweeps (QSIM_OPT_FLIP_NB).  Every ragged range against the oracle's sum of outer products."""
+    monkeypatch.setenv("QSIM_FRAMES", str(frames))
     circ, Su, Sl, ranges, ref = d22_h14
     ctx = make_ctx(prec, circ, {Q.QSIM_OPT_BFS: 0, Q.QSIM_OPT_FLIP: 1, Q.QSIM_OPT_FLIP_NB: nb,
                                 Q.QSIM_OPT_LAZY_LAST: lazy})
@@ -124,7 +127,7 @@ def test_d22_h14_sibling_flips(prec, nb, lazy, d22_h14):
         Q.qsim_destroy(ctx)
     assert_close(A, ref, prec, f"d22 h14 flips nb={nb} lazy={lazy}")
     assert st["flip_siblings"] > 0
-    if nb == 0:
+    if nb == 0 and not frames:
         assert st["undo_sweeps"] > 0
 
 
