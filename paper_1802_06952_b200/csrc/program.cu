@@ -207,6 +207,112 @@ void frame_compose(const Diag &phi2, uint64_t m2, const Diag &phi1, uint64_t m1,
 
 void frame_inverse(const Diag &phi, uint64_t m, Diag &inv_phi) { inv_phi = phi.inverse().shift(m); }
 
+// ---------------------------------------------------------------- linear frames (program.h)
+void LinFrame::add_counts(uint64_t b1, uint64_t b2, uint64_t b4) {
+  const uint64_t s0 = t1 ^ b1, c0 = t1 & b1;
+  const uint64_t s1 = t2 ^ b2 ^ c0, c1 = (t2 & b2) | (c0 & (t2 ^ b2));
+  t1 = s0;
+  t2 = s1;
+  zm = zm ^ b4 ^ c1;
+}
+
+void LinFrame::negate(uint64_t mask) {  // -c = ~c + 1 (mod 8)
+  t1 ^= mask;
+  t2 ^= mask;
+  zm ^= mask;
+  add_counts(mask, 0, 0);
+}
+
+LinFrame LinFrame::shift(uint64_t s) const {
+  LinFrame r = *this;
+  if (!s) return r;
+  r.ph0 = (ph0 + __builtin_popcountll(s & t1) + 2 * __builtin_popcountll(s & t2) + 4 * __builtin_popcountll(s & zm)) & 7;
+  r.negate(s);
+  return r;
+}
+
+Diag LinFrame::diag() const {
+  Diag d;
+  d.t1 = t1;
+  d.t2 = t2;
+  d.zm = zm;
+  d.ph0 = ph0 & 7;
+  return d;
+}
+
+// phi * D / D^m, D a program diagonal (phases; a projector must not meet m)
+static bool lin_ratio(LinFrame &f, const Diag &D) {
+  const uint64_t m = f.m;
+  if (!m) return true;
+  if (D.pm & m) return false;
+  // bits a in m: weight 2 c_a(D), ph0 -= c_a(D)
+  uint64_t b2 = 0, b4 = 0;
+  int ph = 0;
+  for (uint64_t r = m & (D.t1 | D.t2 | D.zm); r; r &= r - 1) {
+    const int a = __builtin_ctzll(r), ca = D.count(a);
+    ph -= ca;
+    if (ca & 1) b2 ^= 1ull << a;  // 2 c_a mod 8: bit plane 2 gets c_a bit 0, plane 4 gets c_a bit 1
+    if (ca & 2) b4 ^= 1ull << a;
+  }
+  uint64_t z4 = 0;
+  for (int d = 1; d < 64; ++d)
+    for (uint64_t r = D.cz[d]; r; r &= r - 1) {
+      const int a = __builtin_ctzll(r), b = a + d;
+      const bool fa = (m >> a) & 1u, fb = (m >> b) & 1u;
+      if (fa) z4 ^= 1ull << b;
+      if (fb) z4 ^= 1ull << a;
+      if (fa && fb) ph += 4;
+    }
+  f.add_counts(0, b2, b4);
+  f.add_counts(0, 0, z4);
+  f.ph0 = ((f.ph0 + ph) % 8 + 8) % 8;
+  return true;
+}
+
+bool lin_through(const Sweep &sw, LinFrame &f0) {
+  if (sw.gen) return false;
+  LinFrame f = f0;
+  if (!lin_ratio(f, sw.pre)) return false;
+  for (const Gate1 &g : sw.gates) {
+    const int t = g.bit;
+    const int c = f.count(t);
+    if (c & 3) return false;
+    const int fl = (int)((f.m >> t) & 1u), z = c >> 2;
+    int nf = fl, nz = z, ph = 0;
+    if (g.kind == 1) {  // I - iX: X -> X, Z -> w^2 Z X, Z X -> w^2 Z
+      if (!fl && z) nf = 1, nz = 1, ph = 2;
+      else if (fl && z) nf = 0, nz = 1, ph = 2;
+    } else {  // I - iY: X -> w^4 Z, Z -> X, Z X -> Z X
+      if (fl && !z) nf = 0, nz = 1, ph = 4;
+      else if (!fl && z) nf = 1, nz = 0;
+    }
+    const uint64_t bit = 1ull << t;
+    f.zm = nz ? (f.zm | bit) : (f.zm & ~bit);
+    f.ph0 = (f.ph0 + ph) & 7;
+    f.m = nf ? (f.m | bit) : (f.m & ~bit);
+  }
+  if (!lin_ratio(f, sw.post)) return false;
+  f0 = f;
+  return true;
+}
+
+LinFrame lin_compose(const LinFrame &f2, const LinFrame &f1) {
+  LinFrame r = f1.shift(f2.m);
+  r.add_counts(f2.t1, f2.t2, f2.zm);
+  r.ph0 = (r.ph0 + f2.ph0) & 7;
+  r.m = f1.m ^ f2.m;
+  return r;
+}
+
+LinFrame lin_inverse(const LinFrame &f) {
+  LinFrame r = f;
+  r.negate(~0ull);
+  r.ph0 = (8 - f.ph0) & 7;
+  r = r.shift(f.m);
+  r.m = f.m;
+  return r;
+}
+
 Diag HalfProgram::fork_diag(int level, uint64_t child) const {
   Diag d;
   if (level <= 0) return d;

@@ -172,6 +172,24 @@ void frame_compose(const Diag &phi2, uint64_t m2, const Diag &phi1, uint64_t m1,
 // F^-1 = (1 / phi)^m . X^m
 void frame_inverse(const Diag &phi, uint64_t m, Diag &inv_phi);
 
+// The frames of Z^b forks stay linear (D / D^m of a quadratic D is linear): phi(x) = w^{ph0 + sum_a
+// c_a x_a} with the counts c_a = t1_a + 2 t2_a + 4 zm_a held as bit planes, so that moving, composing
+// and inverting a frame are a few word operations (the executor keeps one frame per tree node).
+struct LinFrame {
+  uint64_t t1 = 0, t2 = 0, zm = 0, m = 0;
+  int ph0 = 0;
+  bool identity() const { return !t1 && !t2 && !zm && !m && ph0 == 0; }
+  int count(int a) const { return (int)((t1 >> a) & 1u) + 2 * (int)((t2 >> a) & 1u) + 4 * (int)((zm >> a) & 1u); }
+  void add_counts(uint64_t b1, uint64_t b2, uint64_t b4);  // c_a += b1_a + 2 b2_a + 4 b4_a (mod 8)
+  void negate(uint64_t mask);                              // c_a = -c_a on the bits of mask
+  void add_Z(int a) { zm ^= 1ull << a; }
+  LinFrame shift(uint64_t s) const;                        // phi^s (x -> x ^ s), flip unchanged
+  Diag diag() const;                                       // phi as a Diag
+};
+bool lin_through(const Sweep &sw, LinFrame &f);
+LinFrame lin_compose(const LinFrame &f2, const LinFrame &f1);  // f2 . f1
+LinFrame lin_inverse(const LinFrame &f);
+
 // perm: physical bit of each canonical local bit (identity when empty); every bit position of the
 // program (gates, diagonals, forks) is physical.
 HalfProgram compile_half(const Circuit &c, bool upper, const std::vector<int> &perm = {});
