@@ -55,6 +55,9 @@ def parse():
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=None)
+    ap.add_argument("--step", default="job", choices=["job", "group"],
+                    help="job: one step = the whole job (every branch; ranks split the branch range); "
+                         "group: one step = one first-period prefix group per rank (round-1 definition)")
     return ap.parse_args()
 
 
@@ -258,7 +261,7 @@ def run_reference(args):
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_steps / args.steps * 1e3,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
         "config": {"workload": f"{args.config} (oracle: flat partitioned simulator, complex128, "
                                f"{oc.cores} host threads)",
@@ -338,15 +341,21 @@ def main():
         if world > 1:
             Q.qsim_comm_init(ctx, rank, world, uid)
         c, B, cuts = Q.qsim_partition(ctx)
-        G = 1 << first_period_bits(cuts)
-        per_group = B // G
+        if args.step == "job":  # the whole job per step: this rank's prefix-aligned branch range
+            G = 1
+            per_group = B
+            rb0, rb1 = Q.qsim_rank_range(ctx) if world > 1 else (0, B)
+            range_of = lambda step: (rb0, rb1)
+        else:
+            G = 1 << first_period_bits(cuts)
+            per_group = B // G
+            group_of = lambda step: (step * world + rank) % G
+            range_of = lambda step: (group_of(step) * per_group, (group_of(step) + 1) * per_group)
         Q.qsim_set_blocks(ctx, hSu, hSl)
-        group_of = lambda step: (step * world + rank) % G
 
         def step_device(s):
-            g = group_of(s)
             Q.qsim_reset_block(ctx)
-            Q.qsim_evolve_range(ctx, g * per_group, (g + 1) * per_group)
+            Q.qsim_evolve_range(ctx, *range_of(s))
             Q.qsim_sample(ctx, 1000 + s, N_DRAWS, to_host=False)
 
         for s in range(warmup):
@@ -366,9 +375,10 @@ def main():
         clk = clocks.stop() if clocks else None
         t_dev = max_over_ranks(ev0.elapsed_time(ev1) / 1e3)
         st = Q.qsim_stats(ctx)
+        jobs = steps if args.step == "job" else world * steps / G  # jobs completed in the timed region
         out = {"c": c, "B": B, "G": G, "per_group": per_group, "t_dev": t_dev, "clocks": clk,
                "launches": int(sum_over_ranks(st["kernel_launches"])),
-               "value": (n_u * n_l) * world * steps / G / t_dev}
+               "value": (n_u * n_l) * jobs / t_dev}
         if full:
             # profiling step: CUDA events around every sweep / GEMM launch on the launching stream
             Q.qsim_set_option(ctx, Q.QSIM_OPT_TIME_SWEEPS, 1)
@@ -387,14 +397,14 @@ def main():
             barrier()
             t0 = time.perf_counter()
             for s in range(k_e2e):  # 0 steps: e2e skipped (profiling runs)
-                g = group_of(warmup + s)
                 Q.qsim_set_blocks(ctx, hSu, hSl)                                        # H2D of the inputs
-                Q.qsim_evolve_range(ctx, g * per_group, (g + 1) * per_group)
+                Q.qsim_evolve_range(ctx, *range_of(warmup + s))
                 Q.qsim_amplitudes(ctx, hSu, hSl, out=hA, write=(rank == 0))            # D2H of the block
                 Q.qsim_sample(ctx, 2000 + s, N_DRAWS, to_host=(rank == 0), out=hX)     # D2H of the draws
             barrier()
             t_e2e = max_over_ranks(time.perf_counter() - t0)
-            out["e2e"] = (n_u * n_l) * world * k_e2e / G / t_e2e if k_e2e else None
+            jobs_e2e = k_e2e if args.step == "job" else world * k_e2e / G
+            out["e2e"] = (n_u * n_l) * jobs_e2e / t_e2e if k_e2e else None
             out["e2e_steps"] = k_e2e
             del hA
         Q.qsim_destroy(ctx)
@@ -469,7 +479,7 @@ def main():
         line = {
             "metric": METRIC, "value": main_run["value"], "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_dev / args.steps * 1e3,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "higher_is_better": True, "scaling": "strong" if args.step == "job" else "weak", "vs_baseline": None,
             "dtype": "f32" if prec == Q.QSIM_C64 else "f64", "data": "synthetic",
             "config": {
                 "workload": f"{args.config}: {circ.n}q {circ.rows}x{circ.cols} grid depth {circ.depth} random "
@@ -477,9 +487,13 @@ def main():
                             f"sampled block {n_u} x {n_l}",
                 "precision": f"{args.precision} ({'f32' if prec == Q.QSIM_C64 else 'f64'} half-state sweeps, "
                              "f64 reconstruction GEMM)",
-                "step": f"1 of {G} first-period prefix groups ({per_group} branches) per rank: both half "
-                        f"trees from layer 1 (deferred forks), gathers, GEMM-accumulate, |a|^2 + {N_DRAWS} draws",
-                "projected_full_job_s": t_dev / args.steps * G / world,
+                "step": (f"the whole job: all {B} branches (split over {world} rank(s) by prefix-aligned "
+                         f"ranges), both half trees from layer 1 (deferred forks, Pauli frames), leaf "
+                         f"gathers, GEMM-accumulate, block reduction, |a|^2 + {N_DRAWS} draws")
+                        if args.step == "job" else
+                        (f"1 of {G} first-period prefix groups ({per_group} branches) per rank: both half "
+                         f"trees from layer 1 (deferred forks), gathers, GEMM-accumulate, |a|^2 + {N_DRAWS} draws"),
+                "projected_full_job_s": t_dev / args.steps * (1 if args.step == "job" else G / world),
                 "l2": f"inputs larger than L2: half states of {((1 << circ.h_upper) * amp_bytes) >> 20} MiB",
                 "parallelism": f"branch-sharded dp{world}",
             },

@@ -1421,6 +1421,28 @@ void Engine::evolve_range(uint64_t b0, uint64_t b1) {
   // slices for a chunk of branches (bounded at 1 GiB per half)
   const uint64_t per_branch = (uint64_t)std::max(nu, nl) * amp_;
   uint64_t chunk = std::max<uint64_t>(1, ((uint64_t)1 << 30) / per_branch);
+  if (frames_ && (flip_half(0) || flip_half(1))) {
+    // Pauli frames share real states across every branch of a block, so one block should span the
+    // range: slices as large as the memory left beside two state buffers of the larger half allows
+    size_t free_b = 0, total_b = 0;
+    check(cudaMemGetInfo(&free_b, &total_b), "cudaMemGetInfo");
+    size_t have = U_.bytes + L_.bytes;
+    for (auto *b : states_) have += b->bytes;
+    const size_t st = ((size_t)1 << std::max(half_[0].prog.hl, half_[1].prog.hl)) * amp_;
+    const size_t reserve = 2 * st + ((size_t)3 << 30);
+    const size_t room = free_b + have > reserve ? free_b + have - reserve : 0;
+    const uint64_t both = (uint64_t)(nu + nl) * amp_;
+    const uint64_t fit = room / both;
+    if (fit > chunk) {
+      chunk = fit;
+      const uint64_t want = std::min<uint64_t>(chunk, b1 - b0) * both;
+      if (U_.bytes + L_.bytes < want) {  // the state buffers are re-reserved by the executor
+        for (auto *b : states_) b->release();
+        U_.release();
+        L_.release();
+      }
+    }
+  }
   // align the chunk to a power of two so that chunks are whole subtrees
   uint64_t p2 = 1;
   while (p2 * 2 <= chunk) p2 *= 2;
@@ -2969,21 +2991,26 @@ bool Engine::run_tree_frames(int half, const TreeVariant &v, const std::vector<i
   }
   const int nsteps = (int)steps.size();
   struct FNode {
-    Diag phi;
-    uint64_t m = 0;
+    LinFrame f;
     uint64_t bits = 0;
-    bool ident = true;
   };
   std::vector<int> freebuf;
   const int extra = std::max(0, std::min(nbuf - 1, flip_max_nb_ >= 0 ? flip_max_nb_ : 64));
   ensure_states(half, 1 + extra);
   for (int i = extra; i >= 1; --i) freebuf.push_back(i);
   const uint64_t rmask = m >= 64 ? ~0ull : ((1ull << m) - 1ull);
-  const bool dbg = std::getenv("QSIM_DEBUG_TREE") != nullptr;
-  int nreal = 1;
-  std::function<void(int, int, std::vector<FNode>, bool, Diag)> process = [&](int pos, int raw, std::vector<FNode> nodes,
-                                                                               bool keepRaw, Diag pend) {
+  int nreal = 1, nsw = 0;
+  auto lin_of = [](const Diag &d, LinFrame &f) {  // f = d . f for a linear diagonal d
+    if (d.pm || d.allzero || d.has_cz() || d.nhalf) return false;
+    f.add_counts(d.t1, d.t2, d.zm);
+    f.ph0 = (f.ph0 + d.ph0) & 7;
+    return true;
+  };
+  std::function<void(int, int, std::vector<FNode> &, bool, Diag)> process = [&](int pos, int raw,
+                                                                                std::vector<FNode> &nodes,
+                                                                                bool keepRaw, Diag pin_pre) {
     std::vector<Executed> rec;  // in-place sweeps on raw, undone at the end when the caller keeps raw
+    Diag tail;  // fixed forks after the last sweep that are no linear frame (a projector): common to the leaves
     for (;; ++pos) {
       for (int l = 1; l <= F; ++l) {
         if (lstart[l] != pos) continue;
@@ -2991,27 +3018,28 @@ bool Engine::run_tree_frames(int half, const TreeVariant &v, const std::vector<i
         const ChildSet cs = child_set(lev, pin);
         const Diag pd = pinned_diag(lev, pin);
         if (!pd.identity()) {
-          if (nodes.size() == 1 && nodes[0].ident && pos < nsteps) {
-            pend = Diag::merge(pend, pd);  // the real sweep applies it (the root path)
+          if (nodes.size() == 1 && nodes[0].f.identity() && pos < nsteps) {
+            pin_pre = Diag::merge(pin_pre, pd);  // the real sweep applies it (the root path)
           } else {
-            for (FNode &n : nodes) n.phi = Diag::merge(pd, n.phi), n.ident = false;
+            bool lin = true;
+            for (FNode &n : nodes) lin = lin_of(pd, n.f) && lin;
+            if (!lin) {
+              if (pos < nsteps) throw Error(QSIM_EINVAL, "internal: projector fork inside a frame tree");
+              tail = Diag::merge(tail, pd);  // after the last sweep: a common factor of the leaves
+            }
           }
         }
-        for (FNode &n : nodes) n.bits |= branch_bits(lev, cs.base, c);
+        const uint64_t bb = branch_bits(lev, cs.base, c);
+        for (FNode &n : nodes) n.bits |= bb;
         if (cs.free.empty()) continue;
         std::vector<FNode> out;
         out.reserve(nodes.size() << cs.free.size());
         for (const FNode &n : nodes)
           for (uint64_t f = 0; f < (1ull << cs.free.size()); ++f) {
             FNode x = n;
-            Diag z;
             for (size_t t = 0; t < cs.free.size(); ++t)
-              if ((f >> t) & 1u) z.add_Z(lev.cut_bits[cs.free[t]]);
-            if (f) {
-              x.phi = Diag::merge(z, x.phi);
-              x.ident = false;
-            }
-            x.bits |= branch_bits(lev, child_of(lev, cs, f), c) & ~branch_bits(lev, cs.base, c);
+              if ((f >> t) & 1u) x.f.add_Z(lev.cut_bits[cs.free[t]]);
+            x.bits |= branch_bits(lev, child_of(lev, cs, f), c) & ~bb;
             out.push_back(x);
           }
         nodes.swap(out);
@@ -3020,29 +3048,28 @@ bool Engine::run_tree_frames(int half, const TreeVariant &v, const std::vector<i
       const Step &st = steps[pos];
       const Sweep &sw = hp.levels[st.level].sweeps[st.s];
       std::vector<FNode> surv, fail;
+      surv.reserve(nodes.size());
       for (FNode &n : nodes) {
-        if (n.ident || frame_through(sw, n.phi, n.m))
+        if (n.f.identity() || lin_through(sw, n.f))
           surv.push_back(n);
         else
           fail.push_back(n);
       }
+      nodes.clear();
+      nodes.shrink_to_fit();
       // classes of the breaking nodes: a member's frame relative to the representative moves through
       struct Cls {
         FNode rep;
-        std::vector<FNode> mem;  // phi / m relative to the representative's result
+        std::vector<FNode> mem;  // frames relative to the representative, moved through the sweep
       };
       std::vector<Cls> cls;
       for (const FNode &n : fail) {
         bool placed = false;
         for (Cls &k : cls) {
-          Diag ri, rp;
-          uint64_t rm;
-          frame_inverse(k.rep.phi, k.rep.m, ri);
-          frame_compose(n.phi, n.m, ri, k.rep.m, rp, rm);
-          if (frame_through(sw, rp, rm)) {
+          LinFrame rel = lin_compose(n.f, lin_inverse(k.rep.f));
+          if (lin_through(sw, rel)) {
             FNode x = n;
-            x.phi = rp;
-            x.m = rm;
+            x.f = rel;
             k.mem.push_back(x);
             placed = true;
             break;
@@ -3050,9 +3077,48 @@ bool Engine::run_tree_frames(int half, const TreeVariant &v, const std::vector<i
         }
         if (!placed) cls.push_back(Cls{n, {}});
       }
-      for (size_t ci = 0; ci < cls.size(); ++ci) {
-        const Cls &k = cls[ci];
-        const bool last = ci + 1 == cls.size() && surv.empty() && !keepRaw;
+      fail.clear();
+      if (cls.empty()) {  // every frame moved through: one sweep for all nodes
+        VState V;
+        V.buf = raw;
+        flip_exec(st.tps, pin_pre, V, raw, hp, keepRaw ? &rec : nullptr);
+        ++nsw;
+        pin_pre = Diag();
+        nodes.swap(surv);
+        continue;
+      }
+      // a split: the survivors and every class run the sweep from raw, each into a state of its own.
+      // Smaller groups first, into free buffers (else in place, undone afterwards); the largest group
+      // (the most splits still to come) last, in place, with the buffers free again for its splits.
+      struct Group {
+        bool surv;
+        LinFrame rep;
+        std::vector<FNode> nodes;
+      };
+      std::vector<Group> groups;
+      if (!surv.empty()) groups.push_back(Group{true, LinFrame(), std::move(surv)});
+      for (Cls &k : cls) {
+        Group g{false, k.rep.f, {}};
+        LinFrame flip;
+        flip.m = k.rep.f.m;
+        g.nodes.reserve(1 + k.mem.size());
+        FNode r = k.rep;
+        r.f = flip;  // on its new state the representative is X^{m_rep} dst, a member R' X^{m_rep} dst
+        g.nodes.push_back(r);
+        for (const FNode &x : k.mem) {
+          FNode y = x;
+          y.f = lin_compose(x.f, flip);
+          g.nodes.push_back(y);
+        }
+        k.mem.clear();
+        groups.push_back(std::move(g));
+      }
+      cls.clear();
+      std::stable_sort(groups.begin(), groups.end(),
+                       [](const Group &a, const Group &b) { return a.nodes.size() < b.nodes.size(); });
+      for (size_t gi = 0; gi < groups.size(); ++gi) {
+        Group &g = groups[gi];
+        const bool last = gi + 1 == groups.size();
         int dst = raw;
         bool dnew = false, dip = false;
         if (!last) {
@@ -3060,54 +3126,57 @@ bool Engine::run_tree_frames(int half, const TreeVariant &v, const std::vector<i
             dst = freebuf.back(), freebuf.pop_back(), dnew = true;
           else
             dip = true;
+        } else {
+          dip = keepRaw;
         }
         std::vector<Executed> rd;
         VState V;
         V.buf = raw;
-        V.m = k.rep.m;
-        V.phi = k.rep.phi;
-        V.has_phi = true;
-        flip_exec(st.tps, Diag(), V, dst, hp, dip ? &rd : nullptr);
-        ++nreal;
-        // nodes on dst: the representative is X^{m_rep} dst, a member R' X^{m_rep} dst
-        std::vector<FNode> nn;
-        FNode r = k.rep;
-        r.phi = Diag();
-        r.ident = k.rep.m == 0;
-        nn.push_back(r);
-        for (const FNode &x : k.mem) {
-          FNode y = x;
-          frame_compose(x.phi, x.m, Diag(), k.rep.m, y.phi, y.m);
-          y.ident = false;
-          nn.push_back(y);
+        if (!g.surv) {
+          V.m = g.rep.m;
+          V.phi = g.rep.diag();
+          V.has_phi = true;
         }
-        process(pos + 1, dst, nn, dip, Diag());
+        flip_exec(st.tps, g.surv ? pin_pre : Diag(), V, dst, hp, dip ? &rd : nullptr);
+        if (!g.surv) ++nreal;
+        ++nsw;
+        process(pos + 1, dst, g.nodes, dip, Diag());
         if (dip) flip_undo(rd, dst, hp);
         if (dnew) freebuf.push_back(dst);
       }
-      if (surv.empty()) {
-        nodes.clear();
-        break;
-      }
-      VState V;
-      V.buf = raw;
-      flip_exec(st.tps, pend, V, raw, hp, keepRaw ? &rec : nullptr);
-      pend = Diag();
-      nodes.swap(surv);
+      nodes.clear();
+      break;
     }
-    for (const FNode &n : nodes) {
-      if (!n.ident) st_.flip_siblings++;
-      char *row = (char *)slice + (size_t)(n.bits & rmask) * (size_t)nS * amp_;
-      check(launch_gather(states_[raw]->ptr, dS, nS, row, to_dev(n.phi), c128_, stream_, ~0ull, 0, n.m),
-            "gather launch");
-      st_.kernel_launches++;
+    if (!nodes.empty()) {  // leaves: batched gathers through their frames
+      const DiagDev pend = to_dev(tail);
+      FrameLeaves lv;
+      lv.n = 0;
+      auto flush = [&]() {
+        if (!lv.n) return;
+        check(launch_frame_gather(states_[raw]->ptr, dS, nS, slice, lv, pend, c128_, stream_), "frame gather launch");
+        st_.kernel_launches++;
+        lv.n = 0;
+      };
+      for (const FNode &n : nodes) {
+        if (!n.f.identity()) st_.flip_siblings++;
+        FrameLeaf &L = lv.leaf[lv.n++];
+        L.t1 = (uint32_t)n.f.t1;
+        L.t2 = (uint32_t)n.f.t2;
+        L.zm = (uint32_t)n.f.zm;
+        L.m = (uint32_t)n.f.m;
+        L.ph0 = n.f.ph0;
+        L.row = (uint32_t)(n.bits & rmask);
+        if (lv.n == kMaxFrameLeaves) flush();
+      }
+      flush();
     }
     if (keepRaw) flip_undo(rec, raw, hp);
   };
-  FNode root;
-  process(0, 0, std::vector<FNode>{root}, false, Diag());
-  if (dbg) std::fprintf(stderr, "frames half %d m=%d: %d real states, %d steps, %d extra buffers\n", half, m, nreal,
-                        nsteps, extra);
+  std::vector<FNode> root(1);
+  process(0, 0, root, false, Diag());
+  if (std::getenv("QSIM_DEBUG_TREE"))
+    std::fprintf(stderr, "frames half %d m=%d: %d real states, %d sweeps (+%llu undone), %d steps, %d extra buffers\n",
+                 half, m, nreal, nsw, (unsigned long long)st_.undo_sweeps, nsteps, extra);
   return true;
 }
 

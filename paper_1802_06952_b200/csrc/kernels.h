@@ -169,6 +169,20 @@ cudaError_t launch_gather(const void *psi, const uint64_t *S, int64_t n, void *o
 cudaError_t launch_gather_nodes(const void *psi, uint64_t stride, int shift, int64_t nnodes, const uint64_t *S,
                                 int64_t n, void *out, const ForkDev &fork, bool c128, cudaStream_t s,
                                 const DiagDev *pend = nullptr, const uint32_t *rowmap = nullptr);
+// Leaves seen through linear Pauli frames (Engine::run_tree_frames): for leaf i and sampled index
+// x = S[j], out[row_i * n + j] = w^{ph0 + popc(x&t1) + 2 popc(x&t2) + 4 popc(x&zm)} pend(x) psi[x ^ m]
+struct FrameLeaf {
+  uint32_t t1, t2, zm, m;
+  int32_t ph0;
+  uint32_t row;
+};
+constexpr int kMaxFrameLeaves = 1024;
+struct FrameLeaves {
+  int32_t n;
+  FrameLeaf leaf[kMaxFrameLeaves];
+};
+cudaError_t launch_frame_gather(const void *psi, const uint64_t *S, int64_t n, void *out, const FrameLeaves &lv,
+                                const DiagDev &pend, bool c128, cudaStream_t s);
 // Output rows of node-batched leaves: out[N] = base | sum_t ((N >> t) & 1) << pos[t]
 struct RowMapDev {
   int32_t nbits;

@@ -101,6 +101,47 @@ cudaError_t launch_wht_rows(void *A, bool c128, int m, int64_t ncols, cudaStream
   return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------- leaves through frames
+template <typename R>
+__global__ void frame_gather_kernel(const typename CxT<R>::T *__restrict__ psi, const uint64_t *__restrict__ S,
+                                    int64_t n, typename CxT<R>::T *__restrict__ out, const DiagDev pend,
+                                    const __grid_constant__ FrameLeaves lv) {
+  using C = typename CxT<R>::T;
+  const int64_t total = (int64_t)lv.n * n;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e / n, j = e - i * n;
+    const FrameLeaf &f = lv.leaf[i];
+    const uint32_t x = (uint32_t)S[j];
+    const C v = psi[x ^ f.m];
+    int ph = f.ph0 + __popc(x & f.t1) + 2 * __popc(x & f.t2) + 4 * __popc(x & f.zm);
+    double sc = 1.0;
+    bool zero = false;
+    if (pend.active) {
+      ph += diag_phase(x, pend, pend.zm);
+      sc = pend.scale;
+      zero = (x & pend.pm) != pend.pv;
+    }
+    ph &= 7;
+    const R wr = (R)(c_omega[2 * ph] * sc), wi = (R)(c_omega[2 * ph + 1] * sc);
+    C y;
+    y.x = zero ? (R)0 : v.x * wr - v.y * wi;
+    y.y = zero ? (R)0 : v.x * wi + v.y * wr;
+    out[(int64_t)f.row * n + j] = y;
+  }
+}
+
+cudaError_t launch_frame_gather(const void *psi, const uint64_t *S, int64_t n, void *out, const FrameLeaves &lv,
+                                const DiagDev &pend, bool c128, cudaStream_t s) {
+  const int64_t total = (int64_t)lv.n * n;
+  if (total <= 0) return cudaSuccess;
+  const int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 16);
+  if (c128)
+    frame_gather_kernel<double><<<blocks, 256, 0, s>>>((const double2 *)psi, S, n, (double2 *)out, pend, lv);
+  else
+    frame_gather_kernel<float><<<blocks, 256, 0, s>>>((const float2 *)psi, S, n, (float2 *)out, pend, lv);
+  return cudaGetLastError();
+}
+
 // ---------------------------------------------------------------- node-batched leaves
 template <typename R>
 __global__ void gather_nodes_kernel(const typename CxT<R>::T *__restrict__ psi, uint64_t stride, int shift,
