@@ -6,7 +6,9 @@
 // blocks this is the complex contraction over the branch index b,
 //     A[i, j] = sum_b U[b, i] * L[b, j].
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
+#include <string>
 
 #include "sweep_common.cuh"
 
@@ -512,9 +514,147 @@ __global__ void __launch_bounds__(256) branch_gemm_kernel(const typename CxT<R>:
       }
 }
 
+// ---------------------------------------------------------------- branch GEMM, 3M form (DMMA)
+// The reconstruction contraction A += U^T L with complex entries as three real products (Gauss):
+//   T1 = Ur Lr, T2 = Ui Li, T3 = (Ur + Ui)(Lr + Li);  Re A += T1 - T2,  Im A += T3 - T1 - T2
+// (3 DMMAs per complex fragment product instead of 4).  CTA tile 64 x 64, K step 16, 8 warps as
+// 2 (M) x 4 (N) with 32 x 16 warp tiles of m8n8k4 FP64 MMAs; operands stream through a 3-stage
+// cp.async ring of interleaved complex tiles [k][m] (row stride padded so that the fragment loads are
+// bank-conflict free: 66 double2 / 68 float2); tiles are visited in bands of 16 tile rows so that the
+// CTAs in flight share their U and L panels in L2.
+constexpr int G3_T = 64, G3_K = 16, G3_ST = 3, G3_BAND = 16;
+template <typename R>
+__host__ __device__ constexpr int g3_stride() { return sizeof(R) == 8 ? 66 : 68; }
+template <typename R>
+constexpr size_t g3_smem() { return (size_t)2 * G3_ST * G3_K * g3_stride<R>() * sizeof(typename CxT<R>::T); }
+
+template <int BYTES>
+__device__ __forceinline__ void cp_async_zfill(void *dst, const void *src, bool ok) {
+  const uint32_t d = (uint32_t)__cvta_generic_to_shared(dst);
+  const int n = ok ? BYTES : 0;
+  if constexpr (BYTES == 16)
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(src), "r"(n) : "memory");
+  else
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(d), "l"(src), "r"(n) : "memory");
+}
+
+template <typename R>
+__global__ void __launch_bounds__(256, 1) branch_gemm3m_kernel(const typename CxT<R>::T *__restrict__ U,
+                                                               const typename CxT<R>::T *__restrict__ L,
+                                                               int64_t K, int64_t M, int64_t N,
+                                                               double *__restrict__ A, int tiles_m, int tiles_n) {
+  using C = typename CxT<R>::T;
+  constexpr int S = g3_stride<R>();
+  extern __shared__ __align__(16) unsigned char g3_raw[];
+  C *sU = reinterpret_cast<C *>(g3_raw);
+  C *sL = sU + G3_ST * G3_K * S;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = warp >> 2, wn = warp & 3;
+  // banded tile order
+  const int pid = blockIdx.x, per_band = G3_BAND * tiles_n, band = pid / per_band;
+  const int first = band * G3_BAND, rows = min(tiles_m - first, G3_BAND), in = pid - band * per_band;
+  const int64_t m0 = (int64_t)(first + in % rows) * G3_T, n0 = (int64_t)(in / rows) * G3_T;
+
+  auto load = [&](int st, int64_t k0) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int e = tid + q * 256;  // 0..1023 = 16 x 64
+      const int kk = e >> 6, mm = e & 63;
+      const int64_t k = k0 + kk;
+      const bool okk = k < K;
+      const bool oku = okk && m0 + mm < M, okl = okk && n0 + mm < N;
+      cp_async_zfill<sizeof(C)>(sU + (st * G3_K + kk) * S + mm, oku ? (const void *)(U + k * M + m0 + mm) : (const void *)U, oku);
+      cp_async_zfill<sizeof(C)>(sL + (st * G3_K + kk) * S + mm, okl ? (const void *)(L + k * N + n0 + mm) : (const void *)L, okl);
+    }
+  };
+  double t1[4][2][2], t2[4][2][2], t3[4][2][2];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 2; ++b)
+#pragma unroll
+      for (int c = 0; c < 2; ++c) t1[a][b][c] = t2[a][b][c] = t3[a][b][c] = 0.0;
+
+  const int64_t nk = (K + G3_K - 1) / G3_K;
+#pragma unroll
+  for (int s = 0; s < G3_ST - 1; ++s) {
+    if (s < nk) load(s, (int64_t)s * G3_K);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  }
+  for (int64_t kb = 0; kb < nk; ++kb) {
+    asm volatile("cp.async.wait_group %0;" ::"n"(G3_ST - 2) : "memory");
+    __syncthreads();
+    if (kb + G3_ST - 1 < nk) load((int)((kb + G3_ST - 1) % G3_ST), (kb + G3_ST - 1) * G3_K);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    const int st = (int)(kb % G3_ST);
+    const C *tu = sU + st * G3_K * S, *tl = sL + st * G3_K * S;
+#pragma unroll
+    for (int ks = 0; ks < G3_K; ks += 4) {
+      const int kr = ks + (lane & 3);
+      double ar[4], ai[4], as[4], br[2], bi[2], bs[2];
+#pragma unroll
+      for (int mt = 0; mt < 4; ++mt) {
+        const C u = tu[kr * S + wm * 32 + mt * 8 + (lane >> 2)];
+        ar[mt] = (double)u.x;
+        ai[mt] = (double)u.y;
+        as[mt] = ar[mt] + ai[mt];
+      }
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt) {
+        const C l = tl[kr * S + wn * 16 + nt * 8 + (lane >> 2)];
+        br[nt] = (double)l.x;
+        bi[nt] = (double)l.y;
+        bs[nt] = br[nt] + bi[nt];
+      }
+#pragma unroll
+      for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt) {
+          dmma(t1[mt][nt], ar[mt], br[nt]);
+          dmma(t2[mt][nt], ai[mt], bi[nt]);
+          dmma(t3[mt][nt], as[mt], bs[nt]);
+        }
+    }
+  }
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+#pragma unroll
+  for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        const int64_t m = m0 + wm * 32 + mt * 8 + (lane >> 2);
+        const int64_t n = n0 + wn * 16 + nt * 8 + (lane & 3) * 2 + c;
+        if (m < M && n < N) {
+          double *a = A + 2 * (m * N + n);
+          a[0] += t1[mt][nt][c] - t2[mt][nt][c];
+          a[1] += t3[mt][nt][c] - t1[mt][nt][c] - t2[mt][nt][c];
+        }
+      }
+}
+
+template <typename R>
+static cudaError_t launch_gemm3m(const void *U, const void *L, int64_t K, int64_t M, int64_t N, double *A,
+                                 cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute((const void *)branch_gemm3m_kernel<R>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g3_smem<R>());
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  const int tm = (int)((M + G3_T - 1) / G3_T), tn = (int)((N + G3_T - 1) / G3_T);
+  using C = typename CxT<R>::T;
+  branch_gemm3m_kernel<R><<<(unsigned)((int64_t)tm * tn), 256, g3_smem<R>(), s>>>((const C *)U, (const C *)L, K, M, N,
+                                                                                     A, tm, tn);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_branch_gemm(const void *U, const void *L, int64_t K, int64_t M, int64_t N,
                                double *A, bool c128, cudaStream_t s) {
   if (K <= 0 || M <= 0 || N <= 0) return cudaSuccess;
+  static const bool four = std::getenv("QSIM_GEMM") && std::string(std::getenv("QSIM_GEMM")) == "4m";  // A/B
+  if (!four) return c128 ? launch_gemm3m<double>(U, L, K, M, N, A, s) : launch_gemm3m<float>(U, L, K, M, N, A, s);
   dim3 grid((unsigned)((N + GB_N - 1) / GB_N), (unsigned)((M + GB_M - 1) / GB_M));
   if (c128)
     branch_gemm_kernel<double><<<grid, 256, 0, s>>>((const double2 *)U, (const double2 *)L, K, M, N, A, 0, 0, 0);

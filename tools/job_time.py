@@ -18,6 +18,7 @@ ap.add_argument("--precision", default="c128")
 ap.add_argument("--config", default="C5")
 ap.add_argument("--reps", type=int, default=2)
 ap.add_argument("--seed", type=int, default=0)
+ap.add_argument("--time", action="store_true", help="events around every sweep / GEMM launch")
 a = ap.parse_args()
 rows, cols, depth, lu, ll = CONFIGS[a.config]
 circ = generate(rows, cols, depth, a.seed)
@@ -31,6 +32,8 @@ Q.qsim_set_stream(ctx, stream.cuda_stream)
 Q.qsim_load_circuit(ctx, circ.rows, circ.cols, circ.depth, circ.gate_array(), circ.cut_row)
 c, B, cuts = Q.qsim_partition(ctx)
 Q.qsim_set_blocks(ctx, Su, Sl)
+if a.time:
+    Q.qsim_set_option(ctx, Q.QSIM_OPT_TIME_SWEEPS, 1)
 for r in range(a.reps):
     Q.qsim_reset_block(ctx)
     Q.qsim_stats_reset(ctx)
@@ -48,5 +51,6 @@ for r in range(a.reps):
     print(json.dumps({"rep": r, "precision": a.precision, "job_s": t, "issue_s": t_issue,
                       "amps_per_s": Su.size * Sl.size / t, "sweeps": st["sweeps"], "undo": st["undo_sweeps"],
                       "launches": st["kernel_launches"], "gemm_flops": st["gemm_flops"],
-                      "frame_leaves": st["flip_siblings"]}), flush=True)
+                      "frame_leaves": st["flip_siblings"], "sweep_ms": st["sweep_ms"], "gemm_ms": st["gemm_ms"],
+                      "gemm_tflops": st["gemm_flops"] / max(1e-9, st["gemm_ms"] / 1e3) / 1e12 if st["gemm_ms"] else None}), flush=True)
 Q.qsim_destroy(ctx)
