@@ -2990,10 +2990,18 @@ bool Engine::run_tree_frames(int half, const TreeVariant &v, const std::vector<i
     }
   }
   const int nsteps = (int)steps.size();
-  struct FNode {
+  struct FNode {  // one term of a leaf: (cr + i ci) F raw
     LinFrame f;
     uint64_t bits = 0;
+    double cr = 1.0, ci = 0.0;
+    int depth = 0;  // expansions so far
   };
+  // a frame that breaks on T / S phases is expanded into a sum of frames (lin_expand_through) while
+  // its term has been expanded fewer than expand_depth_ times and the step needs <= 16 terms
+  LinFrame xf[16];
+  double xc[32];
+  // the block's slice rows are accumulated (a leaf may be gathered from several real states)
+  check(cudaMemsetAsync(slice, 0, ((size_t)1 << m) * (size_t)nS * amp_, stream_), "zero slice rows");
   std::vector<int> freebuf;
   const int extra = std::max(0, std::min(nbuf - 1, flip_max_nb_ >= 0 ? flip_max_nb_ : 64));
   ensure_states(half, 1 + extra);
@@ -3050,10 +3058,24 @@ bool Engine::run_tree_frames(int half, const TreeVariant &v, const std::vector<i
       std::vector<FNode> surv, fail;
       surv.reserve(nodes.size());
       for (FNode &n : nodes) {
-        if (n.f.identity() || lin_through(sw, n.f))
+        if (n.f.identity() || lin_through(sw, n.f)) {
           surv.push_back(n);
-        else
+          continue;
+        }
+        const int nt = n.depth < expand_depth_ ? lin_expand_through(sw, n.f, 16, xf, xc) : 0;
+        if (nt == 0) {
           fail.push_back(n);
+          continue;
+        }
+        for (int i = 0; i < nt; ++i) {
+          FNode x = n;
+          x.f = xf[i];
+          x.cr = n.cr * xc[2 * i] - n.ci * xc[2 * i + 1];
+          x.ci = n.cr * xc[2 * i + 1] + n.ci * xc[2 * i];
+          x.depth = n.depth + 1;
+          surv.push_back(x);
+        }
+        nterms_ += nt - 1;
       }
       nodes.clear();
       nodes.shrink_to_fit();
@@ -3147,26 +3169,44 @@ bool Engine::run_tree_frames(int half, const TreeVariant &v, const std::vector<i
       nodes.clear();
       break;
     }
-    if (!nodes.empty()) {  // leaves: batched gathers through their frames
+    if (!nodes.empty()) {  // leaves: batched gathers through their frames, the terms of a leaf summed
+      std::stable_sort(nodes.begin(), nodes.end(),
+                       [&](const FNode &a, const FNode &b) { return (a.bits & rmask) < (b.bits & rmask); });
       const DiagDev pend = to_dev(tail);
-      FrameLeaves lv;
-      lv.n = 0;
+      FrameBatch fb;
+      fb.nleaf = 0;
+      fb.off[0] = 0;
+      int nterm = 0;
       auto flush = [&]() {
-        if (!lv.n) return;
-        check(launch_frame_gather(states_[raw]->ptr, dS, nS, slice, lv, pend, c128_, stream_), "frame gather launch");
+        if (!fb.nleaf) return;
+        check(launch_frame_gather(states_[raw]->ptr, dS, nS, slice, fb, pend, c128_, stream_), "frame gather launch");
         st_.kernel_launches++;
-        lv.n = 0;
+        fb.nleaf = 0;
+        nterm = 0;
       };
-      for (const FNode &n : nodes) {
-        if (!n.f.identity()) st_.flip_siblings++;
-        FrameLeaf &L = lv.leaf[lv.n++];
-        L.t1 = (uint32_t)n.f.t1;
-        L.t2 = (uint32_t)n.f.t2;
-        L.zm = (uint32_t)n.f.zm;
-        L.m = (uint32_t)n.f.m;
-        L.ph0 = n.f.ph0;
-        L.row = (uint32_t)(n.bits & rmask);
-        if (lv.n == kMaxFrameLeaves) flush();
+      for (size_t a = 0; a < nodes.size();) {
+        size_t e = a + 1;
+        while (e < nodes.size() && (nodes[e].bits & rmask) == (nodes[a].bits & rmask)) ++e;
+        for (size_t s0 = a; s0 < e; s0 += kMaxBatchTerms) {  // a leaf with more terms spans launches
+          const size_t s1 = std::min(e, s0 + (size_t)kMaxBatchTerms);
+          if (fb.nleaf == kMaxBatchLeaves || nterm + (int)(s1 - s0) > kMaxBatchTerms) flush();
+          for (size_t q = s0; q < s1; ++q) {
+            const FNode &n = nodes[q];
+            if (!n.f.identity()) st_.flip_siblings++;
+            FrameTerm &T = fb.term[nterm++];
+            T.t1 = (uint32_t)n.f.t1;
+            T.t2 = (uint32_t)n.f.t2;
+            T.zm = (uint32_t)n.f.zm;
+            T.m = (uint32_t)n.f.m;
+            T.ph0 = n.f.ph0;
+            T.pad = 0;
+            T.cr = n.cr;
+            T.ci = n.ci;
+          }
+          fb.row[fb.nleaf] = (uint32_t)(nodes[a].bits & rmask);
+          fb.off[++fb.nleaf] = (uint16_t)nterm;
+        }
+        a = e;
       }
       flush();
     }
@@ -3175,8 +3215,9 @@ bool Engine::run_tree_frames(int half, const TreeVariant &v, const std::vector<i
   std::vector<FNode> root(1);
   process(0, 0, root, false, Diag());
   if (std::getenv("QSIM_DEBUG_TREE"))
-    std::fprintf(stderr, "frames half %d m=%d: %d real states, %d sweeps (+%llu undone), %d steps, %d extra buffers\n",
-                 half, m, nreal, nsw, (unsigned long long)st_.undo_sweeps, nsteps, extra);
+    std::fprintf(stderr, "frames half %d m=%d: %d real states, %d sweeps (+%llu undone), %d steps, %d extra buffers, "
+                 "%lld extra terms\n", half, m, nreal, nsw, (unsigned long long)st_.undo_sweeps, nsteps, extra,
+                 (long long)nterms_);
   return true;
 }
 

@@ -239,6 +239,9 @@ class Engine {
   bool run_tree_frames(int half, const TreeVariant &v, const std::vector<int> &pin, int m, void *slice,
                        const uint64_t *dS, int64_t nS, int nbuf);
   bool frames_ = !(std::getenv("QSIM_FRAMES") && std::getenv("QSIM_FRAMES")[0] == '0');
+  // expansions of a breaking frame into a sum of frames per term (QSIM_FRAME_EXPAND; 0: real splits only)
+  int expand_depth_ = std::getenv("QSIM_FRAME_EXPAND") ? std::atoi(std::getenv("QSIM_FRAME_EXPAND")) : 6;
+  long long nterms_ = 0;
   TreeChoice flip_choice(int half, int m) const;
   bool run_tree_flip(int half, const TreeVariant &v, int lz, const std::vector<int> &pin, int m, void *slice,
                      const uint64_t *dS, int64_t nS, int nbuf);

@@ -169,19 +169,22 @@ cudaError_t launch_gather(const void *psi, const uint64_t *S, int64_t n, void *o
 cudaError_t launch_gather_nodes(const void *psi, uint64_t stride, int shift, int64_t nnodes, const uint64_t *S,
                                 int64_t n, void *out, const ForkDev &fork, bool c128, cudaStream_t s,
                                 const DiagDev *pend = nullptr, const uint32_t *rowmap = nullptr);
-// Leaves seen through linear Pauli frames (Engine::run_tree_frames): for leaf i and sampled index
-// x = S[j], out[row_i * n + j] = w^{ph0 + popc(x&t1) + 2 popc(x&t2) + 4 popc(x&zm)} pend(x) psi[x ^ m]
-struct FrameLeaf {
+// Leaves seen through linear Pauli frames (Engine::run_tree_frames): each leaf is a sum of terms
+// c_k w^{ph0_k + popc(x&t1_k) + 2 popc(x&t2_k) + 4 popc(x&zm_k)} psi[x ^ m_k]; for leaf i and x = S[j]
+//   out[row_i * n + j] += pend(x) * sum over the leaf's terms k in [off[i], off[i+1])
+struct FrameTerm {
   uint32_t t1, t2, zm, m;
-  int32_t ph0;
-  uint32_t row;
+  int32_t ph0, pad;
+  double cr, ci;
 };
-constexpr int kMaxFrameLeaves = 1024;
-struct FrameLeaves {
-  int32_t n;
-  FrameLeaf leaf[kMaxFrameLeaves];
+constexpr int kMaxBatchLeaves = 256, kMaxBatchTerms = 512;
+struct FrameBatch {
+  int32_t nleaf;
+  uint16_t off[kMaxBatchLeaves + 1];
+  uint32_t row[kMaxBatchLeaves];
+  FrameTerm term[kMaxBatchTerms];
 };
-cudaError_t launch_frame_gather(const void *psi, const uint64_t *S, int64_t n, void *out, const FrameLeaves &lv,
+cudaError_t launch_frame_gather(const void *psi, const uint64_t *S, int64_t n, void *out, const FrameBatch &b,
                                 const DiagDev &pend, bool c128, cudaStream_t s);
 // Output rows of node-batched leaves: out[N] = base | sum_t ((N >> t) & 1) << pos[t]
 struct RowMapDev {

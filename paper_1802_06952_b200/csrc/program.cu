@@ -269,10 +269,8 @@ static bool lin_ratio(LinFrame &f, const Diag &D) {
   return true;
 }
 
-bool lin_through(const Sweep &sw, LinFrame &f0) {
-  if (sw.gen) return false;
-  LinFrame f = f0;
-  if (!lin_ratio(f, sw.pre)) return false;
+// the gate stage of a frame move (every target's count must be 0 or 4)
+static bool lin_gates(const Sweep &sw, LinFrame &f) {
   for (const Gate1 &g : sw.gates) {
     const int t = g.bit;
     const int c = f.count(t);
@@ -291,9 +289,53 @@ bool lin_through(const Sweep &sw, LinFrame &f0) {
     f.ph0 = (f.ph0 + ph) & 7;
     f.m = nf ? (f.m | bit) : (f.m & ~bit);
   }
-  if (!lin_ratio(f, sw.post)) return false;
+  return true;
+}
+
+bool lin_through(const Sweep &sw, LinFrame &f0) {
+  if (sw.gen) return false;
+  LinFrame f = f0;
+  if (!lin_ratio(f, sw.pre) || !lin_gates(sw, f) || !lin_ratio(f, sw.post)) return false;
   f0 = f;
   return true;
+}
+
+int lin_expand_through(const Sweep &sw, const LinFrame &f0, int max_terms, LinFrame *out, double *coef) {
+  if (sw.gen) return 0;
+  LinFrame f = f0;
+  if (!lin_ratio(f, sw.pre)) return 0;
+  int bad[32], nb = 0;
+  for (const Gate1 &g : sw.gates)
+    if (f.count(g.bit) & 3) {
+      if (nb == 32) return 0;
+      bad[nb++] = g.bit;
+    }
+  if (nb > 30 || (1ll << nb) > max_terms) return 0;
+  const int n = 1 << nb;
+  for (int s = 0; s < n; ++s) {
+    LinFrame h = f;
+    double cr = 1.0, ci = 0.0;
+    for (int i = 0; i < nb; ++i) {
+      const int t = bad[i], cnt = h.count(t);
+      static const double r2 = 0.70710678118654752440;
+      static const double W[8][2] = {{1, 0}, {r2, r2}, {0, 1}, {-r2, r2}, {-1, 0}, {-r2, -r2}, {0, -1}, {r2, -r2}};
+      const double wr = W[cnt & 7][0], wi = W[cnt & 7][1];
+      const bool z = (s >> i) & 1;
+      const double xr = z ? 0.5 * (1.0 - wr) : 0.5 * (1.0 + wr), xi = z ? -0.5 * wi : 0.5 * wi;
+      const double nr = cr * xr - ci * xi, ni = cr * xi + ci * xr;
+      cr = nr;
+      ci = ni;
+      const uint64_t bit = 1ull << t;
+      h.t1 &= ~bit;
+      h.t2 &= ~bit;
+      h.zm = z ? (h.zm | bit) : (h.zm & ~bit);
+    }
+    if (!lin_gates(sw, h) || !lin_ratio(h, sw.post)) return 0;
+    out[s] = h;
+    coef[2 * s] = cr;
+    coef[2 * s + 1] = ci;
+  }
+  return n;
 }
 
 LinFrame lin_compose(const LinFrame &f2, const LinFrame &f1) {

@@ -187,6 +187,12 @@ struct LinFrame {
   Diag diag() const;                                       // phi as a Diag
 };
 bool lin_through(const Sweep &sw, LinFrame &f);
+// Where f breaks on phases alone (a target t whose count c is not 0 or 4), f is a sum of two frames:
+// w^{c x_t} = a + b (-1)^{x_t} with a = (1 + w^c) / 2, b = (1 - w^c) / 2 (count 0 and count 4 at t).
+// Writes the terms moved through sw (frames to out, complex coefficients to coef[2 i], coef[2 i + 1])
+// and returns their number (1 when f moves as it is), or 0 when f breaks otherwise (a projector
+// meets the flip) or would need more than max_terms terms.
+int lin_expand_through(const Sweep &sw, const LinFrame &f, int max_terms, LinFrame *out, double *coef);
 LinFrame lin_compose(const LinFrame &f2, const LinFrame &f1);  // f2 . f1
 LinFrame lin_inverse(const LinFrame &f);
 

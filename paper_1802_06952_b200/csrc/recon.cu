@@ -107,40 +107,44 @@ cudaError_t launch_wht_rows(void *A, bool c128, int m, int64_t ncols, cudaStream
 template <typename R>
 __global__ void frame_gather_kernel(const typename CxT<R>::T *__restrict__ psi, const uint64_t *__restrict__ S,
                                     int64_t n, typename CxT<R>::T *__restrict__ out, const DiagDev pend,
-                                    const __grid_constant__ FrameLeaves lv) {
+                                    const __grid_constant__ FrameBatch b) {
   using C = typename CxT<R>::T;
-  const int64_t total = (int64_t)lv.n * n;
+  const int64_t total = (int64_t)b.nleaf * n;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t i = e / n, j = e - i * n;
-    const FrameLeaf &f = lv.leaf[i];
     const uint32_t x = (uint32_t)S[j];
-    const C v = psi[x ^ f.m];
-    int ph = f.ph0 + __popc(x & f.t1) + 2 * __popc(x & f.t2) + 4 * __popc(x & f.zm);
-    double sc = 1.0;
-    bool zero = false;
-    if (pend.active) {
-      ph += diag_phase(x, pend, pend.zm);
-      sc = pend.scale;
-      zero = (x & pend.pm) != pend.pv;
+    double sr = 0.0, si = 0.0;
+    for (int k = b.off[i]; k < b.off[i + 1]; ++k) {
+      const FrameTerm &f = b.term[k];
+      const C v = psi[x ^ f.m];
+      const int ph = (f.ph0 + __popc(x & f.t1) + 2 * __popc(x & f.t2) + 4 * __popc(x & f.zm)) & 7;
+      const double wr = c_omega[2 * ph] * f.cr - c_omega[2 * ph + 1] * f.ci;
+      const double wi = c_omega[2 * ph] * f.ci + c_omega[2 * ph + 1] * f.cr;
+      sr += (double)v.x * wr - (double)v.y * wi;
+      si += (double)v.x * wi + (double)v.y * wr;
     }
-    ph &= 7;
-    const R wr = (R)(c_omega[2 * ph] * sc), wi = (R)(c_omega[2 * ph + 1] * sc);
-    C y;
-    y.x = zero ? (R)0 : v.x * wr - v.y * wi;
-    y.y = zero ? (R)0 : v.x * wi + v.y * wr;
-    out[(int64_t)f.row * n + j] = y;
+    if (pend.active) {
+      const int ph = diag_phase(x, pend, pend.zm);
+      const double wr = c_omega[2 * ph] * pend.scale, wi = c_omega[2 * ph + 1] * pend.scale;
+      const double tr = sr * wr - si * wi, ti = sr * wi + si * wr;
+      sr = (x & pend.pm) != pend.pv ? 0.0 : tr;
+      si = (x & pend.pm) != pend.pv ? 0.0 : ti;
+    }
+    C &o = out[(int64_t)b.row[i] * n + j];
+    o.x += (R)sr;
+    o.y += (R)si;
   }
 }
 
-cudaError_t launch_frame_gather(const void *psi, const uint64_t *S, int64_t n, void *out, const FrameLeaves &lv,
+cudaError_t launch_frame_gather(const void *psi, const uint64_t *S, int64_t n, void *out, const FrameBatch &b,
                                 const DiagDev &pend, bool c128, cudaStream_t s) {
-  const int64_t total = (int64_t)lv.n * n;
+  const int64_t total = (int64_t)b.nleaf * n;
   if (total <= 0) return cudaSuccess;
   const int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 16);
   if (c128)
-    frame_gather_kernel<double><<<blocks, 256, 0, s>>>((const double2 *)psi, S, n, (double2 *)out, pend, lv);
+    frame_gather_kernel<double><<<blocks, 256, 0, s>>>((const double2 *)psi, S, n, (double2 *)out, pend, b);
   else
-    frame_gather_kernel<float><<<blocks, 256, 0, s>>>((const float2 *)psi, S, n, (float2 *)out, pend, lv);
+    frame_gather_kernel<float><<<blocks, 256, 0, s>>>((const float2 *)psi, S, n, (float2 *)out, pend, b);
   return cudaGetLastError();
 }
 

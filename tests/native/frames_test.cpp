@@ -94,4 +94,39 @@ int lin_check() {
   return bad;
 }
 int main2() { return lin_check(); }
-int main() { int a = main_dense(); int b = lin_check(); return a || b; }
+
+// ---- expansion of a breaking frame into a sum of frames
+int expand_check() {
+  std::mt19937_64 r(5);
+  int bad = 0, multi = 0;
+  for (int it = 0; it < 3000; ++it) {
+    Sweep sw;
+    std::vector<int> bits = {0, 1, 2, 3, 4};
+    std::shuffle(bits.begin(), bits.end(), r);
+    int ng = 1 + r() % 3;
+    for (int k = 0; k < ng; ++k) sw.gates.push_back(Gate1{(uint8_t)bits[k], (uint8_t)(1 + r() % 2)});
+    for (int k = 0; k < 3; ++k) { sw.post.add_T(r() % n); sw.pre.add_T(r() % n); }
+    for (int k = 0; k < 2; ++k) { int a = r() % n, b = r() % n; if (a != b) sw.post.add_cz(a, b); }
+    sw.post.nhalf = ng;
+    LinFrame f; f.m = r() % N; f.ph0 = r() % 8;
+    for (int k = 0; k < 3; ++k) { int a = r() % n; f.add_counts(1ull << a, (r() % 2) ? 1ull << a : 0, 0); }
+    LinFrame out[64]; double coef[128];
+    const int nt = lin_expand_through(sw, f, 64, out, coef);
+    if (nt == 0) continue;
+    if (nt > 1) ++multi;
+    Mat G = diag(sw.pre);
+    for (auto &g : sw.gates) G = mul(gate(g.bit, g.kind), G);
+    G = mul(diag(sw.post), G);
+    Mat L = mul(G, mul(diag(f.diag()), flip(f.m)));
+    Mat R(N * N);
+    for (int i = 0; i < nt; ++i) {
+      Mat T = mul(mul(diag(out[i].diag()), flip(out[i].m)), G);
+      for (int e = 0; e < N * N; ++e) R[e] += cd(coef[2 * i], coef[2 * i + 1]) * T[e];
+    }
+    double e = 0; for (int i = 0; i < N * N; ++i) e = std::max(e, std::abs(L[i] - R[i]));
+    if (e > 1e-12) ++bad;
+  }
+  printf("expand: %d multi-term, bad %d\n", multi, bad);
+  return bad;
+}
+int main() { int a = main_dense(); int b = lin_check(); int c = expand_check(); return a || b || c; }
