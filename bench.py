@@ -61,6 +61,23 @@ def parse():
     return ap.parse_args()
 
 
+# FP64 tensor ceiling measured on B200 with tools/native/dmma_peak.cu (register-only m8n8k4 DMMAs,
+# 8-32 warps per SM; profiles/r02/r02w_dmma_peak.txt)
+DMMA_CEILING = 37.1
+
+
+def fp64_peak():
+    """FP64 tensor peak by the profiling recipe's rule: another dtype's measured peak x the nominal ratio
+    (MEASURED_PEAKS.json bf16 burst x 45 / 2250, the B200 FP64-tensor / BF16 dense nominals)."""
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return float(d["bf16_tflops"]) * 45.0 / 2250.0, "MEASURED_PEAKS.json bf16_tflops x 45/2250 (FP64 tensor / BF16 nominal)"
+    except Exception:
+        return 45.0, "nominal B200 FP64 tensor (guide)"
+
+
 def peaks():
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
@@ -450,9 +467,14 @@ def main():
     h2d = (n_u + n_l) * 8 * world
     d2h = n_u * n_l * amp_bytes + N_DRAWS * 8 + 8
 
-    # ---------------- roofline of the dominant kernel (the gate sweep), from the profiling step
+    # ---------------- rooflines from the profiling step: the reconstruction GEMM (the dominant kernel
+    # since the frame executor cut the sweeps to one real state per half) and the gate sweep
     st = main_run["prof"]
     peak, peak_src = peaks()
+    gemm_s = st["gemm_ms"] / 1e3
+    f64_peak, f64_src = fp64_peak()
+    gemm_exec = 0.75 * st["gemm_flops"] / gemm_s / 1e12 if gemm_s > 0 else None  # 3M: 6MNK executed
+    gemm_alg = st["gemm_flops"] / gemm_s / 1e12 if gemm_s > 0 else None         # 8MNK convention
     sweep_s = st["sweep_ms"] / 1e3
     alg = st["sweep_bytes"] / sweep_s / 1e9 if sweep_s > 0 else None
     moved = st["sweep_bytes_moved"] / sweep_s / 1e9 if sweep_s > 0 else None
@@ -497,7 +519,19 @@ def main():
                 "l2": f"inputs larger than L2: half states of {((1 << circ.h_upper) * amp_bytes) >> 20} MiB",
                 "parallelism": f"branch-sharded dp{world}",
             },
-            "roofline": {"bound": "hbm", "achieved": moved, "peak": peak, "unit": "GB/s",
+            "roofline": {"bound": "tensor", "kernel": "branch_gemm3m_kernel (FP64 DMMA m8n8k4, 3M complex form)",
+                         "achieved": gemm_exec, "peak": f64_peak, "unit": "TFLOP/s",
+                         "frac": (gemm_exec / f64_peak) if gemm_exec else None, "traffic": None,
+                         "peak_source": f64_src,
+                         "achieved_8mnk_convention": gemm_alg,
+                         "dmma_ceiling_tflops": DMMA_CEILING,
+                         "frac_of_dmma_ceiling": (gemm_exec / DMMA_CEILING) if gemm_exec else None,
+                         "executed_flops_per_step": 0.75 * st["gemm_flops"],
+                         "share_of_step": gemm_s / main_run["prof_step_s"] if main_run["prof_step_s"] else None,
+                         "note": "achieved = executed real flops (6MNK: T1 = Ur Lr, T2 = Ui Li, T3 = (Ur+Ui)(Lr+Li)) / "
+                                 "CUDA-event time of the GEMM launches in the profiling step; the 8MNK complex "
+                                 "convention of SURVEY 8(d) is achieved_8mnk_convention"},
+            "roofline_sweep": {"bound": "hbm", "achieved": moved, "peak": peak, "unit": "GB/s",
                          "frac": (moved / peak) if moved else None, "traffic": traffic,
                          "achieved_algorithmic": alg,
                          "frac_algorithmic": (alg / peak) if alg else None,

@@ -657,7 +657,9 @@ static cudaError_t launch_gemm3m(const void *U, const void *L, int64_t K, int64_
 cudaError_t launch_branch_gemm(const void *U, const void *L, int64_t K, int64_t M, int64_t N,
                                double *A, bool c128, cudaStream_t s) {
   if (K <= 0 || M <= 0 || N <= 0) return cudaSuccess;
-  static const bool four = std::getenv("QSIM_GEMM") && std::string(std::getenv("QSIM_GEMM")) == "4m";  // A/B
+  // A/B: QSIM_GEMM=4m runs the four-product kernel below.  (An m16n8k8 form was measured equal: ptxas
+  // splits it into the same DMMA.8x8x4 instructions, the only FP64 MMA of sm_100a.)
+  static const bool four = std::getenv("QSIM_GEMM") && std::string(std::getenv("QSIM_GEMM")) == "4m";
   if (!four) return c128 ? launch_gemm3m<double>(U, L, K, M, N, A, s) : launch_gemm3m<float>(U, L, K, M, N, A, s);
   dim3 grid((unsigned)((N + GB_N - 1) / GB_N), (unsigned)((M + GB_M - 1) / GB_M));
   if (c128)

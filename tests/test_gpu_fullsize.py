@@ -300,3 +300,41 @@ def test_c5_leaf_values_h32(half):
             d, rel, rms = errs(got, ref)
             print(f"C5 h32 half {half} branch {b} {PNAME[prec]}: max|d| {d:.3e} /max {rel:.3e} /rms {rms:.3e}")
             assert_close(got, ref, prec, f"C5 half {half} branch {b}")
+
+
+def _c5_block(prec, Su, Sl, b0, b1, env, monkeypatch):
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    ctx = make_ctx(prec, generate(8, 8, 22, 0))
+    try:
+        Q.qsim_set_blocks(ctx, Su, Sl)
+        Q.qsim_evolve_range(ctx, b0, b1)
+        return Q.qsim_amplitudes(ctx, Su, Sl)
+    finally:
+        Q.qsim_destroy(ctx)
+
+
+@pytest.mark.slow
+def test_c5_frames_vs_tree(monkeypatch):
+    """C5 (64q d22), branches [0, 4096) (one block of 12 free cuts) on a 512 x 512 block in c128: the
+    Pauli-frame executor with expansion (one real state per half, leaves as sums of frame terms), with
+    real splits only (QSIM_FRAME_EXPAND=0), and the plain branch-tree executor (QSIM_FRAMES=0: every
+    leaf from its own sweeps) agree to 1e-12 of max|a|."""
+    Su, Sl = sample_block(32, 512, 80), sample_block(32, 512, 81)
+    ref = _c5_block(Q.QSIM_C128, Su, Sl, 0, 4096, {"QSIM_FRAMES": "0"}, monkeypatch)
+    for env in ({"QSIM_FRAMES": "1", "QSIM_FRAME_EXPAND": "0"}, {"QSIM_FRAMES": "1", "QSIM_FRAME_EXPAND": "6"}):
+        A = _c5_block(Q.QSIM_C128, Su, Sl, 0, 4096, env, monkeypatch)
+        d, rel, rms = errs(A, ref)
+        print(f"C5 [0, 4096) frames {env}: max|d| {d:.3e} /max {rel:.3e} /rms {rms:.3e}")
+        assert rel <= 1e-12
+
+
+@pytest.mark.slow
+def test_c5_whole_job_c64_vs_c128(monkeypatch):
+    """The whole C5 job (all 65536 branches, one block per half) on a 1024 x 1024 block: c64 within
+    1e-5 of max|a| of c128 (R12), both through the frame executor."""
+    Su, Sl = sample_block(32, 1024, 82), sample_block(32, 1024, 83)
+    out = {p: _c5_block(p, Su, Sl, 0, 1 << 16, {}, monkeypatch) for p in PRECS}
+    d, rel, rms = errs(out[Q.QSIM_C64], out[Q.QSIM_C128])
+    print(f"C5 whole job c64 vs c128: max|d| {d:.3e} /max {rel:.3e} /rms {rms:.3e}")
+    assert rel <= 1e-5
