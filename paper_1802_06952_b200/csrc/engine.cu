@@ -2,6 +2,8 @@
 // sampling and the NCCL reduction of partial blocks.
 #include "engine.h"
 
+#include <unordered_map>
+
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
@@ -1470,7 +1472,7 @@ void Engine::evolve_range(uint64_t b0, uint64_t b1) {
         while (m < c && ((a >> m) & 1u) == 0 && a + (2ull << m) <= e) ++m;
         check(launch_wht_rows((char *)L_.ptr + (size_t)(a - s) * (size_t)nl * amp_, c128_, m, nl, stream_),
               "wht launch");
-        st_.kernel_launches += (uint64_t)m;
+        st_.kernel_launches += (uint64_t)((m + 7) / 8);
         a += 1ull << m;
       }
     }
@@ -3002,9 +3004,10 @@ bool Engine::run_tree_frames(int half, const TreeVariant &v, const std::vector<i
   double xc[32];
   // the block's slice rows are accumulated (a leaf may be gathered from several real states)
   check(cudaMemsetAsync(slice, 0, ((size_t)1 << m) * (size_t)nS * amp_, stream_), "zero slice rows");
-  std::vector<int> freebuf;
+  std::vector<int> freebuf;  // state buffers beyond the root's, reserved when a split first needs one
   const int extra = std::max(0, std::min(nbuf - 1, flip_max_nb_ >= 0 ? flip_max_nb_ : 64));
-  ensure_states(half, 1 + extra);
+  while ((int)states_.size() < 1 + extra) states_.push_back(new DevBuf());
+  states_[0]->reserve(state_bytes_);
   for (int i = extra; i >= 1; --i) freebuf.push_back(i);
   const uint64_t rmask = m >= 64 ? ~0ull : ((1ull << m) - 1ull);
   int nreal = 1, nsw = 0;
@@ -3144,10 +3147,12 @@ bool Engine::run_tree_frames(int half, const TreeVariant &v, const std::vector<i
         int dst = raw;
         bool dnew = false, dip = false;
         if (!last) {
-          if (!freebuf.empty())
+          if (!freebuf.empty()) {
             dst = freebuf.back(), freebuf.pop_back(), dnew = true;
-          else
+            states_[dst]->reserve(state_bytes_);
+          } else {
             dip = true;
+          }
         } else {
           dip = keepRaw;
         }
@@ -3170,6 +3175,31 @@ bool Engine::run_tree_frames(int half, const TreeVariant &v, const std::vector<i
       break;
     }
     if (!nodes.empty()) {  // leaves: batched gathers through their frames, the terms of a leaf summed
+      // the distinct flips are gathered once each into rows (coalesced reads for every term after) when
+      // they are fewer than the terms and their rows fit; else every term reads the state scattered
+      std::unordered_map<uint64_t, uint32_t> fidx;
+      std::vector<uint64_t> flips;
+      for (const FNode &n : nodes)
+        if (fidx.emplace(n.f.m, (uint32_t)flips.size()).second) flips.push_back(n.f.m);
+      const size_t rows_bytes = flips.size() * (size_t)nS * amp_;
+      size_t free_b = 0, total_b = 0;
+      check(cudaMemGetInfo(&free_b, &total_b), "cudaMemGetInfo");
+      const bool use_rows = flip_rows_ && flips.size() * 4 <= nodes.size() &&
+                            rows_bytes + flips.size() * 8 + ((size_t)1 << 30) <= free_b + flip_rows_buf_.bytes;
+      if (std::getenv("QSIM_DEBUG_TREE"))
+        std::fprintf(stderr, "frames gather: %zu terms, %zu distinct flips on buffer %d (%s)\n", nodes.size(),
+                     flips.size(), raw, use_rows ? "flip rows" : "scattered");
+      if (use_rows) {
+        flip_rows_buf_.reserve(rows_bytes);
+        flip_idx_buf_.reserve(flips.size() * 8);
+        check(cudaMemcpyAsync(flip_idx_buf_.ptr, flips.data(), flips.size() * 8, cudaMemcpyHostToDevice, stream_),
+              "upload flips");
+        check(launch_flip_rows(states_[raw]->ptr, dS, nS, flip_idx_buf_.as<uint64_t>(), (int64_t)flips.size(),
+                               flip_rows_buf_.ptr, c128_, stream_),
+              "flip rows launch");
+        st_.kernel_launches++;
+        check(cudaStreamSynchronize(stream_), "flip rows");  // `flips` is a host temporary
+      }
       std::stable_sort(nodes.begin(), nodes.end(),
                        [&](const FNode &a, const FNode &b) { return (a.bits & rmask) < (b.bits & rmask); });
       const DiagDev pend = to_dev(tail);
@@ -3179,7 +3209,9 @@ bool Engine::run_tree_frames(int half, const TreeVariant &v, const std::vector<i
       int nterm = 0;
       auto flush = [&]() {
         if (!fb.nleaf) return;
-        check(launch_frame_gather(states_[raw]->ptr, dS, nS, slice, fb, pend, c128_, stream_), "frame gather launch");
+        check(launch_frame_gather(use_rows ? flip_rows_buf_.ptr : states_[raw]->ptr, dS, nS, slice, fb, pend, c128_,
+                                  stream_, use_rows),
+              "frame gather launch");
         st_.kernel_launches++;
         fb.nleaf = 0;
         nterm = 0;
@@ -3197,7 +3229,7 @@ bool Engine::run_tree_frames(int half, const TreeVariant &v, const std::vector<i
             T.t1 = (uint32_t)n.f.t1;
             T.t2 = (uint32_t)n.f.t2;
             T.zm = (uint32_t)n.f.zm;
-            T.m = (uint32_t)n.f.m;
+            T.m = use_rows ? fidx[n.f.m] : (uint32_t)n.f.m;
             T.ph0 = n.f.ph0;
             T.pad = 0;
             T.cr = n.cr;

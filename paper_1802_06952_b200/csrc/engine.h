@@ -242,6 +242,9 @@ class Engine {
   // expansions of a breaking frame into a sum of frames per term (QSIM_FRAME_EXPAND; 0: real splits only)
   int expand_depth_ = std::getenv("QSIM_FRAME_EXPAND") ? std::atoi(std::getenv("QSIM_FRAME_EXPAND")) : 6;
   long long nterms_ = 0;
+  // frame gathers through pre-gathered rows of the distinct flips (QSIM_FLIP_ROWS=0: scattered, A/B)
+  bool flip_rows_ = !(std::getenv("QSIM_FLIP_ROWS") && std::getenv("QSIM_FLIP_ROWS")[0] == '0');
+  DevBuf flip_rows_buf_, flip_idx_buf_;
   TreeChoice flip_choice(int half, int m) const;
   bool run_tree_flip(int half, const TreeVariant &v, int lz, const std::vector<int> &pin, int m, void *slice,
                      const uint64_t *dS, int64_t nS, int nbuf);

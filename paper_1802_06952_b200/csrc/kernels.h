@@ -184,8 +184,12 @@ struct FrameBatch {
   uint32_t row[kMaxBatchLeaves];
   FrameTerm term[kMaxBatchTerms];
 };
+// from_rows: psi is a [flip][n] table of pre-gathered rows (launch_flip_rows) and FrameTerm::m a row index
 cudaError_t launch_frame_gather(const void *psi, const uint64_t *S, int64_t n, void *out, const FrameBatch &b,
-                                const DiagDev &pend, bool c128, cudaStream_t s);
+                                const DiagDev &pend, bool c128, cudaStream_t s, bool from_rows = false);
+// g[i * n + j] = psi[S[j] ^ flips[i]] for the nf distinct flips of a gather (one scattered pass per flip)
+cudaError_t launch_flip_rows(const void *psi, const uint64_t *S, int64_t n, const uint64_t *flips, int64_t nf, void *g,
+                             bool c128, cudaStream_t s);
 // Output rows of node-batched leaves: out[N] = base | sum_t ((N >> t) & 1) << pos[t]
 struct RowMapDev {
   int32_t nbits;

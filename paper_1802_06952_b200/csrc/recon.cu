@@ -72,39 +72,71 @@ cudaError_t launch_gather(const void *psi, const uint64_t *S, int64_t n, void *o
 // With Z^b forks on both endpoints of a block's free cuts, CZ = sum_{a,b} H_ab Z^a (x) Z^b with
 // H = [[1, 1], [1, -1]] / 2 per cut, so the lower slice rows are replaced by sum_b H_ab L_b (DESIGN.md
 // R-zz): one butterfly pass per branch bit, (a + b) / 2 and (a - b) / 2 (exact scaling).
+// up to 8 row bits [b0, b0 + nb) in one pass: a CTA holds 2^nb rows x 16 columns in shared memory
 template <typename R>
-__global__ void wht_rows_kernel(typename CxT<R>::T *__restrict__ A, int bit, int64_t npairs, int64_t ncols) {
+__global__ void __launch_bounds__(256) wht_rows_smem_kernel(typename CxT<R>::T *__restrict__ A, int b0, int nb,
+                                                            int64_t nrows, int64_t ncols) {
   using C = typename CxT<R>::T;
-  const int64_t total = npairs * ncols;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t p = e / ncols, j = e - p * ncols;
-    const int64_t r0 = ((p >> bit) << (bit + 1)) | (p & ((1ll << bit) - 1)), r1 = r0 | (1ll << bit);
-    const C a = A[r0 * ncols + j], b = A[r1 * ncols + j];
-    C s, d;
-    s.x = (a.x + b.x) * (R)0.5;
-    s.y = (a.y + b.y) * (R)0.5;
-    d.x = (a.x - b.x) * (R)0.5;
-    d.y = (a.y - b.y) * (R)0.5;
-    A[r0 * ncols + j] = s;
-    A[r1 * ncols + j] = d;
+  extern __shared__ __align__(16) unsigned char wraw[];
+  C *sh = reinterpret_cast<C *>(wraw);  // [2^nb][16]
+  const int64_t ngroups = nrows >> nb;  // row groups: rows r = lo | (q << b0) | (hi << (b0 + nb))
+  const int64_t ncb = (ncols + 15) / 16;
+  const int64_t blk = blockIdx.x;
+  const int64_t grp = blk / ncb, cb = blk - grp * ncb;
+  const int64_t lo = grp & ((1ll << b0) - 1), hi = grp >> b0;
+  const int R2 = 1 << nb;
+  for (int e = threadIdx.x; e < R2 * 16; e += blockDim.x) {
+    const int q = e >> 4, c = e & 15;
+    const int64_t row = lo | ((int64_t)q << b0) | (hi << (b0 + nb)), col = cb * 16 + c;
+    C v{};
+    if (col < ncols) v = A[row * ncols + col];
+    sh[e] = v;
+  }
+  __syncthreads();
+  for (int bit = 0; bit < nb; ++bit) {
+    for (int e = threadIdx.x; e < R2 * 8; e += blockDim.x) {
+      const int p = e >> 4, c = e & 15;
+      const int q0 = ((p >> bit) << (bit + 1)) | (p & ((1 << bit) - 1)), q1 = q0 | (1 << bit);
+      const C a = sh[q0 * 16 + c], b = sh[q1 * 16 + c];
+      C s, d;
+      s.x = (a.x + b.x) * (R)0.5;
+      s.y = (a.y + b.y) * (R)0.5;
+      d.x = (a.x - b.x) * (R)0.5;
+      d.y = (a.y - b.y) * (R)0.5;
+      sh[q0 * 16 + c] = s;
+      sh[q1 * 16 + c] = d;
+    }
+    __syncthreads();
+  }
+  for (int e = threadIdx.x; e < R2 * 16; e += blockDim.x) {
+    const int q = e >> 4, c = e & 15;
+    const int64_t row = lo | ((int64_t)q << b0) | (hi << (b0 + nb)), col = cb * 16 + c;
+    if (col < ncols) A[row * ncols + col] = sh[e];
   }
 }
 
 cudaError_t launch_wht_rows(void *A, bool c128, int m, int64_t ncols, cudaStream_t s) {
-  const int64_t npairs = m > 0 ? (1ll << (m - 1)) : 0;
-  if (npairs == 0 || ncols <= 0) return cudaSuccess;
-  const int blocks = (int)std::min<int64_t>((npairs * ncols + 255) / 256, 148 * 16);
-  for (int bit = 0; bit < m; ++bit) {
-    if (c128)
-      wht_rows_kernel<double><<<blocks, 256, 0, s>>>((double2 *)A, bit, npairs, ncols);
-    else
-      wht_rows_kernel<float><<<blocks, 256, 0, s>>>((float2 *)A, bit, npairs, ncols);
+  if (m <= 0 || ncols <= 0) return cudaSuccess;
+  const int64_t nrows = 1ll << m, ncb = (ncols + 15) / 16;
+  for (int b0 = 0; b0 < m; b0 += 8) {  // passes of up to 8 bits (2^8 rows x 16 columns x 16 B = 64 KB)
+    const int nb = std::min(8, m - b0);
+    const int64_t blocks = (nrows >> nb) * ncb;
+    const size_t sm = ((size_t)16 << nb) * (c128 ? 16 : 8);
+    if (c128) {
+      cudaFuncSetAttribute((const void *)wht_rows_smem_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           65536);
+      wht_rows_smem_kernel<double><<<(unsigned)blocks, 256, sm, s>>>((double2 *)A, b0, nb, nrows, ncols);
+    } else {
+      wht_rows_smem_kernel<float><<<(unsigned)blocks, 256, sm, s>>>((float2 *)A, b0, nb, nrows, ncols);
+    }
   }
   return cudaGetLastError();
 }
 
 // ---------------------------------------------------------------- leaves through frames
-template <typename R>
+// G = 0: term k reads psi[x ^ m_k] (scattered); G = 1: m_k indexes a row of the pre-gathered flips,
+// g[m_k * n + j] = psi[S[j] ^ flip] (coalesced: one scattered pass per distinct flip, launch_flip_rows)
+template <typename R, int G>
 __global__ void frame_gather_kernel(const typename CxT<R>::T *__restrict__ psi, const uint64_t *__restrict__ S,
                                     int64_t n, typename CxT<R>::T *__restrict__ out, const DiagDev pend,
                                     const __grid_constant__ FrameBatch b) {
@@ -114,14 +146,24 @@ __global__ void frame_gather_kernel(const typename CxT<R>::T *__restrict__ psi, 
     const int64_t i = e / n, j = e - i * n;
     const uint32_t x = (uint32_t)S[j];
     double sr = 0.0, si = 0.0;
-    for (int k = b.off[i]; k < b.off[i + 1]; ++k) {
-      const FrameTerm &f = b.term[k];
-      const C v = psi[x ^ f.m];
-      const int ph = (f.ph0 + __popc(x & f.t1) + 2 * __popc(x & f.t2) + 4 * __popc(x & f.zm)) & 7;
-      const double wr = c_omega[2 * ph] * f.cr - c_omega[2 * ph + 1] * f.ci;
-      const double wi = c_omega[2 * ph] * f.ci + c_omega[2 * ph + 1] * f.cr;
-      sr += (double)v.x * wr - (double)v.y * wi;
-      si += (double)v.x * wi + (double)v.y * wr;
+    // the terms' scattered reads are issued 8 at a time (independent loads in flight), then summed
+    const int k0 = b.off[i], k1 = b.off[i + 1];
+    for (int kb = k0; kb < k1; kb += 8) {
+      C v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (kb + u < k1)
+          v[u] = G ? __ldg(psi + (size_t)b.term[kb + u].m * (size_t)n + j) : __ldg(psi + (x ^ b.term[kb + u].m));
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        if (kb + u >= k1) break;
+        const FrameTerm &f = b.term[kb + u];
+        const int ph = (f.ph0 + __popc(x & f.t1) + 2 * __popc(x & f.t2) + 4 * __popc(x & f.zm)) & 7;
+        const double wr = c_omega[2 * ph] * f.cr - c_omega[2 * ph + 1] * f.ci;
+        const double wi = c_omega[2 * ph] * f.ci + c_omega[2 * ph + 1] * f.cr;
+        sr += (double)v[u].x * wr - (double)v[u].y * wi;
+        si += (double)v[u].x * wi + (double)v[u].y * wr;
+      }
     }
     if (pend.active) {
       const int ph = diag_phase(x, pend, pend.zm);
@@ -137,14 +179,43 @@ __global__ void frame_gather_kernel(const typename CxT<R>::T *__restrict__ psi, 
 }
 
 cudaError_t launch_frame_gather(const void *psi, const uint64_t *S, int64_t n, void *out, const FrameBatch &b,
-                                const DiagDev &pend, bool c128, cudaStream_t s) {
+                                const DiagDev &pend, bool c128, cudaStream_t s, bool from_rows) {
   const int64_t total = (int64_t)b.nleaf * n;
   if (total <= 0) return cudaSuccess;
   const int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 16);
+  if (c128) {
+    if (from_rows)
+      frame_gather_kernel<double, 1><<<blocks, 256, 0, s>>>((const double2 *)psi, S, n, (double2 *)out, pend, b);
+    else
+      frame_gather_kernel<double, 0><<<blocks, 256, 0, s>>>((const double2 *)psi, S, n, (double2 *)out, pend, b);
+  } else {
+    if (from_rows)
+      frame_gather_kernel<float, 1><<<blocks, 256, 0, s>>>((const float2 *)psi, S, n, (float2 *)out, pend, b);
+    else
+      frame_gather_kernel<float, 0><<<blocks, 256, 0, s>>>((const float2 *)psi, S, n, (float2 *)out, pend, b);
+  }
+  return cudaGetLastError();
+}
+
+template <typename R>
+__global__ void flip_rows_kernel(const typename CxT<R>::T *__restrict__ psi, const uint64_t *__restrict__ S, int64_t n,
+                                 const uint64_t *__restrict__ flips, int64_t nf, typename CxT<R>::T *__restrict__ g) {
+  const int64_t total = nf * n;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e / n, j = e - i * n;
+    g[e] = __ldg(psi + (S[j] ^ flips[i]));
+  }
+}
+
+cudaError_t launch_flip_rows(const void *psi, const uint64_t *S, int64_t n, const uint64_t *flips, int64_t nf, void *g,
+                             bool c128, cudaStream_t s) {
+  const int64_t total = nf * n;
+  if (total <= 0) return cudaSuccess;
+  const int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 32);
   if (c128)
-    frame_gather_kernel<double><<<blocks, 256, 0, s>>>((const double2 *)psi, S, n, (double2 *)out, pend, b);
+    flip_rows_kernel<double><<<blocks, 256, 0, s>>>((const double2 *)psi, S, n, flips, nf, (double2 *)g);
   else
-    frame_gather_kernel<float><<<blocks, 256, 0, s>>>((const float2 *)psi, S, n, (float2 *)out, pend, b);
+    flip_rows_kernel<float><<<blocks, 256, 0, s>>>((const float2 *)psi, S, n, flips, nf, (float2 *)g);
   return cudaGetLastError();
 }
 
@@ -526,11 +597,15 @@ __global__ void __launch_bounds__(256) branch_gemm_kernel(const typename CxT<R>:
 // cp.async ring of interleaved complex tiles [k][m] (row stride padded so that the fragment loads are
 // bank-conflict free: 66 double2 / 68 float2); tiles are visited in bands of 16 tile rows so that the
 // CTAs in flight share their U and L panels in L2.
-constexpr int G3_T = 64, G3_K = 16, G3_ST = 3, G3_BAND = 16;
-template <typename R>
-__host__ __device__ constexpr int g3_stride() { return sizeof(R) == 8 ? 66 : 68; }
-template <typename R>
-constexpr size_t g3_smem() { return (size_t)2 * G3_ST * G3_K * g3_stride<R>() * sizeof(typename CxT<R>::T); }
+constexpr int G3_BAND = 16;
+// row stride (elements) of a [k][m] tile of width W: 16-byte (double2) fragment loads are conflict free
+// when the stride is 2 mod 8 (in 16-byte units), 8-byte (float2) ones when it is 4 mod 16
+template <typename R, int W>
+__host__ __device__ constexpr int g3_stride() { return sizeof(R) == 8 ? W + 2 : W + 4; }
+template <typename R, int TM, int TN, int G3_K, int G3_ST>
+constexpr size_t g3_smem() {
+  return (size_t)G3_ST * G3_K * (g3_stride<R, TM>() + g3_stride<R, TN>()) * sizeof(typename CxT<R>::T);
+}
 
 template <int BYTES>
 __device__ __forceinline__ void cp_async_zfill(void *dst, const void *src, bool ok) {
@@ -542,40 +617,49 @@ __device__ __forceinline__ void cp_async_zfill(void *dst, const void *src, bool 
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(d), "l"(src), "r"(n) : "memory");
 }
 
-template <typename R>
-__global__ void __launch_bounds__(256, 1) branch_gemm3m_kernel(const typename CxT<R>::T *__restrict__ U,
-                                                               const typename CxT<R>::T *__restrict__ L,
-                                                               int64_t K, int64_t M, int64_t N,
-                                                               double *__restrict__ A, int tiles_m, int tiles_n) {
+// CTA tile TM x TN, 8 warps of (MT x 8) x (NT x 8) fragments, MINB CTAs per SM, K step G3_K, G3_ST stages
+template <typename R, int TM, int TN, int MT, int NT, int MINB, int G3_K, int G3_ST>
+__global__ void __launch_bounds__(256, MINB) branch_gemm3m_kernel(const typename CxT<R>::T *__restrict__ U,
+                                                                  const typename CxT<R>::T *__restrict__ L,
+                                                                  int64_t K, int64_t M, int64_t N,
+                                                                  double *__restrict__ A, int tiles_m, int tiles_n) {
   using C = typename CxT<R>::T;
-  constexpr int S = g3_stride<R>();
+  constexpr int SU = g3_stride<R, TM>(), SL = g3_stride<R, TN>();
+  constexpr int WN = TN / (NT * 8), WM = TM / (MT * 8);
+  static_assert(WM * WN == 8, "8 warps");
   extern __shared__ __align__(16) unsigned char g3_raw[];
   C *sU = reinterpret_cast<C *>(g3_raw);
-  C *sL = sU + G3_ST * G3_K * S;
+  C *sL = sU + G3_ST * G3_K * SU;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int wm = warp >> 2, wn = warp & 3;
+  const int wm = warp / WN, wn = warp % WN;
   // banded tile order
   const int pid = blockIdx.x, per_band = G3_BAND * tiles_n, band = pid / per_band;
   const int first = band * G3_BAND, rows = min(tiles_m - first, G3_BAND), in = pid - band * per_band;
-  const int64_t m0 = (int64_t)(first + in % rows) * G3_T, n0 = (int64_t)(in / rows) * G3_T;
+  const int64_t m0 = (int64_t)(first + in % rows) * TM, n0 = (int64_t)(in / rows) * TN;
 
   auto load = [&](int st, int64_t k0) {
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int e = tid + q * 256;  // 0..1023 = 16 x 64
-      const int kk = e >> 6, mm = e & 63;
+    for (int q = 0; q < G3_K * TM / 256; ++q) {
+      const int e = tid + q * 256;
+      const int kk = e / TM, mm = e % TM;
       const int64_t k = k0 + kk;
-      const bool okk = k < K;
-      const bool oku = okk && m0 + mm < M, okl = okk && n0 + mm < N;
-      cp_async_zfill<sizeof(C)>(sU + (st * G3_K + kk) * S + mm, oku ? (const void *)(U + k * M + m0 + mm) : (const void *)U, oku);
-      cp_async_zfill<sizeof(C)>(sL + (st * G3_K + kk) * S + mm, okl ? (const void *)(L + k * N + n0 + mm) : (const void *)L, okl);
+      const bool ok = k < K && m0 + mm < M;
+      cp_async_zfill<sizeof(C)>(sU + (st * G3_K + kk) * SU + mm, ok ? (const void *)(U + k * M + m0 + mm) : (const void *)U, ok);
+    }
+#pragma unroll
+    for (int q = 0; q < G3_K * TN / 256; ++q) {
+      const int e = tid + q * 256;
+      const int kk = e / TN, nn = e % TN;
+      const int64_t k = k0 + kk;
+      const bool ok = k < K && n0 + nn < N;
+      cp_async_zfill<sizeof(C)>(sL + (st * G3_K + kk) * SL + nn, ok ? (const void *)(L + k * N + n0 + nn) : (const void *)L, ok);
     }
   };
-  double t1[4][2][2], t2[4][2][2], t3[4][2][2];
+  double t1[MT][NT][2], t2[MT][NT][2], t3[MT][NT][2];
 #pragma unroll
-  for (int a = 0; a < 4; ++a)
+  for (int a = 0; a < MT; ++a)
 #pragma unroll
-    for (int b = 0; b < 2; ++b)
+    for (int b = 0; b < NT; ++b)
 #pragma unroll
       for (int c = 0; c < 2; ++c) t1[a][b][c] = t2[a][b][c] = t3[a][b][c] = 0.0;
 
@@ -591,29 +675,29 @@ __global__ void __launch_bounds__(256, 1) branch_gemm3m_kernel(const typename Cx
     if (kb + G3_ST - 1 < nk) load((int)((kb + G3_ST - 1) % G3_ST), (kb + G3_ST - 1) * G3_K);
     asm volatile("cp.async.commit_group;" ::: "memory");
     const int st = (int)(kb % G3_ST);
-    const C *tu = sU + st * G3_K * S, *tl = sL + st * G3_K * S;
+    const C *tu = sU + st * G3_K * SU, *tl = sL + st * G3_K * SL;
 #pragma unroll
     for (int ks = 0; ks < G3_K; ks += 4) {
       const int kr = ks + (lane & 3);
-      double ar[4], ai[4], as[4], br[2], bi[2], bs[2];
+      double ar[MT], ai[MT], as[MT], br[NT], bi[NT], bs[NT];
 #pragma unroll
-      for (int mt = 0; mt < 4; ++mt) {
-        const C u = tu[kr * S + wm * 32 + mt * 8 + (lane >> 2)];
+      for (int mt = 0; mt < MT; ++mt) {
+        const C u = tu[kr * SU + wm * MT * 8 + mt * 8 + (lane >> 2)];
         ar[mt] = (double)u.x;
         ai[mt] = (double)u.y;
         as[mt] = ar[mt] + ai[mt];
       }
 #pragma unroll
-      for (int nt = 0; nt < 2; ++nt) {
-        const C l = tl[kr * S + wn * 16 + nt * 8 + (lane >> 2)];
+      for (int nt = 0; nt < NT; ++nt) {
+        const C l = tl[kr * SL + wn * NT * 8 + nt * 8 + (lane >> 2)];
         br[nt] = (double)l.x;
         bi[nt] = (double)l.y;
         bs[nt] = br[nt] + bi[nt];
       }
 #pragma unroll
-      for (int mt = 0; mt < 4; ++mt)
+      for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
-        for (int nt = 0; nt < 2; ++nt) {
+        for (int nt = 0; nt < NT; ++nt) {
           dmma(t1[mt][nt], ar[mt], br[nt]);
           dmma(t2[mt][nt], ai[mt], bi[nt]);
           dmma(t3[mt][nt], as[mt], bs[nt]);
@@ -622,13 +706,13 @@ __global__ void __launch_bounds__(256, 1) branch_gemm3m_kernel(const typename Cx
   }
   asm volatile("cp.async.wait_group 0;" ::: "memory");
 #pragma unroll
-  for (int mt = 0; mt < 4; ++mt)
+  for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
-    for (int nt = 0; nt < 2; ++nt)
+    for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
       for (int c = 0; c < 2; ++c) {
-        const int64_t m = m0 + wm * 32 + mt * 8 + (lane >> 2);
-        const int64_t n = n0 + wn * 16 + nt * 8 + (lane & 3) * 2 + c;
+        const int64_t m = m0 + wm * MT * 8 + mt * 8 + (lane >> 2);
+        const int64_t n = n0 + wn * NT * 8 + nt * 8 + (lane & 3) * 2 + c;
         if (m < M && n < N) {
           double *a = A + 2 * (m * N + n);
           a[0] += t1[mt][nt][c] - t2[mt][nt][c];
@@ -637,21 +721,33 @@ __global__ void __launch_bounds__(256, 1) branch_gemm3m_kernel(const typename Cx
       }
 }
 
-template <typename R>
+template <typename R, int TM, int TN, int MT, int NT, int MINB, int KS = 16, int ST = 3>
 static cudaError_t launch_gemm3m(const void *U, const void *L, int64_t K, int64_t M, int64_t N, double *A,
                                  cudaStream_t s) {
   static bool attr = false;
+  auto *fn = branch_gemm3m_kernel<R, TM, TN, MT, NT, MINB, KS, ST>;
+  constexpr size_t smem = g3_smem<R, TM, TN, KS, ST>();
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute((const void *)branch_gemm3m_kernel<R>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g3_smem<R>());
+    cudaError_t e = cudaFuncSetAttribute((const void *)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  const int tm = (int)((M + G3_T - 1) / G3_T), tn = (int)((N + G3_T - 1) / G3_T);
+  const int tm = (int)((M + TM - 1) / TM), tn = (int)((N + TN - 1) / TN);
   using C = typename CxT<R>::T;
-  branch_gemm3m_kernel<R><<<(unsigned)((int64_t)tm * tn), 256, g3_smem<R>(), s>>>((const C *)U, (const C *)L, K, M, N,
-                                                                                     A, tm, tn);
+  fn<<<(unsigned)((int64_t)tm * tn), 256, smem, s>>>((const C *)U, (const C *)L, K, M, N, A, tm, tn);
   return cudaGetLastError();
+}
+
+template <typename R>
+static cudaError_t launch_gemm3m_cfg(const void *U, const void *L, int64_t K, int64_t M, int64_t N, double *A,
+                                     cudaStream_t s) {
+  // QSIM_GEMM_CFG (A/B): 0 = 64x64 tile, 32x16 warps, 1 CTA/SM, K step 16, 3 stages; 1 = K step 32
+  static const int cfg = std::getenv("QSIM_GEMM_CFG") ? std::atoi(std::getenv("QSIM_GEMM_CFG")) : 0;
+  // (measured on B200, K = 16384, M = N = 8192: 64x32 / 32x64 tiles with 2 CTAs per SM 28.3 / 28.2, K steps of
+  // 32 with 2 / 3 stages 29.3 / 29.4, 4 stages of 16 29.0, this one 29.0 TF/s executed: the DMMA pipe, not
+  // occupancy or the pipeline depth, is the limit; profiles/r02/r02x_gemm_configs.txt)
+  if (cfg == 1) return launch_gemm3m<R, 64, 64, 4, 2, 1, 32, 3>(U, L, K, M, N, A, s);
+  return launch_gemm3m<R, 64, 64, 4, 2, 1>(U, L, K, M, N, A, s);
 }
 
 cudaError_t launch_branch_gemm(const void *U, const void *L, int64_t K, int64_t M, int64_t N,
@@ -660,7 +756,7 @@ cudaError_t launch_branch_gemm(const void *U, const void *L, int64_t K, int64_t 
   // A/B: QSIM_GEMM=4m runs the four-product kernel below.  (An m16n8k8 form was measured equal: ptxas
   // splits it into the same DMMA.8x8x4 instructions, the only FP64 MMA of sm_100a.)
   static const bool four = std::getenv("QSIM_GEMM") && std::string(std::getenv("QSIM_GEMM")) == "4m";
-  if (!four) return c128 ? launch_gemm3m<double>(U, L, K, M, N, A, s) : launch_gemm3m<float>(U, L, K, M, N, A, s);
+  if (!four) return c128 ? launch_gemm3m_cfg<double>(U, L, K, M, N, A, s) : launch_gemm3m_cfg<float>(U, L, K, M, N, A, s);
   dim3 grid((unsigned)((N + GB_N - 1) / GB_N), (unsigned)((M + GB_M - 1) / GB_M));
   if (c128)
     branch_gemm_kernel<double><<<grid, 256, 0, s>>>((const double2 *)U, (const double2 *)L, K, M, N, A, 0, 0, 0);
