@@ -2465,7 +2465,7 @@ void Engine::evolve_block(int half, uint64_t b0, int m, void *slice, const uint6
   if (std::find(eff.begin(), eff.end(), 0) == eff.end()) eff.clear();
   std::vector<int> pin(c, -1);
   for (int g = 0; g < c - m; ++g) pin[g] = (int)((b0 >> (c - 1 - g)) & 1u);
-  if (flip && !bfs) {  // sibling flips (run_tree_flip); false: not applicable, the executor below
+  if (flip && (!bfs || frames_)) {  // frames / sibling flips; false: not applicable, the executors below
     const TreeChoice fc = flip_choice(half, m);
     const TreeVariant &fv = variant(half, fc.apply, eff);
     if (std::getenv("QSIM_DEBUG_TREE")) {
@@ -2474,7 +2474,7 @@ void Engine::evolve_block(int half, uint64_t b0, int m, void *slice, const uint6
       std::fprintf(stderr, "\n");
     }
     if (frames_ && run_tree_frames(half, fv, pin, m, slice, dS, nS, nbuf)) return;
-    if (run_tree_flip(half, fv, lz, pin, m, slice, dS, nS, nbuf)) return;
+    if (!bfs && run_tree_flip(half, fv, lz, pin, m, slice, dS, nS, nbuf)) return;
   }
   const TreeChoice tc = choose_tree(half, m, lz, nS, nbuf, !bfs);
   const TreeVariant &v = variant(half, tc.apply, eff);
@@ -2710,8 +2710,9 @@ bool Engine::bfs_tree(const TreeVariant &v, int lz, int M, const std::vector<int
 bool Engine::flip_half(int half) const {
   const HalfExec &he = half_[half];
   if (!flip_ || !deferred_ || dist_ || !he.tree || sweep_kernel_ == 1 || he.prog.hl > 32) return false;
+  if (frames_) return true;  // the frame executor needs few sweeps at any state size
   const size_t sb = ((size_t)1 << he.prog.hl) * amp_;
-  return !(bfs_ && sb <= ((size_t)256 << 20));
+  return !(bfs_ && sb <= ((size_t)256 << 20));  // small states: level-synchronous subtrees
 }
 
 // every free cut forks at the input of its first target layer (latest placement; with sibling flips

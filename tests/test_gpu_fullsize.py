@@ -93,9 +93,12 @@ def run_ranges(circ, Su, Sl, ranges, prec, opts):
 @pytest.mark.parametrize("defer", [0, 1])
 @pytest.mark.parametrize("bfs", [0, 1])
 @pytest.mark.parametrize("lazy", [0, 2, 3, 4])
-def test_d22_h14_forks(prec, defer, bfs, lazy, d22_h14):
+@pytest.mark.parametrize("frames", [0, 1])
+def test_d22_h14_forks(prec, defer, bfs, lazy, frames, d22_h14, monkeypatch):
     """Deferred (default) and eager forks, depth-first and level-synchronous, lazy tail off / by the
-    cost model / forced to two / three stages (cones of cones)."""
+    cost model / forced to two / three stages (cones of cones); with the frame executor on (the default,
+    every state size) and off (the tree executors)."""
+    monkeypatch.setenv("QSIM_FRAMES", str(frames))
     circ, Su, Sl, ranges, ref = d22_h14
     A = run_ranges(circ, Su, Sl, ranges, prec,
                    {Q.QSIM_OPT_DEFER: defer, Q.QSIM_OPT_BFS: bfs, Q.QSIM_OPT_LAZY_LAST: lazy})
