@@ -55,7 +55,12 @@ def main():
             same = int(np.sum(x1 == x2))
             print(f"rank0 world={world} grid={grid}: draws identical to 1 GPU {same}/{x1.size}, "
                   f"W {W2:.15f} vs {W1:.15f}", flush=True)
-            ok = ok and same >= x1.size - 2 and abs(W2 - W1) <= 1e-12
+            # c128: the blocks differ by the ranks' summation order only; c64: also by the rounding of the
+            # lower rows' Walsh-Hadamard transform (R-zz), which spans each rank's block of free cuts
+            if prec == Q.QSIM_C128:
+                ok = ok and same >= x1.size - 2 and abs(W2 - W1) <= 1e-12
+            else:
+                ok = ok and same >= 0.999 * x1.size and abs(W2 - W1) <= 1e-6 * abs(W1)
             from oracle import partition as OP, sampler as OS
             ref = OP.amplitudes(circ, Su, Sl)
             err = np.abs(A.astype(np.complex128) - ref).max()
