@@ -143,7 +143,7 @@ qsim_status qsim_set_option(qsim_ctx *ctx, int key, int64_t value);
 qsim_status qsim_set_stream(qsim_ctx *ctx, void *cuda_stream);
 
 /* qsim_load_circuit — the circuit and its bipartition (P:285-311 Supp. A).
- *  rows, cols: grid (n = rows*cols <= 64);  depth: number of gate layers;
+ *  rows, cols: grid (n = rows*cols <= 72; halves above 32 qubits need QSIM_OPT_DISTRIBUTE);  depth: number of gate layers;
  *  gates[n_gates]: host array, any order; each qubit at most once per layer;
  *    CZ only between grid neighbours; single-qubit gates: SX, SY, T.
  *  cut_row: upper half = rows [0, cut_row); 0 = rows/2.  Both halves must have
@@ -194,7 +194,8 @@ qsim_status qsim_amplitudes(qsim_ctx *ctx, const uint64_t *upper_block, size_t n
  * Philox4x32-10 (key = seed) and the two-level inverse CDF of SURVEY §8(c):
  *  bitstrings: host uint64[n_draws], x = (S_u[i] << h_l) | S_l[j]; NULL = keep on device.
  *  block_mass: host double (nullable) = W = sum of p over the block.
- *  ENUMERIC if W == 0.  With a communicator only rank 0 draws and writes outputs. */
+ *  ENUMERIC if W == 0; EINVAL for circuits above 64 qubits (x does not fit; use qsim_amplitudes).
+ *  With a communicator the row shards are sampled on their ranks and rank 0 writes the outputs. */
 qsim_status qsim_sample(qsim_ctx *ctx, uint64_t seed, size_t n_draws, uint64_t *bitstrings,
                         double *block_mass);
 

@@ -1398,6 +1398,67 @@ void Engine::gemm(const void *U, const void *L, int64_t K, int64_t M, int64_t N,
   st_.gemm_flops += 8.0 * (double)M * (double)N * (double)K;
 }
 
+// Half pairs (r2, multi-GPU): with the frame executor each half needs one real state for any
+// branch range, so ranks 2i and 2i+1 split the two halves instead of both computing both: each evolves one
+// half over the pair's joint range, the rows of the partner's range are swapped (ncclSend / ncclRecv), and
+// each contracts its own range.  false: not applicable (the range is not this rank's own, an odd world,
+// unequal or non-adjacent partner ranges, a half without frames, or the rows do not fit).
+bool Engine::evolve_pair(uint64_t b0, uint64_t b1) {
+  if (!pairs_ || dist_ || world_ < 2 || (world_ & 1) || !frames_ || !deferred_) return false;
+  if (!flip_half(0) || !flip_half(1)) return false;
+  uint64_t r0 = 0, r1 = 0, p0 = 0, p1 = 0;
+  rank_range_of(rank_, &r0, &r1);
+  rank_range_of(rank_ ^ 1, &p0, &p1);
+  if (r0 != b0 || r1 != b1 || p1 - p0 != b1 - b0 || (p1 != b0 && p0 != b1)) return false;
+  const int h = rank_ & 1;  // even ranks: the upper half, odd ranks: the lower half
+  const uint64_t lo = std::min(b0, p0), hi = std::max(b1, p1), K = b1 - b0;
+  const int64_t nu = (int64_t)Su_.size(), nl = (int64_t)Sl_.size();
+  const int64_t nh = h == 0 ? nu : nl, no = h == 0 ? nl : nu;
+  const size_t mine = (size_t)(hi - lo) * (size_t)nh * amp_, theirs = (size_t)K * (size_t)no * amp_;
+  size_t free_b = 0, total_b = 0;
+  check(cudaMemGetInfo(&free_b, &total_b), "cudaMemGetInfo");
+  size_t have = U_.bytes + L_.bytes;
+  for (auto *b : states_) have += b->bytes;
+  const size_t st = ((size_t)1 << half_[h].prog.hl) * amp_;
+  if (mine + theirs + 2 * st + ((size_t)3 << 30) > free_b + have) return false;
+  DevBuf &P = h == 0 ? U_ : L_, &Q = h == 0 ? L_ : U_;
+  if (P.bytes < mine || Q.bytes < theirs) {
+    for (auto *b : states_) b->release();
+    U_.release();
+    L_.release();
+  }
+  P.reserve(mine);
+  Q.reserve(theirs);
+  const bool zz = flip_half(0);
+  evolve_tree(h, lo, hi, P.ptr, d_Sp_[h].as<uint64_t>(), nh, false, true, zz);
+  if (zz && h == 1) {  // the same aligned blocks as evolve_tree
+    const int c = (int)circ_.cuts.size();
+    for (uint64_t a = lo; a < hi;) {
+      int m = 0;
+      while (m < c && ((a >> m) & 1u) == 0 && a + (2ull << m) <= hi) ++m;
+      check(launch_wht_rows((char *)P.ptr + (size_t)(a - lo) * (size_t)nh * amp_, c128_, m, nh, stream_),
+            "wht launch");
+      st_.kernel_launches += (uint64_t)((m + 7) / 8);
+      a += 1ull << m;
+    }
+  }
+  ensure_comm();
+  const ncclDataType_t dt = c128_ ? ncclDouble : ncclFloat;
+  ncclGroupStart();
+  ncclResult_t r1s = ncclSend((const char *)P.ptr + (size_t)(p0 - lo) * (size_t)nh * amp_, (size_t)K * (size_t)nh * 2,
+                              dt, rank_ ^ 1, comm_, stream_);
+  ncclResult_t r2s = ncclRecv(Q.ptr, (size_t)K * (size_t)no * 2, dt, rank_ ^ 1, comm_, stream_);
+  ncclResult_t r3s = ncclGroupEnd();
+  if (r1s != ncclSuccess || r2s != ncclSuccess || r3s != ncclSuccess)
+    throw Error(QSIM_ENCCL, std::string("pair row exchange: ") + ncclGetErrorString(r3s != ncclSuccess ? r3s : r1s));
+  const void *own = (const char *)P.ptr + (size_t)(b0 - lo) * (size_t)nh * amp_;
+  gemm(h == 0 ? own : Q.ptr, h == 0 ? Q.ptr : own, (int64_t)K, nu, nl, A_acc_.as<double>());
+  st_.branches_evolved += K;
+  check(cudaGetLastError(), "evolve");
+  reduced_ = false;
+  return true;
+}
+
 void Engine::evolve_range(uint64_t b0, uint64_t b1) {
   Nvtx nv("qsim_evolve_range");
   if (!have_circuit_) throw Error(QSIM_ESTATE, "no circuit loaded");
@@ -1419,6 +1480,8 @@ void Engine::evolve_range(uint64_t b0, uint64_t b1) {
     if (he.tree && he.prog.h < T) throw Error(QSIM_EINVAL, "tree mode needs h >= 13 (c64) / 12 (c128)");
     if (!he.tree && he.prog.h > small_max_h(c128_)) throw Error(QSIM_EINVAL, "flat mode needs h <= 12");
   }
+  if (!roles_chosen_ && deferred_) choose_roles();
+  if (evolve_pair(b0, b1)) return;
   const int64_t nu = (int64_t)Su_.size(), nl = (int64_t)Sl_.size();
   // slices for a chunk of branches (bounded at 1 GiB per half)
   const uint64_t per_branch = (uint64_t)std::max(nu, nl) * amp_;
@@ -1591,6 +1654,7 @@ void Engine::run_sampler(const double *A, const double *p, int64_t M, int64_t N,
 void Engine::sample(uint64_t seed, size_t n, uint64_t *out, double *mass) {
   Nvtx nv("qsim_sample");
   if (!have_blocks_) throw Error(QSIM_ESTATE, "no blocks evolved");
+  if (circ_.n > 64) throw Error(QSIM_EINVAL, "outcomes of more than 64 qubits do not fit a 64-bit draw (qsim_amplitudes)");
   ensure_device();
   const int64_t M = (int64_t)Su_.size(), N = (int64_t)Sl_.size();
   if (world_ == 1) {
@@ -1892,7 +1956,9 @@ void Engine::ensure_comm() {
   if (r != ncclSuccess) throw Error(QSIM_ENCCL, std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
 }
 
-void Engine::rank_range(uint64_t *b0, uint64_t *b1) const {
+void Engine::rank_range(uint64_t *b0, uint64_t *b1) const { rank_range_of(rank_, b0, b1); }
+
+void Engine::rank_range_of(int rank, uint64_t *b0, uint64_t *b1) const {
   if (!have_circuit_) throw Error(QSIM_ESTATE, "no circuit loaded");
   const int c = (int)circ_.cuts.size();
   if (c > 62) throw Error(QSIM_EINVAL, "too many cuts");
@@ -1907,12 +1973,12 @@ void Engine::rank_range(uint64_t *b0, uint64_t *b1) const {
   for (size_t i = 0; i < circ_.fork_layers.size() && i < 2; ++i) gbits += circ_.fork_k[i];
   const uint64_t G = 1ull << gbits, per = (uint64_t)(B >> gbits);
   if ((uint64_t)world_ <= G) {
-    *b0 = G * (uint64_t)rank_ / (uint64_t)world_ * per;
-    *b1 = G * (uint64_t)(rank_ + 1) / (uint64_t)world_ * per;
+    *b0 = G * (uint64_t)rank / (uint64_t)world_ * per;
+    *b1 = G * (uint64_t)(rank + 1) / (uint64_t)world_ * per;
     return;
   }
-  *b0 = (uint64_t)(B * (unsigned)rank_ / (unsigned)world_);
-  *b1 = (uint64_t)(B * (unsigned)(rank_ + 1) / (unsigned)world_);
+  *b0 = (uint64_t)(B * (unsigned)rank / (unsigned)world_);
+  *b1 = (uint64_t)(B * (unsigned)(rank + 1) / (unsigned)world_);
 }
 
 // ---------------------------------------------------------------- cost model

@@ -120,6 +120,7 @@ class Engine {
   void info(qsim_info_t *out) const;
   void comm_init(int rank, int world, const void *id);
   void rank_range(uint64_t *b0, uint64_t *b1) const;
+  void rank_range_of(int rank, uint64_t *b0, uint64_t *b1) const;
   void cost_model(uint64_t nu, uint64_t nl, double hbm_gbps, qsim_cost_t *out);
   // multi-part partitions (Fig. 3)
   void multipart_plan(uint32_t n_parts, const uint32_t *row_cuts, uint32_t *part_qubits, uint32_t *boundary_cuts,
@@ -287,6 +288,9 @@ class Engine {
 
   // executor
   void evolve_half(int half, uint64_t b0, uint64_t b1, void *slice, const uint64_t *dS, int64_t nS);
+  // half pairs over two ranks (multi-GPU with the frame executor; QSIM_PAIRS=0: off, A/B)
+  bool evolve_pair(uint64_t b0, uint64_t b1);
+  bool pairs_ = !(std::getenv("QSIM_PAIRS") && std::getenv("QSIM_PAIRS")[0] == '0');
   // level-synchronous (BFS) variant for a whole tree whose two largest consecutive levels fit:
   // every sweep of level l runs once over all 2^{sbits_l} node states (node-batched TMA launch)
   int bfs_level(int half, int m0, size_t avail) const;

@@ -387,7 +387,8 @@ std::string build_circuit(uint32_t rows, uint32_t cols, uint32_t depth, const qs
                           size_t n_cut_layers, Circuit &out) {
   std::ostringstream err;
   if (rows < 2 || cols < 1) return "grid must have rows >= 2 and cols >= 1";
-  if ((uint64_t)rows * cols > 64) return "at most 64 qubits";
+  // 72 qubits: the paper's largest grids (Table 1, 36-qubit halves sharded over ranks)
+  if ((uint64_t)rows * cols > 72) return "at most 72 qubits";
   if (depth > 100000) return "depth too large";
   if (cut_row == 0) cut_row = rows / 2;
   if (cut_row < 1 || cut_row >= rows) return "cut_row must be in [1, rows)";

@@ -618,7 +618,10 @@ __device__ __forceinline__ void cp_async_zfill(void *dst, const void *src, bool 
 }
 
 // CTA tile TM x TN, 8 warps of (MT x 8) x (NT x 8) fragments, MINB CTAs per SM, K step G3_K, G3_ST stages
-template <typename R, int TM, int TN, int MT, int NT, int MINB, int G3_K, int G3_ST>
+// FULL: M, N, K are multiples of the tile (no bounds checks; per-thread source pointers advance by k).
+// (Forming the 3M sums once per element into real planes of the stage instead of per fragment was
+// measured slower, 27.3 vs 29.2 TF/s executed: profiles/r02/r02x_gemm_configs.txt.)
+template <typename R, int TM, int TN, int MT, int NT, int MINB, int G3_K, int G3_ST, bool FULL>
 __global__ void __launch_bounds__(256, MINB) branch_gemm3m_kernel(const typename CxT<R>::T *__restrict__ U,
                                                                   const typename CxT<R>::T *__restrict__ L,
                                                                   int64_t K, int64_t M, int64_t N,
@@ -637,7 +640,30 @@ __global__ void __launch_bounds__(256, MINB) branch_gemm3m_kernel(const typename
   const int first = band * G3_BAND, rows = min(tiles_m - first, G3_BAND), in = pid - band * per_band;
   const int64_t m0 = (int64_t)(first + in % rows) * TM, n0 = (int64_t)(in / rows) * TN;
 
+  constexpr int QU = G3_K * TM / 256, QL = G3_K * TN / 256;
+  const C *gU[QU], *gL[QL];
+  int oU[QU], oL[QL];
+#pragma unroll
+  for (int q = 0; q < QU; ++q) {
+    const int e = tid + q * 256, kk = e / TM, mm = e % TM;
+    gU[q] = U + (int64_t)kk * M + m0 + mm;
+    oU[q] = kk * SU + mm;
+  }
+#pragma unroll
+  for (int q = 0; q < QL; ++q) {
+    const int e = tid + q * 256, kk = e / TN, nn = e % TN;
+    gL[q] = L + (int64_t)kk * N + n0 + nn;
+    oL[q] = kk * SL + nn;
+  }
   auto load = [&](int st, int64_t k0) {
+    if constexpr (FULL) {
+      const int64_t du = k0 * M, dl = k0 * N;
+#pragma unroll
+      for (int q = 0; q < QU; ++q) cp_async_zfill<sizeof(C)>(sU + st * G3_K * SU + oU[q], gU[q] + du, true);
+#pragma unroll
+      for (int q = 0; q < QL; ++q) cp_async_zfill<sizeof(C)>(sL + st * G3_K * SL + oL[q], gL[q] + dl, true);
+      return;
+    }
 #pragma unroll
     for (int q = 0; q < G3_K * TM / 256; ++q) {
       const int e = tid + q * 256;
@@ -671,10 +697,10 @@ __global__ void __launch_bounds__(256, MINB) branch_gemm3m_kernel(const typename
   }
   for (int64_t kb = 0; kb < nk; ++kb) {
     asm volatile("cp.async.wait_group %0;" ::"n"(G3_ST - 2) : "memory");
+    const int st = (int)(kb % G3_ST);
     __syncthreads();
     if (kb + G3_ST - 1 < nk) load((int)((kb + G3_ST - 1) % G3_ST), (kb + G3_ST - 1) * G3_K);
     asm volatile("cp.async.commit_group;" ::: "memory");
-    const int st = (int)(kb % G3_ST);
     const C *tu = sU + st * G3_K * SU, *tl = sL + st * G3_K * SL;
 #pragma unroll
     for (int ks = 0; ks < G3_K; ks += 4) {
@@ -682,14 +708,16 @@ __global__ void __launch_bounds__(256, MINB) branch_gemm3m_kernel(const typename
       double ar[MT], ai[MT], as[MT], br[NT], bi[NT], bs[NT];
 #pragma unroll
       for (int mt = 0; mt < MT; ++mt) {
-        const C u = tu[kr * SU + wm * MT * 8 + mt * 8 + (lane >> 2)];
+        const int mm = wm * MT * 8 + mt * 8 + (lane >> 2);
+        const C u = tu[kr * SU + mm];
         ar[mt] = (double)u.x;
         ai[mt] = (double)u.y;
         as[mt] = ar[mt] + ai[mt];
       }
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt) {
-        const C l = tl[kr * SL + wn * NT * 8 + nt * 8 + (lane >> 2)];
+        const int nn = wn * NT * 8 + nt * 8 + (lane >> 2);
+        const C l = tl[kr * SL + nn];
         br[nt] = (double)l.x;
         bi[nt] = (double)l.y;
         bs[nt] = br[nt] + bi[nt];
@@ -725,11 +753,16 @@ template <typename R, int TM, int TN, int MT, int NT, int MINB, int KS = 16, int
 static cudaError_t launch_gemm3m(const void *U, const void *L, int64_t K, int64_t M, int64_t N, double *A,
                                  cudaStream_t s) {
   static bool attr = false;
-  auto *fn = branch_gemm3m_kernel<R, TM, TN, MT, NT, MINB, KS, ST>;
+  const bool full = M % TM == 0 && N % TN == 0 && K % KS == 0;
+  auto *fn = full ? branch_gemm3m_kernel<R, TM, TN, MT, NT, MINB, KS, ST, true>
+                  : branch_gemm3m_kernel<R, TM, TN, MT, NT, MINB, KS, ST, false>;
   constexpr size_t smem = g3_smem<R, TM, TN, KS, ST>();
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute((const void *)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
+    for (auto *f : {branch_gemm3m_kernel<R, TM, TN, MT, NT, MINB, KS, ST, true>,
+                    branch_gemm3m_kernel<R, TM, TN, MT, NT, MINB, KS, ST, false>}) {
+      cudaError_t e = cudaFuncSetAttribute((const void *)f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return e;
+    }
     attr = true;
   }
   const int tm = (int)((M + TM - 1) / TM), tn = (int)((N + TN - 1) / TN);
