@@ -298,6 +298,50 @@ def test_porter_thomas_analyzer_oracle():
 
 
 @pytest.mark.parametrize("grid", [(4, 3, 12, 5), (4, 4, 16, 2)])
+def test_rzz_both_endpoints_z(grid):
+    """DESIGN.md R-zz: per cut CZ = sum_{a,b} H_ab Z^a (x) Z^b with H = [[1,1],[1,-1]]/2, so with Z on BOTH
+    endpoints of a block's free cuts (the block's fixed cuts keep P_b (x) Z^b) and the lower rows of each
+    block Walsh-Hadamard transformed over the free bits (1/2 per bit), the sum over all blocks of
+    sum_a V_a (x) (H L)_a is the direct state — and any split of the sum over a (half pairs over two
+    ranks) is a partition of the same terms."""
+    rows, cols, d, seed = grid
+    circ = generate(rows, cols, d, seed)
+    cuts = P.cut_list(circ)
+    c, hu = len(cuts), circ.h_upper
+    m = min(c, 3)  # free cuts per block: the last m
+
+    def half(half_i, b):
+        lo, hi = (0, hu) if half_i == 0 else (hu, circ.n)
+        out = [(l, k, q0 - lo, (q1 - lo) if k == 4 else 0) for (l, k, q0, q1) in circ.gates
+               if all(lo <= q < hi for q in ([q0] if k != 4 else [q0, q1]))]
+        for g, (layer, qu, ql) in enumerate(cuts):
+            bit = (b >> (c - 1 - g)) & 1
+            q = (qu if half_i == 0 else ql) - lo
+            if half_i == 0 and g < c - m:
+                out.append((layer, "P1" if bit else "P0", q, 0))
+            elif bit:
+                out.append((layer, "Z", q, 0))
+        return sorted(out, key=lambda g_: g_[0])
+
+    hl = circ.n - hu
+    A = np.zeros((1 << hu, 1 << hl), dtype=np.complex128)
+    split = np.zeros_like(A)
+    for blk in range(1 << (c - m)):
+        bs = [(blk << m) | a for a in range(1 << m)]
+        V = np.array([SV.run_gates(SV.initial_state(hu), hu, half(0, b)) for b in bs])
+        L = np.array([SV.run_gates(SV.initial_state(hl), hl, half(1, b)) for b in bs])
+        for t_ in range(m):  # Walsh-Hadamard over the free bits, 1/2 per bit
+            L = L.reshape(-1, 2, 1 << t_, 1 << hl)
+            L = np.stack([(L[:, 0] + L[:, 1]) / 2, (L[:, 0] - L[:, 1]) / 2], axis=1).reshape(1 << m, 1 << hl)
+        A += V.T @ L
+        split += V[: len(bs) // 2].T @ L[: len(bs) // 2]
+        split += V[len(bs) // 2:].T @ L[len(bs) // 2:]
+    ref = SV.simulate(circ)
+    assert np.abs(A.reshape(-1) - ref).max() < 1e-14
+    assert np.abs(split.reshape(-1) - ref).max() < 1e-14
+
+
+@pytest.mark.parametrize("grid", [(4, 3, 12, 5), (4, 4, 16, 2)])
 def test_eq1_read_both_ways(grid):
     """DESIGN.md R6': CZ = P0 (x) I + P1 (x) Z = I (x) P0 + Z (x) P1, so with the projector put on the
     lower endpoint of any subset of the cuts the branch sum is still the direct state (Eq. 1)."""
