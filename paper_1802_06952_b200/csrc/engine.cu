@@ -291,7 +291,10 @@ void Engine::compile_all() {
     } else if (half_[h].tree && half_[h].prog.h <= 32) {  // relabel qubits to physical bits (choose_perm)
       std::vector<double> lw;
       if (deferred_) lw = deferred_layer_weights(h, perm_ns_[h]);
-      const std::vector<int> perm = choose_perm(half_[h], perm_ns_[h], deferred_ ? &lw : nullptr);
+      // the frame executor gathers the leaves with direct reads (no lazy tail): no gather term
+      static const bool frames_w = !(std::getenv("QSIM_PERM_FRAMES") && std::getenv("QSIM_PERM_FRAMES")[0] == '0');
+      const bool frame_mode = deferred_ && frames_ && frames_w && flip_half(h);
+      const std::vector<int> perm = choose_perm(half_[h], frame_mode ? 0 : perm_ns_[h], deferred_ ? &lw : nullptr);
       bool ident = true;
       for (size_t b = 0; b < perm.size(); ++b) ident = ident && perm[b] == (int)b;
       if (!ident) {
@@ -416,9 +419,14 @@ std::vector<double> Engine::deferred_layer_weights(int half, int64_t nS) {
   // sibling flips: a level's first sweep runs once per parent, its later ones once per child, so the
   // sweep of layer t runs 2^{#forks applied before t} times; else 2^{#forks applied at or before t}
   const bool flip = flip_half(half);
-  const TreeChoice tc = flip ? flip_choice(half, c) : choose_tree(half, c, lz, nS, 6, true);
   std::vector<double> w(circ_.depth + 2, 0.0);
   const int S = (int)he.glayers.size();
+  static const bool frames_w = !(std::getenv("QSIM_PERM_FRAMES") && std::getenv("QSIM_PERM_FRAMES")[0] == '0');
+  if (flip && frames_ && frames_w) {  // the frame executor: every sweep runs once, on the one real state
+    for (int i = 0; i < S; ++i) w[he.glayers[i]] = 1.0;
+    return w;
+  }
+  const TreeChoice tc = flip ? flip_choice(half, c) : choose_tree(half, c, lz, nS, 6, true);
   for (int i = 0; i + lz < S; ++i) {
     const int t = he.glayers[i];
     int n = 0;

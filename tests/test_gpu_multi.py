@@ -56,9 +56,12 @@ def _host_gib():
 @pytest.mark.slow
 @pytest.mark.skipif(_ngpus() < 2, reason="needs >= 2 GPUs")
 @pytest.mark.skipif(_host_gib() < 150, reason="the oracle's 2^33 leaf needs 128 GiB of host memory")
+@pytest.mark.skipif(os.environ.get("QSIM_TEST_H33") != "1",
+                    reason="the oracle's 2^33 leaf takes ~40 min on 16 host cores (QSIM_TEST_H33=1); "
+                           "profiles/r02/r02z_dist_h33_leaf_parity.log")
 def test_distributed_halves_above_32_qubits():
     """66-qubit 6x11 grid: 33-qubit halves sharded over 2 GPUs (32-qubit shards, 64-bit host diagonals
-    restricted to each shard), depth 8: leaf values of branch 0 (upper) and B-1 (lower) vs the oracle's 2^33 leaves."""
+    restricted to each shard), depth 8: leaf values of branch 0 of the upper half vs the oracle's 2^33 leaf."""
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
            "--master-addr", "127.0.0.1", "--master-port", "29541", os.path.join(ROOT, "tools", "dist_big.py"),
            "check", "8"]
