@@ -1518,23 +1518,85 @@ void Engine::evolve_range(uint64_t b0, uint64_t b1) {
     // sibling flips need Z^b forks: in the upper half (P_b canonically) the blocks' free cuts then
     // take Z^b on both endpoints and the lower slices the Walsh-Hadamard transform (R-zz)
     const bool zz = flip_half(0) && deferred_;
+    // frame basis for the lower half (one rank, frame executor): the Walsh-Hadamard transform then goes to the
+    // upper rows (sum_a V_a (H L)_a = sum_b (H V)_b L_b, H symmetric) so that L stays a sparse combination
+    const uint64_t len = e - s;
+    const bool one_block = (len & (len - 1)) == 0 && (s & (len - 1)) == 0;  // evolve_tree runs it as one block
+    const bool basis = basis_enabled_ && zz && world_ == 1 && !dist_ && frames_ && flip_half(1) && half_[1].tree &&
+                       one_block;
+    bool basis_ok = false;
     for (int h = 0; h < 2; ++h) {
       void *sl = h == 0 ? U_.ptr : L_.ptr;
       const int64_t ns = h == 0 ? nu : nl;
+      if (h == 1 && basis) {
+        basis_on_ = true;
+        basis_rows_ = &L_;
+        basis_cap_ = (int64_t)(e - s);
+        basis_entries_.clear();
+        basis_T_ = 0;
+        basis_points_ = 0;
+        bool aborted = false;
+        try {
+          evolve_tree(h, s, e, sl, d_Sp_[h].as<uint64_t>(), ns, false, true, zz);
+        } catch (const BasisAbort &) {
+          aborted = true;
+        }
+        basis_on_ = false;
+        basis_ok = !aborted && basis_points_ == 1;
+        // basis_points_ == 0: another executor ran the block and wrote the leaf rows as usual
+        if (!aborted) continue;
+      }
       if (deferred_ && !dist_ && half_[h].tree)
         evolve_tree(h, s, e, sl, d_Sp_[h].as<uint64_t>(), ns, false, flip_half(h), zz);
       else
         evolve_half(h, s, e, sl, d_Sp_[h].as<uint64_t>(), ns);
     }
     if (zz) {  // the same aligned blocks as evolve_tree
+      DevBuf &W = basis ? U_ : L_;
+      const int64_t nw = basis ? nu : nl;
       for (uint64_t a = s; a < e;) {
         int m = 0;
         while (m < c && ((a >> m) & 1u) == 0 && a + (2ull << m) <= e) ++m;
-        check(launch_wht_rows((char *)L_.ptr + (size_t)(a - s) * (size_t)nl * amp_, c128_, m, nl, stream_),
+        check(launch_wht_rows((char *)W.ptr + (size_t)(a - s) * (size_t)nw * amp_, c128_, m, nw, stream_),
               "wht launch");
         st_.kernel_launches += (uint64_t)((m + 7) / 8);
         a += 1ull << m;
       }
+    }
+    if (basis_ok && basis_T_ > 0) {
+      // A += (C^T (H V))^T B: U'[t] = sum over the terms (b, t, c) of c (H V)_b, then the GEMM over the basis
+      const int64_t T = basis_T_;
+      std::vector<uint32_t> off((size_t)T + 1, 0), src(basis_entries_.size());
+      std::vector<double> coef(2 * basis_entries_.size());
+      for (const BasisEntry &x : basis_entries_) off[x.t + 1]++;
+      for (int64_t t = 0; t < T; ++t) off[t + 1] += off[t];
+      std::vector<uint32_t> pos(off.begin(), off.end() - 1);
+      for (const BasisEntry &x : basis_entries_) {
+        const uint32_t q = pos[x.t]++;
+        src[q] = x.row;
+        coef[2 * q] = x.cr;
+        coef[2 * q + 1] = x.ci;
+      }
+      basis_off_.reserve(off.size() * 4);
+      basis_src_.reserve(src.size() * 4);
+      basis_coef_.reserve(coef.size() * 8);
+      check(cudaMemcpyAsync(basis_off_.ptr, off.data(), off.size() * 4, cudaMemcpyHostToDevice, stream_), "basis off");
+      check(cudaMemcpyAsync(basis_src_.ptr, src.data(), src.size() * 4, cudaMemcpyHostToDevice, stream_), "basis src");
+      check(cudaMemcpyAsync(basis_coef_.ptr, coef.data(), coef.size() * 8, cudaMemcpyHostToDevice, stream_),
+            "basis coef");
+      // U' in the (now idle) state buffer of the lower half when it is large enough
+      const size_t ub = (size_t)T * (size_t)nu * amp_;
+      DevBuf *scratch = (!states_.empty() && states_[0]->bytes >= ub) ? states_[0] : &tmp_;
+      if (scratch == &tmp_) tmp_.reserve(ub);
+      check(launch_combine_rows(U_.ptr, nu, basis_off_.as<uint32_t>(), basis_src_.as<uint32_t>(), basis_coef_.ptr, T,
+                                scratch->ptr, c128_, stream_),
+            "combine rows launch");
+      st_.kernel_launches++;
+      check(cudaStreamSynchronize(stream_), "basis upload");  // off / src / coef are host temporaries
+      gemm(scratch->ptr, L_.ptr, T, nu, nl, A_acc_.as<double>());
+      st_.branches_evolved += e - s;
+      s = e;
+      continue;
     }
     if (dist_ && world_ > 1) {
       // §2.3.3: each rank gathered the sampled entries it owns (zeros elsewhere).  The lower

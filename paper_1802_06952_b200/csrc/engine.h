@@ -243,6 +243,21 @@ class Engine {
   // expansions of a breaking frame into a sum of frames per term (QSIM_FRAME_EXPAND; 0: real splits only)
   int expand_depth_ = std::getenv("QSIM_FRAME_EXPAND") ? std::atoi(std::getenv("QSIM_FRAME_EXPAND")) : 6;
   long long nterms_ = 0;
+  // frame basis (qsim_evolve_range, world 1): the lower half's leaves as sparse combinations of the rows of
+  // its distinct frames; the GEMM then contracts over those rows (QSIM_FRAME_BASIS=0: off, A/B)
+  struct BasisEntry {
+    uint32_t row, t;
+    double cr, ci;
+  };
+  struct BasisAbort {};
+  bool basis_enabled_ = !(std::getenv("QSIM_FRAME_BASIS") && std::getenv("QSIM_FRAME_BASIS")[0] == '0');
+  bool basis_on_ = false;
+  DevBuf *basis_rows_ = nullptr;
+  int64_t basis_cap_ = 0, basis_T_ = 0;
+  uint64_t basis_row0_ = 0;
+  int basis_points_ = 0;
+  std::vector<BasisEntry> basis_entries_;
+  DevBuf basis_off_, basis_src_, basis_coef_;
   // frame gathers through pre-gathered rows of the distinct flips (QSIM_FLIP_ROWS=0: scattered, A/B)
   bool flip_rows_ = !(std::getenv("QSIM_FLIP_ROWS") && std::getenv("QSIM_FLIP_ROWS")[0] == '0');
   DevBuf flip_rows_buf_, flip_idx_buf_;

@@ -197,6 +197,10 @@ struct RowMapDev {
   uint8_t pos[32];
 };
 cudaError_t launch_rowmap(uint32_t *out, int64_t n, const RowMapDev &rm, cudaStream_t s);
+// out[r][j] = sum_{e in [off[r], off[r+1])} coef[e] * in[src[e]][j] for r < nrows (complex rows of n entries of
+// the ctx precision, coef double2, fp64 sums): the frame basis' sparse combinations (Engine::evolve_range)
+cudaError_t launch_combine_rows(const void *in, int64_t n, const uint32_t *off, const uint32_t *src, const void *coef,
+                                int64_t nrows, void *out, bool c128, cudaStream_t s);
 // rows [0, 2^m) of a slice (ncols entries each, ctx precision): Walsh-Hadamard transform over the m
 // row-index bits with 1/2 per bit (m launches)
 cudaError_t launch_wht_rows(void *A, bool c128, int m, int64_t ncols, cudaStream_t s);

@@ -219,6 +219,48 @@ cudaError_t launch_flip_rows(const void *psi, const uint64_t *S, int64_t n, cons
   return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------- sparse row combination (frame basis)
+// out[r][j] = sum_{e in [off[r], off[r+1])} coef[e] * in[src[e]][j]  (complex, fp64 sums, ctx-precision rows)
+template <typename R>
+__global__ void __launch_bounds__(256) combine_rows_kernel(const typename CxT<R>::T *__restrict__ in, int64_t n,
+                                                           const uint32_t *__restrict__ off,
+                                                           const uint32_t *__restrict__ src,
+                                                           const double2 *__restrict__ coef,
+                                                           typename CxT<R>::T *__restrict__ out) {
+  using C = typename CxT<R>::T;
+  const int64_t r = blockIdx.y;
+  const uint32_t e0 = off[r], e1 = off[r + 1];
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
+    double sr = 0.0, si = 0.0;
+    for (uint32_t e = e0; e < e1; ++e) {
+      const C v = in[(int64_t)src[e] * n + j];
+      const double2 c = coef[e];
+      sr += c.x * (double)v.x - c.y * (double)v.y;
+      si += c.x * (double)v.y + c.y * (double)v.x;
+    }
+    C o;
+    o.x = (R)sr;
+    o.y = (R)si;
+    out[r * n + j] = o;
+  }
+}
+
+cudaError_t launch_combine_rows(const void *in, int64_t n, const uint32_t *off, const uint32_t *src, const void *coef,
+                                int64_t nrows, void *out, bool c128, cudaStream_t s) {
+  if (nrows <= 0 || n <= 0) return cudaSuccess;
+  for (int64_t r0 = 0; r0 < nrows; r0 += 65535) {  // grid.y <= 65535
+    const int64_t nr = std::min<int64_t>(65535, nrows - r0);
+    dim3 grid((unsigned)std::min<int64_t>((n + 255) / 256, 16), (unsigned)nr);
+    if (c128)
+      combine_rows_kernel<double><<<grid, 256, 0, s>>>((const double2 *)in, n, off + r0, src, (const double2 *)coef,
+                                                       (double2 *)out + r0 * n);
+    else
+      combine_rows_kernel<float><<<grid, 256, 0, s>>>((const float2 *)in, n, off + r0, src, (const double2 *)coef,
+                                                      (float2 *)out + r0 * n);
+  }
+  return cudaGetLastError();
+}
+
 // ---------------------------------------------------------------- node-batched leaves
 template <typename R>
 __global__ void gather_nodes_kernel(const typename CxT<R>::T *__restrict__ psi, uint64_t stride, int shift,

@@ -265,6 +265,7 @@ void Engine::evolve_tree(int half, uint64_t b0, uint64_t b1, void *slice, const 
     int m = 0;
     while (m < c && ((s >> m) & 1u) == 0 && s + (2ull << m) <= b1) ++m;
     static const std::vector<char> none;
+    basis_row0_ = s - b0;  // the block's first row in the slice (frame basis entries)
     // zz: Z^b on the upper endpoint of every free cut of the block (evolve_block keeps the fixed ones)
     const std::vector<char> zroles(zz && half == 0 ? (size_t)c : 0, 0);
     evolve_block(half, s, m, (char *)slice + (s - b0) * (uint64_t)nS * amp_, dS, nS,
@@ -1056,9 +1057,64 @@ bool Engine::run_tree_frames(int half, const TreeVariant &v, const std::vector<i
         st_.kernel_launches++;
         check(cudaStreamSynchronize(stream_), "flip rows");  // `flips` is a host temporary
       }
+      const DiagDev pend = to_dev(tail);
+      if (basis_on_) {
+        // basis mode (qsim_evolve_range, DESIGN.md §5 "Frame basis"): every distinct frame (t1, t2, zm, m)
+        // becomes ONE gathered row of the basis; each leaf is recorded as its terms' (row, basis, c w^ph0)
+        if (basis_points_++ > 0) throw BasisAbort();
+        struct KH {
+          size_t operator()(const std::array<uint64_t, 4> &k) const {
+            uint64_t h = 1469598103934665603ull;
+            for (uint64_t v : k) h = (h ^ v) * 1099511628211ull;
+            return (size_t)h;
+          }
+        };
+        static const double r2 = 0.70710678118654752440;
+        static const double W[8][2] = {{1, 0}, {r2, r2}, {0, 1}, {-r2, r2}, {-1, 0}, {-r2, -r2}, {0, -1}, {r2, -r2}};
+        std::unordered_map<std::array<uint64_t, 4>, uint32_t, KH> bidx;
+        std::vector<const FNode *> reps;
+        basis_entries_.reserve(basis_entries_.size() + nodes.size());
+        for (const FNode &n : nodes) {
+          const auto it = bidx.emplace(std::array<uint64_t, 4>{n.f.t1, n.f.t2, n.f.zm, n.f.m}, (uint32_t)reps.size());
+          if (it.second) reps.push_back(&n);
+          const int ph = n.f.ph0 & 7;
+          basis_entries_.push_back(BasisEntry{(uint32_t)(basis_row0_ + (n.bits & rmask)), it.first->second,
+                                              n.cr * W[ph][0] - n.ci * W[ph][1], n.cr * W[ph][1] + n.ci * W[ph][0]});
+          if (!n.f.identity()) st_.flip_siblings++;
+        }
+        if ((int64_t)reps.size() > basis_cap_) throw BasisAbort();
+        basis_T_ = (int64_t)reps.size();
+        check(cudaMemsetAsync(basis_rows_->ptr, 0, (size_t)basis_T_ * (size_t)nS * amp_, stream_), "zero basis rows");
+        FrameBatch fb;
+        fb.nleaf = 0;
+        fb.off[0] = 0;
+        for (size_t t = 0; t < reps.size(); ++t) {
+          const FNode &n = *reps[t];
+          FrameTerm &T = fb.term[fb.nleaf];
+          T.t1 = (uint32_t)n.f.t1;
+          T.t2 = (uint32_t)n.f.t2;
+          T.zm = (uint32_t)n.f.zm;
+          T.m = use_rows ? fidx[n.f.m] : (uint32_t)n.f.m;
+          T.ph0 = 0;
+          T.pad = 0;
+          T.cr = 1.0;
+          T.ci = 0.0;
+          fb.row[fb.nleaf] = (uint32_t)t;
+          fb.off[fb.nleaf + 1] = (uint16_t)(fb.nleaf + 1);
+          if (++fb.nleaf == kMaxBatchLeaves || t + 1 == reps.size()) {
+            check(launch_frame_gather(use_rows ? flip_rows_buf_.ptr : states_[raw]->ptr, dS, nS, basis_rows_->ptr, fb,
+                                      pend, c128_, stream_, use_rows),
+                  "basis gather launch");
+            st_.kernel_launches++;
+            fb.nleaf = 0;
+          }
+        }
+        if (std::getenv("QSIM_DEBUG_TREE"))
+          std::fprintf(stderr, "frame basis: %zu terms over %lld distinct frames\n", nodes.size(), (long long)basis_T_);
+        nodes.clear();
+      }
       std::stable_sort(nodes.begin(), nodes.end(),
                        [&](const FNode &a, const FNode &b) { return (a.bits & rmask) < (b.bits & rmask); });
-      const DiagDev pend = to_dev(tail);
       FrameBatch fb;
       fb.nleaf = 0;
       fb.off[0] = 0;
