@@ -1478,7 +1478,26 @@ void Engine::evolve_range(uint64_t b0, uint64_t b1) {
     if (!he.tree && he.prog.h > small_max_h(c128_)) throw Error(QSIM_EINVAL, "flat mode needs h <= 12");
   }
   if (!roles_chosen_ && deferred_) choose_roles();
-  if (evolve_pair(b0, b1)) return;
+  // shared basis (ranks <= QSIM_SHARED_BASIS_MAX, default 2): every rank evolves both halves
+  // over the union of the ranks' ranges (the frame executor needs one state per half for any range) and
+  // contracts its share of the frame basis; no data exchange.  Else half pairs, else the own range.
+  uint64_t own0 = b0, own1 = b1;
+  int share_r = 0, share_n = 1;
+  if (world_ >= 2 && world_ <= shared_basis_max_ && !dist_ && frames_ && basis_enabled_ && deferred_ &&
+      flip_half(0) && flip_half(1)) {
+    uint64_t r0 = 0, r1 = 0, g0 = 0, g1 = 0, x0 = 0, x1 = 0;
+    rank_range_of(rank_, &r0, &r1);
+    rank_range_of(0, &g0, &x0);
+    rank_range_of(world_ - 1, &x1, &g1);
+    const uint64_t len = g1 - g0;
+    if (r0 == b0 && r1 == b1 && (len & (len - 1)) == 0 && (g0 & (len - 1)) == 0) {
+      b0 = g0;
+      b1 = g1;
+      share_r = rank_;
+      share_n = world_;
+    }
+  }
+  if (share_n == 1 && evolve_pair(b0, b1)) return;
   const int64_t nu = (int64_t)Su_.size(), nl = (int64_t)Sl_.size();
   // slices for a chunk of branches (bounded at 1 GiB per half)
   const uint64_t per_branch = (uint64_t)std::max(nu, nl) * amp_;
@@ -1522,8 +1541,8 @@ void Engine::evolve_range(uint64_t b0, uint64_t b1) {
     // upper rows (sum_a V_a (H L)_a = sum_b (H V)_b L_b, H symmetric) so that L stays a sparse combination
     const uint64_t len = e - s;
     const bool one_block = (len & (len - 1)) == 0 && (s & (len - 1)) == 0;  // evolve_tree runs it as one block
-    const bool basis = basis_enabled_ && zz && world_ == 1 && !dist_ && frames_ && flip_half(1) && half_[1].tree &&
-                       one_block;
+    const bool basis = basis_enabled_ && zz && (world_ == 1 || share_n > 1) && !dist_ && frames_ && flip_half(1) &&
+                       half_[1].tree && one_block;
     bool basis_ok = false;
     for (int h = 0; h < 2; ++h) {
       void *sl = h == 0 ? U_.ptr : L_.ptr;
@@ -1564,10 +1583,18 @@ void Engine::evolve_range(uint64_t b0, uint64_t b1) {
       }
     }
     if (basis_ok && basis_T_ > 0) {
-      // A += (C^T (H V))^T B: U'[t] = sum over the terms (b, t, c) of c (H V)_b, then the GEMM over the basis
-      const int64_t T = basis_T_;
+      // A += (C^T (H V))^T B: U'[t] = sum over the terms (b, t, c) of c (H V)_b, then the GEMM over the basis;
+      // with a shared basis this rank takes the basis rows [t0, t1)
+      const int64_t Tall = basis_T_;
+      const int64_t t0 = Tall * share_r / share_n, t1 = Tall * (share_r + 1) / share_n, T = t1 - t0;
       std::vector<uint32_t> off((size_t)T + 1, 0), src(basis_entries_.size());
       std::vector<double> coef(2 * basis_entries_.size());
+      for (BasisEntry &x : basis_entries_) x.t = (x.t >= t0 && x.t < t1) ? (uint32_t)(x.t - t0) : ~0u;
+      basis_entries_.erase(std::remove_if(basis_entries_.begin(), basis_entries_.end(),
+                                          [](const BasisEntry &x) { return x.t == ~0u; }),
+                           basis_entries_.end());
+      src.resize(basis_entries_.size());
+      coef.resize(2 * basis_entries_.size());
       for (const BasisEntry &x : basis_entries_) off[x.t + 1]++;
       for (int64_t t = 0; t < T; ++t) off[t + 1] += off[t];
       std::vector<uint32_t> pos(off.begin(), off.end() - 1);
@@ -1593,8 +1620,18 @@ void Engine::evolve_range(uint64_t b0, uint64_t b1) {
             "combine rows launch");
       st_.kernel_launches++;
       check(cudaStreamSynchronize(stream_), "basis upload");  // off / src / coef are host temporaries
-      gemm(scratch->ptr, L_.ptr, T, nu, nl, A_acc_.as<double>());
+      gemm(scratch->ptr, (const char *)L_.ptr + (size_t)t0 * (size_t)nl * amp_, T, nu, nl, A_acc_.as<double>());
       st_.branches_evolved += e - s;
+      s = e;
+      continue;
+    }
+    if (share_n > 1) {  // the basis was not applicable: this rank contracts its own branch range only
+      const uint64_t a0 = std::max(s, own0), a1 = std::min(e, own1);
+      if (a1 > a0)
+        gemm((const char *)U_.ptr + (size_t)(a0 - s) * (size_t)nu * amp_,
+             (const char *)L_.ptr + (size_t)(a0 - s) * (size_t)nl * amp_, (int64_t)(a1 - a0), nu, nl,
+             A_acc_.as<double>());
+      st_.branches_evolved += a1 > a0 ? a1 - a0 : 0;
       s = e;
       continue;
     }

@@ -251,6 +251,7 @@ class Engine {
   };
   struct BasisAbort {};
   bool basis_enabled_ = !(std::getenv("QSIM_FRAME_BASIS") && std::getenv("QSIM_FRAME_BASIS")[0] == '0');
+  int shared_basis_max_ = std::getenv("QSIM_SHARED_BASIS_MAX") ? std::atoi(std::getenv("QSIM_SHARED_BASIS_MAX")) : 2;
   bool basis_on_ = false;
   DevBuf *basis_rows_ = nullptr;
   int64_t basis_cap_ = 0, basis_T_ = 0;
