@@ -530,7 +530,8 @@ def main():
                          "share_of_step": gemm_s / main_run["prof_step_s"] if main_run["prof_step_s"] else None,
                          "note": "achieved = executed real flops (6MNK: T1 = Ur Lr, T2 = Ui Li, T3 = (Ur+Ui)(Lr+Li)) / "
                                  "CUDA-event time of the GEMM launches in the profiling step; the 8MNK complex "
-                                 "convention of SURVEY 8(d) is achieved_8mnk_convention"},
+                                 "convention of SURVEY 8(d) is achieved_8mnk_convention; K is the number of frame-basis "
+                                 "rows of the lower half when the frame basis applies (41,472 for C5), else the branches"},
             "roofline_sweep": {"bound": "hbm", "achieved": moved, "peak": peak, "unit": "GB/s",
                          "frac": (moved / peak) if moved else None, "traffic": traffic,
                          "achieved_algorithmic": alg,
