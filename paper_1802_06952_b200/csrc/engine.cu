@@ -1561,7 +1561,7 @@ void Engine::evolve_range(uint64_t b0, uint64_t b1) {
           aborted = true;
         }
         basis_on_ = false;
-        basis_ok = !aborted && basis_points_ == 1;
+        basis_ok = !aborted && basis_points_ >= 1;
         // basis_points_ == 0: another executor ran the block and wrote the leaf rows as usual
         if (!aborted) continue;
       }
@@ -1581,6 +1581,40 @@ void Engine::evolve_range(uint64_t b0, uint64_t b1) {
         st_.kernel_launches += (uint64_t)((m + 7) / 8);
         a += 1ull << m;
       }
+    }
+    if (basis_ok && basis_T_ > 0 && share_n == 1 && basis_T_ >= (int64_t)(e - s)) {
+      // as many distinct frames as branches: no gain from the basis, the leaf rows L = C B are formed instead
+      const int64_t K = (int64_t)(e - s);
+      std::vector<uint32_t> off((size_t)K + 1, 0), src(basis_entries_.size());
+      std::vector<double> coef(2 * basis_entries_.size());
+      for (const BasisEntry &x : basis_entries_) off[x.row + 1]++;
+      for (int64_t r = 0; r < K; ++r) off[r + 1] += off[r];
+      std::vector<uint32_t> pos(off.begin(), off.end() - 1);
+      for (const BasisEntry &x : basis_entries_) {
+        const uint32_t q = pos[x.row]++;
+        src[q] = x.t;
+        coef[2 * q] = x.cr;
+        coef[2 * q + 1] = x.ci;
+      }
+      basis_off_.reserve(off.size() * 4);
+      basis_src_.reserve(src.size() * 4);
+      basis_coef_.reserve(coef.size() * 8);
+      check(cudaMemcpyAsync(basis_off_.ptr, off.data(), off.size() * 4, cudaMemcpyHostToDevice, stream_), "basis off");
+      check(cudaMemcpyAsync(basis_src_.ptr, src.data(), src.size() * 4, cudaMemcpyHostToDevice, stream_), "basis src");
+      check(cudaMemcpyAsync(basis_coef_.ptr, coef.data(), coef.size() * 8, cudaMemcpyHostToDevice, stream_),
+            "basis coef");
+      const size_t lb = (size_t)K * (size_t)nl * amp_;
+      DevBuf *scratch = (!states_.empty() && states_[0]->bytes >= lb) ? states_[0] : &tmp_;
+      if (scratch == &tmp_) tmp_.reserve(lb);
+      check(launch_combine_rows(L_.ptr, nl, basis_off_.as<uint32_t>(), basis_src_.as<uint32_t>(), basis_coef_.ptr, K,
+                                scratch->ptr, c128_, stream_),
+            "combine rows launch");
+      st_.kernel_launches++;
+      check(cudaStreamSynchronize(stream_), "basis upload");
+      gemm(U_.ptr, scratch->ptr, K, nu, nl, A_acc_.as<double>());
+      st_.branches_evolved += e - s;
+      s = e;
+      continue;
     }
     if (basis_ok && basis_T_ > 0) {
       // A += (C^T (H V))^T B: U'[t] = sum over the terms (b, t, c) of c (H V)_b, then the GEMM over the basis;

@@ -13,6 +13,7 @@
 #include <set>
 #include <sstream>
 #include <unordered_map>
+#include <unordered_set>
 
 namespace qsim {
 
@@ -815,6 +816,16 @@ bool Engine::run_tree_flip(int half, const TreeVariant &v, int lz, const std::ve
 // frames (x ^ m, phi).  In the App. A.1 circuits a Z inserted after the second cut period mostly
 // survives to the last layer, so a 256-branch block needs a handful of real states instead of one
 // per branch.  false: not applicable (a free projector fork, a pinned projector after a free fork).
+namespace {
+struct KeyHash4 {  // FNV-1a over a frame's bit planes and flip (frame basis keys)
+  size_t operator()(const std::array<uint64_t, 4> &k) const {
+    uint64_t h = 1469598103934665603ull;
+    for (uint64_t v : k) h = (h ^ v) * 1099511628211ull;
+    return (size_t)h;
+  }
+};
+}  // namespace
+
 bool Engine::run_tree_frames(int half, const TreeVariant &v, const std::vector<int> &pin, int m, void *slice,
                              const uint64_t *dS, int64_t nS, int nbuf) {
   const HalfProgram &hp = v.prog;
@@ -1058,17 +1069,21 @@ bool Engine::run_tree_frames(int half, const TreeVariant &v, const std::vector<i
         check(cudaStreamSynchronize(stream_), "flip rows");  // `flips` is a host temporary
       }
       const DiagDev pend = to_dev(tail);
+      if (basis_on_) {  // more distinct frames than the basis rows hold: gather the leaves (first point only)
+        std::unordered_set<std::array<uint64_t, 4>, KeyHash4> dk;
+        for (const FNode &n : nodes) dk.insert(std::array<uint64_t, 4>{n.f.t1, n.f.t2, n.f.zm, n.f.m});
+        if (basis_T_ + (int64_t)dk.size() > basis_cap_) {
+          if (basis_points_ > 0) throw BasisAbort();
+          basis_on_ = false;
+        }
+      }
       if (basis_on_) {
         // basis mode (qsim_evolve_range, DESIGN.md §5 "Frame basis"): every distinct frame (t1, t2, zm, m)
         // becomes ONE gathered row of the basis; each leaf is recorded as its terms' (row, basis, c w^ph0)
-        if (basis_points_++ > 0) throw BasisAbort();
-        struct KH {
-          size_t operator()(const std::array<uint64_t, 4> &k) const {
-            uint64_t h = 1469598103934665603ull;
-            for (uint64_t v : k) h = (h ^ v) * 1099511628211ull;
-            return (size_t)h;
-          }
-        };
+        // every gather point (a real state) appends its distinct frames after the rows of the earlier ones
+        basis_points_++;
+        const int64_t T0 = basis_T_;
+        using KH = KeyHash4;
         static const double r2 = 0.70710678118654752440;
         static const double W[8][2] = {{1, 0}, {r2, r2}, {0, 1}, {-r2, r2}, {-1, 0}, {-r2, -r2}, {0, -1}, {r2, -r2}};
         std::unordered_map<std::array<uint64_t, 4>, uint32_t, KH> bidx;
@@ -1078,13 +1093,14 @@ bool Engine::run_tree_frames(int half, const TreeVariant &v, const std::vector<i
           const auto it = bidx.emplace(std::array<uint64_t, 4>{n.f.t1, n.f.t2, n.f.zm, n.f.m}, (uint32_t)reps.size());
           if (it.second) reps.push_back(&n);
           const int ph = n.f.ph0 & 7;
-          basis_entries_.push_back(BasisEntry{(uint32_t)(basis_row0_ + (n.bits & rmask)), it.first->second,
+          basis_entries_.push_back(BasisEntry{(uint32_t)(basis_row0_ + (n.bits & rmask)), (uint32_t)(T0 + it.first->second),
                                               n.cr * W[ph][0] - n.ci * W[ph][1], n.cr * W[ph][1] + n.ci * W[ph][0]});
           if (!n.f.identity()) st_.flip_siblings++;
         }
-        if ((int64_t)reps.size() > basis_cap_) throw BasisAbort();
-        basis_T_ = (int64_t)reps.size();
-        check(cudaMemsetAsync(basis_rows_->ptr, 0, (size_t)basis_T_ * (size_t)nS * amp_, stream_), "zero basis rows");
+        if (T0 + (int64_t)reps.size() > basis_cap_) throw BasisAbort();
+        basis_T_ = T0 + (int64_t)reps.size();
+        char *brows = (char *)basis_rows_->ptr + (size_t)T0 * (size_t)nS * amp_;
+        check(cudaMemsetAsync(brows, 0, reps.size() * (size_t)nS * amp_, stream_), "zero basis rows");
         FrameBatch fb;
         fb.nleaf = 0;
         fb.off[0] = 0;
@@ -1102,8 +1118,8 @@ bool Engine::run_tree_frames(int half, const TreeVariant &v, const std::vector<i
           fb.row[fb.nleaf] = (uint32_t)t;
           fb.off[fb.nleaf + 1] = (uint16_t)(fb.nleaf + 1);
           if (++fb.nleaf == kMaxBatchLeaves || t + 1 == reps.size()) {
-            check(launch_frame_gather(use_rows ? flip_rows_buf_.ptr : states_[raw]->ptr, dS, nS, basis_rows_->ptr, fb,
-                                      pend, c128_, stream_, use_rows),
+            check(launch_frame_gather(use_rows ? flip_rows_buf_.ptr : states_[raw]->ptr, dS, nS, brows, fb, pend, c128_,
+                                      stream_, use_rows),
                   "basis gather launch");
             st_.kernel_launches++;
             fb.nleaf = 0;
