@@ -1069,12 +1069,17 @@ bool Engine::run_tree_frames(int half, const TreeVariant &v, const std::vector<i
         check(cudaStreamSynchronize(stream_), "flip rows");  // `flips` is a host temporary
       }
       const DiagDev pend = to_dev(tail);
-      if (basis_on_) {  // more distinct frames than the basis rows hold: gather the leaves (first point only)
-        std::unordered_set<std::array<uint64_t, 4>, KeyHash4> dk;
-        for (const FNode &n : nodes) dk.insert(std::array<uint64_t, 4>{n.f.t1, n.f.t2, n.f.zm, n.f.m});
-        if (basis_T_ + (int64_t)dk.size() > basis_cap_) {
-          if (basis_points_ > 0) throw BasisAbort();
-          basis_on_ = false;
+      std::unordered_map<std::array<uint64_t, 4>, uint32_t, KeyHash4> bidx;  // frame -> basis row
+      std::vector<const FNode *> reps;
+      if (basis_on_) {  // the distinct frames; more than the basis rows hold: gather the leaves (first point only)
+        for (const FNode &n : nodes) {
+          if (bidx.emplace(std::array<uint64_t, 4>{n.f.t1, n.f.t2, n.f.zm, n.f.m}, (uint32_t)reps.size()).second)
+            reps.push_back(&n);
+          if (basis_T_ + (int64_t)reps.size() > basis_cap_) {
+            if (basis_points_ > 0) throw BasisAbort();
+            basis_on_ = false;
+            break;
+          }
         }
       }
       if (basis_on_) {
@@ -1083,21 +1088,16 @@ bool Engine::run_tree_frames(int half, const TreeVariant &v, const std::vector<i
         // every gather point (a real state) appends its distinct frames after the rows of the earlier ones
         basis_points_++;
         const int64_t T0 = basis_T_;
-        using KH = KeyHash4;
         static const double r2 = 0.70710678118654752440;
         static const double W[8][2] = {{1, 0}, {r2, r2}, {0, 1}, {-r2, r2}, {-1, 0}, {-r2, -r2}, {0, -1}, {r2, -r2}};
-        std::unordered_map<std::array<uint64_t, 4>, uint32_t, KH> bidx;
-        std::vector<const FNode *> reps;
         basis_entries_.reserve(basis_entries_.size() + nodes.size());
         for (const FNode &n : nodes) {
-          const auto it = bidx.emplace(std::array<uint64_t, 4>{n.f.t1, n.f.t2, n.f.zm, n.f.m}, (uint32_t)reps.size());
-          if (it.second) reps.push_back(&n);
+          const uint32_t tb = bidx.find(std::array<uint64_t, 4>{n.f.t1, n.f.t2, n.f.zm, n.f.m})->second;
           const int ph = n.f.ph0 & 7;
-          basis_entries_.push_back(BasisEntry{(uint32_t)(basis_row0_ + (n.bits & rmask)), (uint32_t)(T0 + it.first->second),
+          basis_entries_.push_back(BasisEntry{(uint32_t)(basis_row0_ + (n.bits & rmask)), (uint32_t)(T0 + tb),
                                               n.cr * W[ph][0] - n.ci * W[ph][1], n.cr * W[ph][1] + n.ci * W[ph][0]});
           if (!n.f.identity()) st_.flip_siblings++;
         }
-        if (T0 + (int64_t)reps.size() > basis_cap_) throw BasisAbort();
         basis_T_ = T0 + (int64_t)reps.size();
         char *brows = (char *)basis_rows_->ptr + (size_t)T0 * (size_t)nS * amp_;
         check(cudaMemsetAsync(brows, 0, reps.size() * (size_t)nS * amp_, stream_), "zero basis rows");
