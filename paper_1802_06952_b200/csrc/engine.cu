@@ -1427,8 +1427,31 @@ bool Engine::evolve_pair(uint64_t b0, uint64_t b1) {
   P.reserve(mine);
   Q.reserve(theirs);
   const bool zz = flip_half(0);
-  evolve_tree(h, lo, hi, P.ptr, d_Sp_[h].as<uint64_t>(), nh, false, true, zz);
-  if (zz && h == 1) {  // the same aligned blocks as evolve_tree
+  // the frame basis over the pair range (the lower rank builds it): the Walsh-Hadamard rows
+  // then go to the upper side whatever the lower rank's outcome, since sum_a V_a (H L)_a = sum_b (H V)_b L_b
+  const uint64_t plen = hi - lo;
+  const bool use_basis = basis_enabled_ && zz && (plen & (plen - 1)) == 0 && (lo & (plen - 1)) == 0;
+  bool basis_ok = false;
+  if (h == 1 && use_basis) {
+    basis_on_ = true;
+    basis_rows_ = &P;
+    basis_cap_ = (int64_t)plen;
+    basis_entries_.clear();
+    basis_T_ = 0;
+    basis_points_ = 0;
+    bool aborted = false;
+    try {
+      evolve_tree(h, lo, hi, P.ptr, d_Sp_[h].as<uint64_t>(), nh, false, true, zz);
+    } catch (const BasisAbort &) {
+      aborted = true;
+    }
+    basis_on_ = false;
+    basis_ok = !aborted && basis_points_ >= 1 && basis_T_ >= 2;
+    if (aborted) evolve_tree(h, lo, hi, P.ptr, d_Sp_[h].as<uint64_t>(), nh, false, true, zz);
+  } else {
+    evolve_tree(h, lo, hi, P.ptr, d_Sp_[h].as<uint64_t>(), nh, false, true, zz);
+  }
+  if (zz && h == (use_basis ? 0 : 1)) {  // the same aligned blocks as evolve_tree
     const int c = (int)circ_.cuts.size();
     for (uint64_t a = lo; a < hi;) {
       int m = 0;
@@ -1441,6 +1464,110 @@ bool Engine::evolve_pair(uint64_t b0, uint64_t b1) {
   }
   ensure_comm();
   const ncclDataType_t dt = c128_ ? ncclDouble : ncclFloat;
+  auto nccl_ok = [&](ncclResult_t r, const char *what) {
+    if (r != ncclSuccess) throw Error(QSIM_ENCCL, std::string(what) + ": " + ncclGetErrorString(r));
+  };
+  if (use_basis) {
+    // header lower -> upper: basis used, T, terms of the upper's share of the basis rows
+    int64_t hdr[4] = {0, 0, 0, 0};
+    std::vector<uint32_t> off_lo, src_lo, off_hi, src_hi;
+    std::vector<double> coef_lo, coef_hi;
+    int64_t T = 0, th = 0;
+    if (h == 1 && basis_ok) {
+      T = basis_T_;
+      th = T / 2;  // the lower rank contracts basis rows [0, th), the upper one [th, T)
+      off_lo.assign((size_t)th + 1, 0);
+      off_hi.assign((size_t)(T - th) + 1, 0);
+      for (const BasisEntry &x : basis_entries_) (x.t < th ? off_lo[x.t + 1] : off_hi[x.t - th + 1])++;
+      for (int64_t t = 0; t < th; ++t) off_lo[t + 1] += off_lo[t];
+      for (int64_t t = 0; t < T - th; ++t) off_hi[t + 1] += off_hi[t];
+      src_lo.resize(off_lo.back());
+      coef_lo.resize(2 * (size_t)off_lo.back());
+      src_hi.resize(off_hi.back());
+      coef_hi.resize(2 * (size_t)off_hi.back());
+      std::vector<uint32_t> plo(off_lo.begin(), off_lo.end() - 1), phi(off_hi.begin(), off_hi.end() - 1);
+      for (const BasisEntry &x : basis_entries_) {
+        const bool lw = x.t < th;
+        const uint32_t q = lw ? plo[x.t]++ : phi[x.t - th]++;
+        (lw ? src_lo : src_hi)[q] = x.row;
+        (lw ? coef_lo : coef_hi)[2 * q] = x.cr;
+        (lw ? coef_lo : coef_hi)[2 * q + 1] = x.ci;
+      }
+      hdr[0] = 1;
+      hdr[1] = T;
+      hdr[2] = (int64_t)off_hi.back();
+    }
+    basis_hdr_.reserve(32);
+    if (h == 1) check(cudaMemcpyAsync(basis_hdr_.ptr, hdr, 32, cudaMemcpyHostToDevice, stream_), "pair header");
+    nccl_ok(h == 1 ? ncclSend(basis_hdr_.ptr, 4, ncclInt64, rank_ ^ 1, comm_, stream_)
+                   : ncclRecv(basis_hdr_.ptr, 4, ncclInt64, rank_ ^ 1, comm_, stream_),
+            "pair header");
+    if (h == 0) {
+      check(cudaMemcpyAsync(hdr, basis_hdr_.ptr, 32, cudaMemcpyDeviceToHost, stream_), "pair header");
+      check(cudaStreamSynchronize(stream_), "pair header");
+      T = hdr[1];
+      th = T / 2;
+    }
+    if (hdr[0] == 1) {
+      const int64_t nnz_hi = hdr[2];
+      // the lower rank: its CSR of [0, th) local, the upper's sent; the upper rank: all H V rows sent
+      DevBuf &hv = h == 0 ? U_ : Q;  // the (H V) rows of the pair range on each rank
+      if (h == 1) Q.reserve((size_t)plen * (size_t)nu * amp_);
+      if (h == 0) Q.reserve((size_t)(T - th) * (size_t)nl * amp_);
+      const int64_t Tm = h == 0 ? T - th : th;
+      basis_off_.reserve((size_t)(Tm + 1) * 4);
+      basis_src_.reserve((size_t)std::max<int64_t>(1, h == 0 ? nnz_hi : (int64_t)src_lo.size()) * 4);
+      basis_coef_.reserve((size_t)std::max<int64_t>(1, h == 0 ? nnz_hi : (int64_t)src_lo.size()) * 16);
+      if (h == 1) {
+        check(cudaMemcpyAsync(basis_off_.ptr, off_lo.data(), off_lo.size() * 4, cudaMemcpyHostToDevice, stream_), "csr");
+        check(cudaMemcpyAsync(basis_src_.ptr, src_lo.data(), src_lo.size() * 4, cudaMemcpyHostToDevice, stream_), "csr");
+        check(cudaMemcpyAsync(basis_coef_.ptr, coef_lo.data(), coef_lo.size() * 8, cudaMemcpyHostToDevice, stream_),
+              "csr");
+        basis_xoff_.reserve(off_hi.size() * 4);
+        basis_xsrc_.reserve(std::max<size_t>(1, src_hi.size()) * 4);
+        basis_xcoef_.reserve(std::max<size_t>(1, src_hi.size()) * 16);
+        check(cudaMemcpyAsync(basis_xoff_.ptr, off_hi.data(), off_hi.size() * 4, cudaMemcpyHostToDevice, stream_), "csr");
+        check(cudaMemcpyAsync(basis_xsrc_.ptr, src_hi.data(), src_hi.size() * 4, cudaMemcpyHostToDevice, stream_), "csr");
+        check(cudaMemcpyAsync(basis_xcoef_.ptr, coef_hi.data(), coef_hi.size() * 8, cudaMemcpyHostToDevice, stream_),
+              "csr");
+      }
+      ncclGroupStart();
+      if (h == 1) {
+        nccl_ok(ncclSend((const char *)P.ptr + (size_t)th * (size_t)nl * amp_, (size_t)(T - th) * (size_t)nl * 2, dt,
+                         rank_ ^ 1, comm_, stream_), "basis rows");
+        nccl_ok(ncclSend(basis_xoff_.ptr, (size_t)(T - th) + 1, ncclUint32, rank_ ^ 1, comm_, stream_), "basis csr");
+        if (nnz_hi) {
+          nccl_ok(ncclSend(basis_xsrc_.ptr, (size_t)nnz_hi, ncclUint32, rank_ ^ 1, comm_, stream_), "basis csr");
+          nccl_ok(ncclSend(basis_xcoef_.ptr, 2 * (size_t)nnz_hi, ncclDouble, rank_ ^ 1, comm_, stream_), "basis csr");
+        }
+        nccl_ok(ncclRecv(hv.ptr, (size_t)plen * (size_t)nu * 2, dt, rank_ ^ 1, comm_, stream_), "H V rows");
+      } else {
+        nccl_ok(ncclSend(U_.ptr, (size_t)plen * (size_t)nu * 2, dt, rank_ ^ 1, comm_, stream_), "H V rows");
+        nccl_ok(ncclRecv(Q.ptr, (size_t)(T - th) * (size_t)nl * 2, dt, rank_ ^ 1, comm_, stream_), "basis rows");
+        nccl_ok(ncclRecv(basis_off_.ptr, (size_t)(T - th) + 1, ncclUint32, rank_ ^ 1, comm_, stream_), "basis csr");
+        if (nnz_hi) {
+          nccl_ok(ncclRecv(basis_src_.ptr, (size_t)nnz_hi, ncclUint32, rank_ ^ 1, comm_, stream_), "basis csr");
+          nccl_ok(ncclRecv(basis_coef_.ptr, 2 * (size_t)nnz_hi, ncclDouble, rank_ ^ 1, comm_, stream_), "basis csr");
+        }
+      }
+      nccl_ok(ncclGroupEnd(), "pair basis exchange");
+      // U' of this rank's basis rows in the idle state buffer, then the GEMM over them
+      const size_t ub = (size_t)Tm * (size_t)nu * amp_;
+      DevBuf *scratch = (!states_.empty() && states_[0]->bytes >= ub) ? states_[0] : &tmp_;
+      if (scratch == &tmp_) tmp_.reserve(ub);
+      check(launch_combine_rows(hv.ptr, nu, basis_off_.as<uint32_t>(), basis_src_.as<uint32_t>(), basis_coef_.ptr, Tm,
+                                scratch->ptr, c128_, stream_),
+            "combine rows launch");
+      st_.kernel_launches++;
+      check(cudaStreamSynchronize(stream_), "pair basis");  // host CSR temporaries
+      const void *brows = h == 0 ? Q.ptr : P.ptr;  // the upper received rows [th, T); the lower keeps [0, th)
+      gemm(scratch->ptr, brows, Tm, nu, nl, A_acc_.as<double>());
+      st_.branches_evolved += K;
+      check(cudaGetLastError(), "evolve");
+      reduced_ = false;
+      return true;
+    }
+  }
   ncclGroupStart();
   ncclResult_t r1s = ncclSend((const char *)P.ptr + (size_t)(p0 - lo) * (size_t)nh * amp_, (size_t)K * (size_t)nh * 2,
                               dt, rank_ ^ 1, comm_, stream_);

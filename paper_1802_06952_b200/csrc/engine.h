@@ -251,7 +251,8 @@ class Engine {
   };
   struct BasisAbort {};
   bool basis_enabled_ = !(std::getenv("QSIM_FRAME_BASIS") && std::getenv("QSIM_FRAME_BASIS")[0] == '0');
-  int shared_basis_max_ = std::getenv("QSIM_SHARED_BASIS_MAX") ? std::atoi(std::getenv("QSIM_SHARED_BASIS_MAX")) : 2;
+  // shared basis for up to this many ranks (0: off; half pairs with a split basis measured faster at N = 2)
+  int shared_basis_max_ = std::getenv("QSIM_SHARED_BASIS_MAX") ? std::atoi(std::getenv("QSIM_SHARED_BASIS_MAX")) : 0;
   bool basis_on_ = false;
   DevBuf *basis_rows_ = nullptr;
   int64_t basis_cap_ = 0, basis_T_ = 0;
@@ -259,6 +260,7 @@ class Engine {
   int basis_points_ = 0;
   std::vector<BasisEntry> basis_entries_;
   DevBuf basis_off_, basis_src_, basis_coef_;
+  DevBuf basis_xoff_, basis_xsrc_, basis_xcoef_, basis_hdr_;  // half pairs: the partner's share
   // frame gathers through pre-gathered rows of the distinct flips (QSIM_FLIP_ROWS=0: scattered, A/B)
   bool flip_rows_ = !(std::getenv("QSIM_FLIP_ROWS") && std::getenv("QSIM_FLIP_ROWS")[0] == '0');
   DevBuf flip_rows_buf_, flip_idx_buf_;
