@@ -125,6 +125,11 @@ Engine::Engine(qsim_precision prec, int device) : prec_(prec), device_(device) {
 }
 
 Engine::~Engine() {
+  for (auto &s : staging_) {
+    if (s.ev) cudaEventSynchronize(s.ev), cudaEventDestroy(s.ev);
+    if (s.host) cudaFreeHost(s.host);
+  }
+  staging_.clear();
   if (inited_) {
     cudaSetDevice(device_);
     cudaStreamSynchronize(stream_);
@@ -143,6 +148,37 @@ Engine::~Engine() {
     if (comm_) ncclCommDestroy(comm_);
     if (own_stream_) cudaStreamDestroy(own_stream_);
   }
+}
+
+void Engine::upload_async(void *dst, const void *src, size_t bytes) {
+  if (!bytes) return;
+  Staging *slot = nullptr;
+  for (auto &s : staging_)
+    if (!s.pending || cudaEventQuery(s.ev) == cudaSuccess) {
+      slot = &s;
+      break;
+    }
+  if (!slot) {
+    if (staging_.size() < 8) {
+      staging_.emplace_back();
+      slot = &staging_.back();
+      check(cudaEventCreateWithFlags(&slot->ev, cudaEventDisableTiming), "cudaEventCreate");
+    } else {
+      slot = &staging_.front();
+      check(cudaEventSynchronize(slot->ev), "staging wait");
+    }
+  }
+  if (slot->cap < bytes) {
+    if (slot->host) cudaFreeHost(slot->host);
+    slot->host = nullptr;
+    slot->cap = 0;
+    check(cudaMallocHost(&slot->host, bytes), "cudaMallocHost");
+    slot->cap = bytes;
+  }
+  std::memcpy(slot->host, src, bytes);
+  check(cudaMemcpyAsync(dst, slot->host, bytes, cudaMemcpyHostToDevice, stream_), "upload");
+  check(cudaEventRecord(slot->ev, stream_), "cudaEventRecord");
+  slot->pending = true;
 }
 
 void Engine::ensure_device() {
@@ -1726,10 +1762,9 @@ void Engine::evolve_range(uint64_t b0, uint64_t b1) {
       basis_off_.reserve(off.size() * 4);
       basis_src_.reserve(src.size() * 4);
       basis_coef_.reserve(coef.size() * 8);
-      check(cudaMemcpyAsync(basis_off_.ptr, off.data(), off.size() * 4, cudaMemcpyHostToDevice, stream_), "basis off");
-      check(cudaMemcpyAsync(basis_src_.ptr, src.data(), src.size() * 4, cudaMemcpyHostToDevice, stream_), "basis src");
-      check(cudaMemcpyAsync(basis_coef_.ptr, coef.data(), coef.size() * 8, cudaMemcpyHostToDevice, stream_),
-            "basis coef");
+      upload_async(basis_off_.ptr, off.data(), off.size() * 4);
+      upload_async(basis_src_.ptr, src.data(), src.size() * 4);
+      upload_async(basis_coef_.ptr, coef.data(), coef.size() * 8);
       const size_t lb = (size_t)K * (size_t)nl * amp_;
       DevBuf *scratch = (!states_.empty() && states_[0]->bytes >= lb) ? states_[0] : &tmp_;
       if (scratch == &tmp_) tmp_.reserve(lb);
@@ -1737,7 +1772,6 @@ void Engine::evolve_range(uint64_t b0, uint64_t b1) {
                                 scratch->ptr, c128_, stream_),
             "combine rows launch");
       st_.kernel_launches++;
-      check(cudaStreamSynchronize(stream_), "basis upload");
       gemm(U_.ptr, scratch->ptr, K, nu, nl, A_acc_.as<double>());
       st_.branches_evolved += e - s;
       s = e;
@@ -1768,10 +1802,9 @@ void Engine::evolve_range(uint64_t b0, uint64_t b1) {
       basis_off_.reserve(off.size() * 4);
       basis_src_.reserve(src.size() * 4);
       basis_coef_.reserve(coef.size() * 8);
-      check(cudaMemcpyAsync(basis_off_.ptr, off.data(), off.size() * 4, cudaMemcpyHostToDevice, stream_), "basis off");
-      check(cudaMemcpyAsync(basis_src_.ptr, src.data(), src.size() * 4, cudaMemcpyHostToDevice, stream_), "basis src");
-      check(cudaMemcpyAsync(basis_coef_.ptr, coef.data(), coef.size() * 8, cudaMemcpyHostToDevice, stream_),
-            "basis coef");
+      upload_async(basis_off_.ptr, off.data(), off.size() * 4);
+      upload_async(basis_src_.ptr, src.data(), src.size() * 4);
+      upload_async(basis_coef_.ptr, coef.data(), coef.size() * 8);
       // U' in the (now idle) state buffer of the lower half when it is large enough
       const size_t ub = (size_t)T * (size_t)nu * amp_;
       DevBuf *scratch = (!states_.empty() && states_[0]->bytes >= ub) ? states_[0] : &tmp_;
@@ -1780,7 +1813,6 @@ void Engine::evolve_range(uint64_t b0, uint64_t b1) {
                                 scratch->ptr, c128_, stream_),
             "combine rows launch");
       st_.kernel_launches++;
-      check(cudaStreamSynchronize(stream_), "basis upload");  // off / src / coef are host temporaries
       gemm(scratch->ptr, (const char *)L_.ptr + (size_t)t0 * (size_t)nl * amp_, T, nu, nl, A_acc_.as<double>());
       st_.branches_evolved += e - s;
       s = e;

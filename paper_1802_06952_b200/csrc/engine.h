@@ -193,6 +193,16 @@ class Engine {
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_sweep_, ev_gemm_;
   std::vector<cudaEvent_t> ev_pool_;
 
+  // small H2D uploads without a stream sync: the data is copied into a pinned staging slot whose copy is
+  // fenced by an event; a slot is reused only once that event completed (the host keeps running ahead)
+  struct Staging {
+    void *host = nullptr;
+    size_t cap = 0;
+    cudaEvent_t ev = nullptr;
+    bool pending = false;
+  };
+  std::vector<Staging> staging_;
+  void upload_async(void *dst, const void *src, size_t bytes);
   void ensure_device();
   void check(cudaError_t e, const char *what);
   void compile_plans(HalfExec &he);

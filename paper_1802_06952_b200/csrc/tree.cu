@@ -1060,13 +1060,11 @@ bool Engine::run_tree_frames(int half, const TreeVariant &v, const std::vector<i
       if (use_rows) {
         flip_rows_buf_.reserve(rows_bytes);
         flip_idx_buf_.reserve(flips.size() * 8);
-        check(cudaMemcpyAsync(flip_idx_buf_.ptr, flips.data(), flips.size() * 8, cudaMemcpyHostToDevice, stream_),
-              "upload flips");
+        upload_async(flip_idx_buf_.ptr, flips.data(), flips.size() * 8);
         check(launch_flip_rows(states_[raw]->ptr, dS, nS, flip_idx_buf_.as<uint64_t>(), (int64_t)flips.size(),
                                flip_rows_buf_.ptr, c128_, stream_),
               "flip rows launch");
         st_.kernel_launches++;
-        check(cudaStreamSynchronize(stream_), "flip rows");  // `flips` is a host temporary
       }
       const DiagDev pend = to_dev(tail);
       std::unordered_map<std::array<uint64_t, 4>, uint32_t, KeyHash4> bidx;  // frame -> basis row
