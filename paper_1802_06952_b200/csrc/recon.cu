@@ -816,8 +816,9 @@ static cudaError_t launch_gemm3m(const void *U, const void *L, int64_t K, int64_
 template <typename R>
 static cudaError_t launch_gemm3m_cfg(const void *U, const void *L, int64_t K, int64_t M, int64_t N, double *A,
                                      cudaStream_t s) {
-  // QSIM_GEMM_CFG (A/B): 0 = 64x64 tile, 32x16 warps, 1 CTA/SM, K step 16, 3 stages; 1 = K step 32
-  static const int cfg = std::getenv("QSIM_GEMM_CFG") ? std::atoi(std::getenv("QSIM_GEMM_CFG")) : 0;
+  // QSIM_GEMM_CFG (A/B): 1 (default) = 64x64 tile, 32x16 warps, 1 CTA/SM, K step 32, 3 stages (202 KB of
+  // shared memory); 0 = K step 16 (whole C5 job: 2.21 vs 2.28 s of GEMM)
+  static const int cfg = std::getenv("QSIM_GEMM_CFG") ? std::atoi(std::getenv("QSIM_GEMM_CFG")) : 1;
   // (measured on B200, K = 16384, M = N = 8192: 64x32 / 32x64 tiles with 2 CTAs per SM 28.3 / 28.2, K steps of
   // 32 with 2 / 3 stages 29.3 / 29.4, 4 stages of 16 29.0, this one 29.0 TF/s executed: the DMMA pipe, not
   // occupancy or the pipeline depth, is the limit; profiles/r02/r02x_gemm_configs.txt)
